@@ -1,0 +1,209 @@
+/*
+ * alnnls.h — C ABI of the B200-native anti-lopsided NNLS solver.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   antilop::solve_nnls  (/root/reference/proj/include/antilop/nnls.hpp:129-144)
+ *   antilop::solve_nqp   (/root/reference/proj/include/antilop/nqp.hpp:215-339)
+ *   antilop::gram / transpose_matvec / masked_matvec / matvec
+ *                        (/root/reference/proj/include/antilop/linalg.hpp:160-219)
+ *   antilop::rescale / unscale (/root/reference/proj/include/antilop/nnls.hpp:41-96)
+ * The reference is a header-only C++ library with no FFI; its public C++ API is
+ * re-declared on top of this ABI by include/antilop/*.hpp.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Matrices are column-major fp64, leading
+ *    dimension = rows unless an explicit ld is passed (reference linalg.hpp:116).
+ *  - Every entry point returns an alnnls_status. Exceptions never cross the ABI:
+ *    EINVAL  <-> std::invalid_argument   (reference detail::require, linalg.hpp:22-24)
+ *    ERANGE  <-> std::out_of_range       (linalg.hpp:199)
+ *    ENUMERIC<-> antilop::NumericFailure (nqp.hpp:136-145); the trace up to the
+ *                failing iteration stays retrievable with alnnls_get_trace.
+ *    ECUDA / ENOMEM / ENCCL / ENODEV: device-side failures (no reference analogue).
+ *  - A context (alnnls_ctx) owns device memory, streams and events for one GPU.
+ *    It is single-threaded; independent contexts may run concurrently.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point fails with ENODEV.
+ */
+#ifndef ALNNLS_H
+#define ALNNLS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ALNNLS_ABI_VERSION 1
+
+typedef enum alnnls_status {
+  ALNNLS_OK = 0,
+  ALNNLS_EINVAL = 1,
+  ALNNLS_ENUMERIC = 2,
+  ALNNLS_ECUDA = 3,
+  ALNNLS_ENOMEM = 4,
+  ALNNLS_ENCCL = 5,
+  ALNNLS_ERANGE = 6,
+  ALNNLS_ECAPACITY = 7, /* caller buffer too small */
+  ALNNLS_ENODEV = 8
+} alnnls_status;
+
+/* Same order as antilop::Termination (nqp.hpp:47-54). */
+typedef enum alnnls_termination {
+  ALNNLS_EMPTY_PASSIVE_SET = 0,
+  ALNNLS_GRADIENT_BELOW_EPSILON = 1,
+  ALNNLS_MAX_ITERS = 2,
+  ALNNLS_TIME_CAP = 3,
+  ALNNLS_STALLED = 4,
+  ALNNLS_ZERO_CURVATURE = 5
+} alnnls_termination;
+
+/* Numerics profile. EXACT replicates the reference operation sequence bit for
+ * bit (rounded product then rounded sum, one ascending chain per output). */
+typedef enum alnnls_profile { ALNNLS_PROFILE_EXACT = 0, ALNNLS_PROFILE_FAST = 1 } alnnls_profile;
+
+/* antilop::SolverConfig (nqp.hpp:71-99) as POD. Unset optionals have has_* = 0.
+ * Defaults are resolved against the retained dimension m exactly like
+ * resolve_epsilon / resolve_max_iters (nqp.hpp:84-98). */
+typedef struct alnnls_config {
+  int32_t has_epsilon;
+  double epsilon;
+  int32_t has_max_iters;
+  uint64_t max_iters;
+  int32_t has_time_cap;
+  double time_cap_s;
+  uint64_t stall_window; /* reference default 50 */
+  uint64_t trace_every;  /* reference default 1; 0 is treated as 1 (nqp.hpp:222) */
+  int32_t profile;       /* alnnls_profile */
+  int32_t record_multiplies; /* fill SolveStats::multiplies_per_iter */
+} alnnls_config;
+
+/* antilop::IterRecord (nqp.hpp:103-110). has_alpha = 0 on the final record. */
+typedef struct alnnls_iter_record {
+  uint64_t iter;
+  double f;
+  double grad_bar_sq;
+  uint64_t passive_count;
+  double elapsed_s;
+  double alpha;
+  int64_t has_alpha;
+} alnnls_iter_record;
+
+/* Scalars of one solve (NnlsResult / SolveResult without the arrays). */
+typedef struct alnnls_summary {
+  int32_t termination;   /* alnnls_termination */
+  int32_t numeric_failure; /* 1 when the solve ended in NumericFailure */
+  uint64_t iterations;   /* SolveResult::iterations() = last record's iter */
+  uint64_t trace_len;
+  uint64_t mult_len;
+  uint64_t n;            /* original dimension (NNLS) or m (NQP) */
+  uint64_t m;            /* retained dimension */
+  uint64_t n_dropped;
+  double min_iterate;
+  double residual_sq;    /* NNLS only: ||Ax-b||^2 recomputed from A, b (nnls.hpp:142) */
+  double f_final;        /* last trace record's f */
+  double gbs_final;      /* last trace record's grad_bar_sq */
+  uint64_t multiplies_total; /* sum of multiplies_per_iter (algorithmic GEMV work) */
+  /* device timings (CUDA events around each phase; seconds) */
+  double t_setup_s;
+  double t_loop_s;
+  double t_finish_s;
+  double t_total_s;
+} alnnls_summary;
+
+/* Per-column result of a batched solve (one NnlsResult without arrays). */
+typedef struct alnnls_column_result {
+  int32_t termination;
+  int32_t numeric_failure;
+  uint64_t iterations;
+  double residual_sq;
+  double f_final;
+  double gbs_final;
+  uint64_t multiplies_total;
+} alnnls_column_result;
+
+typedef struct alnnls_ctx alnnls_ctx;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+int alnnls_abi_version(void);
+/* Fills a config with the reference defaults (SolverConfig{}). */
+void alnnls_config_default(alnnls_config* cfg);
+/* Creates a context on CUDA device `device`; ENODEV without an sm_100 GPU. */
+int alnnls_create(alnnls_ctx** out, int device);
+void alnnls_destroy(alnnls_ctx* ctx);
+/* Message of the last failure on this context (never NULL). */
+const char* alnnls_last_error(const alnnls_ctx* ctx);
+/* Device properties seen by the context. */
+int alnnls_device_info(alnnls_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- hot path: host buffers (H2D/D2H inside) ---------------------------- */
+/* solve_nnls(A, b, cfg) — nnls.hpp:129-144. A is d x n column-major (lda = d). */
+int alnnls_solve_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A,
+                      const double* b, const alnnls_config* cfg, alnnls_summary* out);
+/* solve_nqp(p, cfg, start) — nqp.hpp:215-339. Q is m x m column-major and must be
+ * exactly symmetric (nqp.hpp:37-41); start may be NULL. */
+int alnnls_solve_nqp(alnnls_ctx* ctx, uint64_t m, const double* Q, const double* q,
+                     const double* start, const alnnls_config* cfg, alnnls_summary* out);
+
+/* ---- hot path: device-resident inputs ---------------------------------- */
+int alnnls_solve_nnls_device(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA,
+                             uint64_t lda, const double* db, const alnnls_config* cfg,
+                             alnnls_summary* out);
+int alnnls_solve_nqp_device(alnnls_ctx* ctx, uint64_t m, const double* dQ, uint64_t ldq,
+                            const double* dq, const double* dstart,
+                            const alnnls_config* cfg, alnnls_summary* out);
+
+/* ---- results of the last solve on ctx ----------------------------------- */
+/* NNLS: x has n entries (unscaled, dropped columns 0). NQP: x has m entries. */
+int alnnls_get_x(alnnls_ctx* ctx, double* x, uint64_t len);
+/* Rescaled-space solution y (m) and maintained gradient final_grad (m). */
+int alnnls_get_inner_x(alnnls_ctx* ctx, double* y, uint64_t len);
+int alnnls_get_final_grad(alnnls_ctx* ctx, double* g, uint64_t len);
+int alnnls_get_trace(alnnls_ctx* ctx, alnnls_iter_record* rec, uint64_t cap);
+int alnnls_get_multiplies(alnnls_ctx* ctx, uint64_t* mults, uint64_t cap);
+/* rescale bookkeeping of the last NNLS solve/setup (nnls.hpp:32-37). */
+int alnnls_get_scale(alnnls_ctx* ctx, double* scale, uint64_t cap);
+int alnnls_get_retained(alnnls_ctx* ctx, uint64_t* idx, uint64_t cap);
+int alnnls_get_dropped(alnnls_ctx* ctx, uint64_t* idx, uint64_t cap);
+
+/* ---- setup kernels (K1-K3) and dense helpers, for parity and reuse ------- */
+/* rescale(gram(A), -A^T b) on device; afterwards Q (m x m), q (m), scale,
+ * retained and dropped are retrievable. out->m / n_dropped are set. */
+int alnnls_setup(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, const double* b,
+                 alnnls_summary* out);
+int alnnls_get_Q(alnnls_ctx* ctx, double* Q, uint64_t cap);
+int alnnls_get_q(alnnls_ctx* ctx, double* q, uint64_t cap);
+/* rescale(H, h) — nnls.hpp:41-83, host H (n x n) and h (n). EINVAL on an
+ * asymmetric H or a negative diagonal, like the reference. */
+int alnnls_rescale(alnnls_ctx* ctx, uint64_t n, const double* H, const double* h,
+                   alnnls_summary* out);
+/* gram(A) — linalg.hpp:160-174: H (n x n) = A^T A, exactly symmetric. */
+int alnnls_gram(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, double* H);
+/* transpose_matvec(A, v) — linalg.hpp:209-219. */
+int alnnls_transpose_matvec(alnnls_ctx* ctx, uint64_t rows, uint64_t cols, const double* M,
+                            const double* v, double* y);
+/* matvec(M, v) — linalg.hpp:179-188. */
+int alnnls_matvec(alnnls_ctx* ctx, uint64_t rows, uint64_t cols, const double* M,
+                  const double* v, double* y);
+/* masked_matvec(M, v, mask) — linalg.hpp:193-206. ERANGE on an index >= cols.
+ * *multiply_count (if non-NULL) is incremented by rows*mask_len. */
+int alnnls_masked_matvec(alnnls_ctx* ctx, uint64_t rows, uint64_t cols, const double* M,
+                         const double* v, const uint64_t* mask, uint64_t mask_len, double* y,
+                         uint64_t* multiply_count);
+
+/* ---- batched multi-RHS (NMF H-update; one solve_nnls per column of B) ---- */
+/* X (n x nrhs, column-major) and per-column results are written by the call.
+ * Column j is bitwise equal to solve_nnls(A, B[:, j], cfg) under EXACT. */
+int alnnls_solve_nnls_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A,
+                              uint64_t nrhs, const double* B, const alnnls_config* cfg,
+                              double* X, alnnls_column_result* cols, alnnls_summary* out);
+int alnnls_solve_nnls_batched_device(alnnls_ctx* ctx, uint64_t d, uint64_t n,
+                                     const double* dA, uint64_t nrhs, const double* dB,
+                                     const alnnls_config* cfg, double* dX,
+                                     alnnls_column_result* cols, alnnls_summary* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ALNNLS_H */

@@ -1,0 +1,349 @@
+"""Python mirror of the reference's public solver API, backed by the C ABI.
+
+Same names, argument meaning and error behaviour as the reference headers
+(/root/reference/proj/include/antilop/{linalg,nqp,nnls}.hpp):
+
+    solve_nnls(A, b, config)            nnls.hpp:129-144
+    solve_nqp(Q, q, config, start)      nqp.hpp:215-339
+    gram / matvec / masked_matvec / transpose_matvec   linalg.hpp:160-219
+    rescale(H, h)                       nnls.hpp:41-83
+
+Errors: std::invalid_argument -> ValueError, std::out_of_range -> IndexError,
+antilop::NumericFailure -> NumericFailure (carries .trace). All compute runs on
+the GPU through lib/libalnnls.so; there is no CPU fallback.
+"""
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import abi
+from ._native import load
+
+TERMINATIONS = abi.TERMINATIONS
+
+
+class NumericFailure(RuntimeError):
+    """antilop::NumericFailure (nqp.hpp:136-145)."""
+
+    def __init__(self, what, trace):
+        super().__init__(what)
+        self.trace = trace
+
+
+@dataclass
+class SolverConfig:
+    """antilop::SolverConfig (nqp.hpp:71-99) + the numerics profile extension."""
+    epsilon: Optional[float] = None
+    max_iters: Optional[int] = None
+    time_cap: Optional[float] = None  # seconds
+    stall_window: int = 50
+    trace_every: int = 1
+    nesterov_restart: bool = False    # accelerated baseline only (unused here)
+    active_set_tol: Optional[float] = None  # active-set baseline only (unused here)
+    profile: int = abi.PROFILE_EXACT
+
+    def to_abi(self, record_multiplies=True):
+        return abi.make_config(self.epsilon, self.max_iters, self.time_cap, self.stall_window,
+                               self.trace_every, self.profile, record_multiplies)
+
+    def resolve_epsilon(self, n):
+        if self.epsilon is not None:
+            if not self.epsilon > 0.0:
+                raise ValueError("SolverConfig: epsilon must be > 0")
+            return self.epsilon
+        return 1e-10 * n
+
+    def resolve_max_iters(self, n):
+        if self.max_iters is not None:
+            if self.max_iters < 1:
+                raise ValueError("SolverConfig: max_iters must be >= 1")
+            return self.max_iters
+        return 5 * n
+
+
+@dataclass
+class IterRecord:
+    iter: int
+    f: float
+    grad_bar_sq: float
+    passive_count: int
+    elapsed: float
+    alpha: Optional[float]
+
+
+@dataclass
+class SolveResult:
+    x: np.ndarray
+    trace: List[IterRecord]
+    termination: str
+    final_grad: np.ndarray
+    min_iterate: float
+    multiplies_per_iter: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    timings: dict = field(default_factory=dict)
+
+    def iterations(self):
+        return self.trace[-1].iter if self.trace else 0
+
+
+@dataclass
+class NnlsResult:
+    x: np.ndarray
+    residual_sq: float
+    inner: SolveResult
+    dropped_columns: List[int]
+    timings: dict = field(default_factory=dict)
+
+
+def _f64(a, name):
+    a = np.asarray(a, dtype=np.float64)
+    return a
+
+
+def _fortran(M):
+    M = np.asarray(M, dtype=np.float64)
+    if M.ndim != 2:
+        raise ValueError("DenseMatrix: expected a 2-D array")
+    return np.asfortranarray(M)
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Solver:
+    """One alnnls_ctx (device memory, stream, events) on one GPU.
+
+    Single-threaded like the C context; use one Solver per thread/device."""
+
+    def __init__(self, device=0):
+        self.lib = load()
+        self.ctx = C.c_void_p()
+        st = self.lib.alnnls_create(C.byref(self.ctx), device)
+        if st != abi.OK:
+            raise RuntimeError(f"alnnls_create(device={device}) failed: {abi.STATUS_NAMES[st]} "
+                               "(no sm_100 GPU visible; there is no CPU fallback)")
+        self.device = device
+
+    def close(self):
+        if self.ctx:
+            self.lib.alnnls_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- error mapping ------------------------------------------------------------
+    def _raise(self, st, trace=None):
+        msg = self.lib.alnnls_last_error(self.ctx).decode()
+        if st == abi.EINVAL:
+            raise ValueError(msg)
+        if st == abi.ERANGE:
+            raise IndexError(msg)
+        if st == abi.ENUMERIC:
+            raise NumericFailure(msg, trace if trace is not None else self._trace())
+        raise RuntimeError(f"{abi.STATUS_NAMES[st]}: {msg}")
+
+    def _check(self, st):
+        if st != abi.OK:
+            self._raise(st)
+
+    def _vec(self, fn, n, dtype=np.float64):
+        out = np.zeros(max(1, n), dtype=dtype)
+        self._check(fn(self.ctx, _ptr(out), n))
+        return out[:n]
+
+    def _trace(self):
+        s = self._summary
+        buf = (abi.IterRecord * max(1, s.trace_len))()
+        self._check(self.lib.alnnls_get_trace(self.ctx, C.cast(buf, C.c_void_p), s.trace_len))
+        return [IterRecord(r.iter, r.f, r.grad_bar_sq, r.passive_count, r.elapsed_s,
+                           r.alpha if r.has_alpha else None) for r in buf[:s.trace_len]]
+
+    def _solve_result(self, nnls):
+        s = self._summary
+        m = s.m
+        if nnls:
+            x_inner = self._vec(self.lib.alnnls_get_inner_x, m)
+        else:
+            x_inner = self._vec(self.lib.alnnls_get_x, m)
+        mults = self._vec(self.lib.alnnls_get_multiplies, s.mult_len, np.uint64)
+        return SolveResult(
+            x=x_inner,
+            trace=self._trace(),
+            termination=TERMINATIONS[s.termination],
+            final_grad=self._vec(self.lib.alnnls_get_final_grad, m),
+            min_iterate=s.min_iterate,
+            multiplies_per_iter=mults,
+            timings={"loop_s": s.t_loop_s},
+        )
+
+    # ---- solvers ------------------------------------------------------------------
+    def solve_nnls(self, A, b, config: SolverConfig = SolverConfig()):
+        A = _fortran(A)
+        b = np.ascontiguousarray(_f64(b, "b")).reshape(-1)
+        if A.shape[0] != b.shape[0]:
+            raise ValueError("solve_nnls: A and b dimension mismatch")
+        d, n = A.shape
+        self._summary = abi.Summary()
+        cfg = config.to_abi()
+        st = self.lib.alnnls_solve_nnls(self.ctx, d, n, _ptr(A), _ptr(b), C.byref(cfg),
+                                        C.byref(self._summary))
+        if st != abi.OK:
+            self._raise(st)
+        return self._nnls_result()
+
+    def solve_nnls_device(self, A_ptr, lda, d, n, b_ptr, config: SolverConfig = SolverConfig(),
+                          fetch=True):
+        """Inputs already in HBM (e.g. torch tensors' data_ptr()); A column-major."""
+        self._summary = abi.Summary()
+        cfg = config.to_abi()
+        st = self.lib.alnnls_solve_nnls_device(self.ctx, d, n, C.c_void_p(A_ptr), lda,
+                                               C.c_void_p(b_ptr), C.byref(cfg),
+                                               C.byref(self._summary))
+        if st != abi.OK:
+            self._raise(st)
+        return self._nnls_result() if fetch else self._summary
+
+    def _nnls_result(self):
+        s = self._summary
+        x = self._vec(self.lib.alnnls_get_x, s.n)
+        dropped = self._vec(self.lib.alnnls_get_dropped, s.n_dropped, np.uint64)
+        inner = self._solve_result(True)
+        return NnlsResult(x=x, residual_sq=s.residual_sq, inner=inner,
+                          dropped_columns=[int(v) for v in dropped],
+                          timings={"setup_s": s.t_setup_s, "loop_s": s.t_loop_s,
+                                   "finish_s": s.t_finish_s, "total_s": s.t_total_s})
+
+    def solve_nqp(self, Q, q, config: SolverConfig = SolverConfig(), start=None):
+        Q = _fortran(Q)
+        q = np.ascontiguousarray(_f64(q, "q")).reshape(-1)
+        if Q.shape[0] != Q.shape[1]:
+            raise ValueError("NqpProblem: Q must be square")
+        if Q.shape[0] != q.shape[0]:
+            raise ValueError("NqpProblem: Q and q dimension mismatch")
+        m = q.shape[0]
+        sp = None
+        if start is not None:
+            start = np.ascontiguousarray(_f64(start, "start")).reshape(-1)
+            if start.shape[0] != m:
+                raise ValueError("solve_nqp: start dimension mismatch")
+            sp = _ptr(start)
+        self._summary = abi.Summary()
+        cfg = config.to_abi()
+        st = self.lib.alnnls_solve_nqp(self.ctx, m, _ptr(Q), _ptr(q), sp, C.byref(cfg),
+                                       C.byref(self._summary))
+        if st != abi.OK:
+            self._raise(st)
+        return self._solve_result(False)
+
+    # ---- setup and dense kernels ---------------------------------------------------------
+    def setup(self, A, b):
+        """rescale(gram(A), -A^T b) on device -> dict(Q, q, scale, retained, dropped)."""
+        A = _fortran(A)
+        b = np.ascontiguousarray(_f64(b, "b")).reshape(-1)
+        self._summary = abi.Summary()
+        self._check(self.lib.alnnls_setup(self.ctx, A.shape[0], A.shape[1], _ptr(A), _ptr(b),
+                                          C.byref(self._summary)))
+        return self._scaled()
+
+    def rescale(self, H, h):
+        H = _fortran(H)
+        h = np.ascontiguousarray(_f64(h, "h")).reshape(-1)
+        if H.shape[0] != H.shape[1]:
+            raise ValueError("rescale: H must be square")
+        if H.shape[0] != h.shape[0]:
+            raise ValueError("rescale: H and h dimension mismatch")
+        self._summary = abi.Summary()
+        self._check(self.lib.alnnls_rescale(self.ctx, H.shape[0], _ptr(H), _ptr(h),
+                                            C.byref(self._summary)))
+        return self._scaled()
+
+    def _scaled(self):
+        s = self._summary
+        m = s.m
+        Qf = self._vec(self.lib.alnnls_get_Q, m * m)
+        return {
+            "Q": Qf.reshape(m, m, order="F"),
+            "q": self._vec(self.lib.alnnls_get_q, m),
+            "scale": self._vec(self.lib.alnnls_get_scale, m),
+            "retained": self._vec(self.lib.alnnls_get_retained, m, np.uint64),
+            "dropped": self._vec(self.lib.alnnls_get_dropped, s.n_dropped, np.uint64),
+            "t_setup_s": s.t_setup_s,
+        }
+
+    def gram(self, A):
+        A = _fortran(A)
+        d, n = A.shape
+        H = np.zeros(n * n)
+        self._check(self.lib.alnnls_gram(self.ctx, d, n, _ptr(A), _ptr(H)))
+        return H.reshape(n, n, order="F")
+
+    def transpose_matvec(self, M, v):
+        M = _fortran(M)
+        v = np.ascontiguousarray(_f64(v, "v")).reshape(-1)
+        if M.shape[0] != v.shape[0]:
+            raise ValueError("transpose_matvec: dimension mismatch")
+        y = np.zeros(M.shape[1])
+        self._check(self.lib.alnnls_transpose_matvec(self.ctx, M.shape[0], M.shape[1], _ptr(M),
+                                                     _ptr(v), _ptr(y)))
+        return y
+
+    def matvec(self, M, v):
+        M = _fortran(M)
+        v = np.ascontiguousarray(_f64(v, "v")).reshape(-1)
+        if M.shape[1] != v.shape[0]:
+            raise ValueError("matvec: dimension mismatch")
+        y = np.zeros(M.shape[0])
+        self._check(self.lib.alnnls_matvec(self.ctx, M.shape[0], M.shape[1], _ptr(M), _ptr(v),
+                                           _ptr(y)))
+        return y
+
+    def masked_matvec(self, M, v, mask, multiply_count=None):
+        """Returns y (and the incremented count when multiply_count is given)."""
+        M = _fortran(M)
+        v = np.ascontiguousarray(_f64(v, "v")).reshape(-1)
+        if M.shape[1] != v.shape[0]:
+            raise ValueError("masked_matvec: dimension mismatch")
+        mk = np.ascontiguousarray(np.asarray(mask, dtype=np.uint64).reshape(-1))
+        y = np.zeros(M.shape[0])
+        cnt = C.c_uint64(multiply_count or 0)
+        self._check(self.lib.alnnls_masked_matvec(
+            self.ctx, M.shape[0], M.shape[1], _ptr(M), _ptr(v),
+            _ptr(mk) if len(mk) else None, len(mk), _ptr(y), C.byref(cnt)))
+        return (y, cnt.value) if multiply_count is not None else y
+
+
+_default = {}
+
+
+def default_solver(device=0):
+    if device not in _default:
+        _default[device] = Solver(device)
+    return _default[device]
+
+
+def solve_nnls(A, b, config: SolverConfig = SolverConfig()):
+    return default_solver().solve_nnls(A, b, config)
+
+
+def solve_nqp(Q, q, config: SolverConfig = SolverConfig(), start=None):
+    return default_solver().solve_nqp(Q, q, config, start)
+
+
+# Host-side helpers the reference's tests call (nqp.hpp:149-157, :183-207). They are
+# O(n) / O(n^2) checks, not the hot path, and are restated here in numpy.
+def passive_mask(x, grad):
+    x = np.asarray(x, np.float64)
+    grad = np.asarray(grad, np.float64)
+    if x.shape != grad.shape:
+        raise ValueError("passive_mask: length mismatch")
+    return [i for i in range(len(x)) if x[i] > 0.0 or grad[i] < 0.0]
+
+
+def to_string(termination):
+    return termination

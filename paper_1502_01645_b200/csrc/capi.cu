@@ -1,0 +1,795 @@
+// capi.cu — the C ABI (include/alnnls.h): context, device buffers, host-side
+// validation with the reference's error semantics, and the orchestration of
+// the sm_100a kernels for solve_nnls / solve_nqp and the dense helpers.
+//
+// Validation mirrors the reference preconditions (linalg.hpp:22-24, :42-52,
+// :74-85; nqp.hpp:35-41, :84-98, :227-230; nnls.hpp:43-56, :131) so that the
+// same inputs fail with the same category (EINVAL / ERANGE / ENUMERIC).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/alnnls.h"
+#include "kernels.cuh"
+
+using namespace alnnls;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct alnnls_ctx {
+  int device = 0;
+  int sm_count = 0;
+  int cc_major = 0, cc_minor = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  std::string err;
+
+  DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
+  DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
+      hvec, start, bcols, X;
+
+  // last solve
+  bool last_nnls = false;
+  uint64_t last_n = 0, last_m = 0;
+  uint64_t ldq = 0;
+  alnnls_summary last{};
+  std::vector<uint64_t> dropped_h;
+  bool have_setup = false;
+};
+
+namespace {
+
+int set_err(alnnls_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(alnnls_ctx* c, cudaError_t e, const char* where) {
+  const int code = (e == cudaErrorMemoryAllocation) ? ALNNLS_ENOMEM : ALNNLS_ECUDA;
+  return set_err(c, code, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                              \
+  do {                                                        \
+    cudaError_t e__ = (call);                                 \
+    if (e__ != cudaSuccess) return cuda_fail(ctx, e__, #call); \
+  } while (0)
+
+template <class T>
+T* ensure(alnnls_ctx* ctx, DevBuf& b, size_t count, int* st) {
+  const size_t bytes = sizeof(T) * (count + 4);
+  if (b.bytes < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e != cudaSuccess) {
+      *st = cuda_fail(ctx, e, "cudaMalloc");
+      return nullptr;
+    }
+    b.bytes = bytes;
+  }
+  return static_cast<T*>(b.p);
+}
+
+#define ENSURE(T, buf, count)                      \
+  ensure<T>(ctx, ctx->buf, (size_t)(count), &st__); \
+  if (st__ != ALNNLS_OK) return st__
+
+uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+bool all_finite(const double* p, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+struct Resolved {
+  double eps;
+  uint64_t max_iters;
+  uint64_t trace_every;
+};
+
+// SolverConfig::resolve_epsilon / resolve_max_iters (nqp.hpp:84-98).
+int resolve(alnnls_ctx* ctx, const alnnls_config* cfg, uint64_t m, Resolved* r) {
+  if (cfg->has_epsilon) {
+    if (!(cfg->epsilon > 0.0)) return set_err(ctx, ALNNLS_EINVAL, "SolverConfig: epsilon must be > 0");
+    r->eps = cfg->epsilon;
+  } else {
+    r->eps = 1e-10 * (double)m;
+  }
+  if (cfg->has_max_iters) {
+    if (cfg->max_iters < 1) return set_err(ctx, ALNNLS_EINVAL, "SolverConfig: max_iters must be >= 1");
+    r->max_iters = cfg->max_iters;
+  } else {
+    r->max_iters = 5 * m;
+  }
+  r->trace_every = cfg->trace_every > 0 ? cfg->trace_every : 1;
+  if (cfg->profile != ALNNLS_PROFILE_EXACT && cfg->profile != ALNNLS_PROFILE_FAST)
+    return set_err(ctx, ALNNLS_EINVAL, "alnnls_config: unknown profile");
+  return ALNNLS_OK;
+}
+
+int check_ctx(alnnls_ctx* ctx) {
+  if (!ctx) return ALNNLS_EINVAL;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  return ALNNLS_OK;
+}
+
+// ---- the device-resident NQP solve on ctx->Q / ctx->q (already uploaded) ------
+// x0: nullptr -> start at 0 (g = q); otherwise device start vector (validated).
+int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config* cfg,
+            const double* dstart, alnnls_summary* out) {
+  int st__ = ALNNLS_OK;
+  const double* Q = static_cast<const double*>(ctx->Q.p);
+  const double* q = static_cast<const double*>(ctx->q.p);
+  double* x = ENSURE(double, x, m);
+  double* g = ENSURE(double, g, m);
+  double* u = ENSURE(double, u, m);
+  double* gd = ENSURE(double, gd, m);
+  uint32_t* mask = ENSURE(uint32_t, mask, m);
+  double* gP = ENSURE(double, gP, m + 8);
+  uint32_t* chg = ENSURE(uint32_t, chg, m);
+  double* dC = ENSURE(double, dC, m + 8);
+  double* candC = ENSURE(double, candC, m);
+  double* gC = ENSURE(double, gC, m);
+  double* p0 = ENSURE(double, prod0, m + 8);
+  double* p1 = ENSURE(double, prod1, m + 8);
+  double* p2 = ENSURE(double, prod2, m + 8);
+  LoopCtrl* ctrl = ENSURE(LoopCtrl, ctrl, 1);
+  const uint64_t tcap = r.max_iters / r.trace_every + 2;
+  alnnls_iter_record* trace = ENSURE(alnnls_iter_record, trace, tcap);
+  uint64_t mcap = 0;
+  uint64_t* mults = nullptr;
+  if (cfg->record_multiplies) {
+    mcap = r.max_iters + 1;
+    mults = ENSURE(uint64_t, mults, mcap);
+  }
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemsetAsync(gP, 0, sizeof(double) * (m + 8), s));
+  CK(cudaMemsetAsync(dC, 0, sizeof(double) * (m + 8), s));
+  if (!dstart) {
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * m, s));
+    CK(cudaMemcpyAsync(g, q, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+  } else {
+    // g = matvec(Q, start) + q (nqp.hpp:231-233); skipping x_j == 0 columns is exact.
+    CK(cudaMemcpyAsync(x, dstart, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    uint32_t* list = ENSURE(uint32_t, list, m);
+    double* vals = ENSURE(double, vals, m + 8);
+    int* len = ENSURE(int, mscalar, 4);
+    CK(launch_support(x, (int)m, list, vals, len, s));
+    int hlen = 0;
+    CK(cudaMemcpyAsync(&hlen, len, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(launch_masked_gemv(Q, ctx->ldq, (int)m, list, vals, hlen, u, ctx->sm_count, s));
+    CK(launch_add(u, q, g, (int)m, s));
+  }
+  LoopArgs a{};
+  a.Q = Q;
+  a.ldq = ctx->ldq;
+  a.q = q;
+  a.m = (int)m;
+  a.x = x;
+  a.g = g;
+  a.u = u;
+  a.gd = gd;
+  a.mask = mask;
+  a.gP = gP;
+  a.chg = chg;
+  a.dC = dC;
+  a.candC = candC;
+  a.gC = gC;
+  a.prod0 = p0;
+  a.prod1 = p1;
+  a.prod2 = p2;
+  a.eps = r.eps;
+  a.max_iters = r.max_iters;
+  a.has_time_cap = cfg->has_time_cap;
+  a.time_cap_s = cfg->time_cap_s;
+  a.stall_window = cfg->stall_window;
+  a.trace_every = r.trace_every;
+  a.trace = trace;
+  a.trace_cap = tcap;
+  a.mults = mults;
+  a.mults_cap = mcap;
+  a.ctrl = ctrl;
+  a.rows_per_cta = nqp_rows_per_cta((int)m, ctx->sm_count);
+  if (a.rows_per_cta > 480)
+    return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: dimension too large for one GPU row split");
+  const int nctas = (int)((m + a.rows_per_cta - 1) / a.rows_per_cta);
+  CK(cudaEventRecord(ctx->ev[2], s));
+  CK(launch_nqp_loop(a, nctas, s));
+  CK(cudaEventRecord(ctx->ev[3], s));
+  LoopCtrl hc;
+  CK(cudaMemcpyAsync(&hc, ctrl, sizeof(LoopCtrl), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+  out->t_loop_s = ms * 1e-3;
+  out->termination = hc.termination;
+  out->numeric_failure = hc.numeric_failure;
+  out->iterations = hc.iterations;
+  out->trace_len = hc.trace_len;
+  out->mult_len = cfg->record_multiplies ? hc.mult_len : 0;
+  out->multiplies_total = hc.mult_total;
+  out->min_iterate = hc.min_iterate;
+  out->f_final = hc.f_final;
+  out->gbs_final = hc.gbs_final;
+  out->m = m;
+  if (hc.numeric_failure)
+    return set_err(ctx, ALNNLS_ENUMERIC, "solve_nqp: non-finite objective or gradient");
+  return ALNNLS_OK;
+}
+
+// ---- setup on device A (lda) and b: rescale(gram(A), -A^T b) -> ctx->Q, q ----
+int run_setup(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t lda,
+              const double* db, uint64_t* m_out) {
+  int st__ = ALNNLS_OK;
+  cudaStream_t s = ctx->stream;
+  SetupArgs sa{};
+  sa.A = dA;
+  sa.lda = lda;
+  sa.b = db;
+  sa.d = (int)d;
+  sa.n = (int)n;
+  sa.diag = ENSURE(double, diag, n);
+  sa.pos = ENSURE(int, pos, n);
+  sa.scale = ENSURE(double, scale, n);
+  sa.retained = ENSURE(uint32_t, retained, n);
+  sa.m_out = ENSURE(int, mscalar, 4);
+  CK(launch_gram_diag(sa, s));
+  CK(launch_retained(sa, s));
+  int hm = 0;
+  CK(cudaMemcpyAsync(&hm, sa.m_out, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint64_t m = (uint64_t)hm;
+  ctx->ldq = round_up(m > 0 ? m : 1, 32);
+  sa.Q = ENSURE(double, Q, ctx->ldq * (m > 0 ? m : 1));
+  sa.ldq = ctx->ldq;
+  sa.q = ENSURE(double, q, m + 8);
+  if (m > 0) CK(launch_syrk(sa, 1, s));
+  *m_out = m;
+  ctx->have_setup = true;
+  return ALNNLS_OK;
+}
+
+// nnls.hpp:129-144 on device-resident A (lda, 16B-aligned, lda even) and b.
+int run_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t lda,
+             const double* db, const alnnls_config* cfg, alnnls_summary* out) {
+  int st__ = ALNNLS_OK;
+  cudaStream_t s = ctx->stream;
+  alnnls_summary sum{};
+  CK(cudaEventRecord(ctx->ev[0], s));
+  uint64_t m = 0;
+  int rc = run_setup(ctx, d, n, dA, lda, db, &m);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev[1], s));
+  ctx->last_nnls = true;
+  ctx->last_n = n;
+  ctx->last_m = m;
+  double* y = ENSURE(double, y_out, m);
+  if (m > 0) {
+    Resolved r;
+    rc = resolve(ctx, cfg, m, &r);  // solve_nqp validates its config (nqp.hpp:220-221)
+    if (rc) return rc;
+    rc = run_nqp(ctx, m, r, cfg, nullptr, &sum);
+    if (rc) {
+      if (out) *out = sum;
+      ctx->last = sum;
+      return rc;
+    }
+    CK(cudaMemcpyAsync(y, ctx->x.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+  } else {
+    // detail::empty_solve_result (nnls.hpp:107-113)
+    alnnls_iter_record rec{};
+    alnnls_iter_record* tr = ENSURE(alnnls_iter_record, trace, 2);
+    CK(cudaMemcpyAsync(tr, &rec, sizeof(rec), cudaMemcpyHostToDevice, s));
+    sum.termination = ALNNLS_EMPTY_PASSIVE_SET;
+    sum.trace_len = 1;
+    sum.min_iterate = 0.0;
+    sum.iterations = 0;
+    CK(cudaEventRecord(ctx->ev[2], s));
+    CK(cudaEventRecord(ctx->ev[3], s));
+  }
+  // K7: unscale + residual recomputed from A and b (nnls.hpp:141-142)
+  double* xn = ENSURE(double, X, n);
+  CK(launch_unscale(y, static_cast<double*>(ctx->scale.p), static_cast<uint32_t*>(ctx->retained.p),
+                    (int)m, xn, (int)n, s));
+  uint32_t* list = ENSURE(uint32_t, list, n);
+  double* vals = ENSURE(double, vals, n + 8);
+  int* len = ENSURE(int, mscalar, 4);
+  CK(launch_support(xn, (int)n, list, vals, len, s));
+  int hlen = 0;
+  CK(cudaMemcpyAsync(&hlen, len, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  double* ax = ENSURE(double, ax, d);
+  double* pr = ENSURE(double, prod0, d + 8);
+  double* res = ENSURE(double, resid, 2);
+  CK(launch_masked_gemv(dA, lda, (int)d, list, vals, hlen, ax, ctx->sm_count, s));
+  CK(launch_residual(ax, db, (int)d, pr, res, s));
+  CK(cudaEventRecord(ctx->ev[4], s));
+  double hres = 0.0;
+  CK(cudaMemcpyAsync(&hres, res, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  float t01 = 0, t23 = 0, t34 = 0, t04 = 0;
+  cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
+  cudaEventElapsedTime(&t34, ctx->ev[3], ctx->ev[4]);
+  cudaEventElapsedTime(&t04, ctx->ev[0], ctx->ev[4]);
+  sum.t_setup_s = t01 * 1e-3;
+  sum.t_loop_s = t23 * 1e-3;
+  sum.t_finish_s = t34 * 1e-3;
+  sum.t_total_s = t04 * 1e-3;
+  sum.residual_sq = hres;
+  sum.n = n;
+  sum.m = m;
+  sum.n_dropped = n - m;
+  ctx->last = sum;
+  if (out) *out = sum;
+  return ALNNLS_OK;
+}
+
+// Uploads host A (d x n, ld d) into ctx->A with an even, 32B-friendly ld.
+int upload_matrix(alnnls_ctx* ctx, DevBuf& buf, uint64_t rows, uint64_t cols, const double* h,
+                  uint64_t* ld_out) {
+  int st__ = ALNNLS_OK;
+  const uint64_t ld = round_up(rows, 4);
+  double* dst = ensure<double>(ctx, buf, ld * cols, &st__);
+  if (st__) return st__;
+  CK(cudaMemcpy2DAsync(dst, ld * sizeof(double), h, rows * sizeof(double), rows * sizeof(double),
+                       cols, cudaMemcpyHostToDevice, ctx->stream));
+  *ld_out = ld;
+  return ALNNLS_OK;
+}
+
+int copy_out(alnnls_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return ALNNLS_OK;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ALNNLS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int alnnls_abi_version(void) { return ALNNLS_ABI_VERSION; }
+
+void alnnls_config_default(alnnls_config* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->stall_window = 50;
+  cfg->trace_every = 1;
+  cfg->profile = ALNNLS_PROFILE_EXACT;
+  cfg->record_multiplies = 1;
+}
+
+int alnnls_create(alnnls_ctx** out, int device) {
+  if (!out) return ALNNLS_EINVAL;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0)
+    return ALNNLS_ENODEV;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return ALNNLS_ENODEV;
+  if (prop.major != 10) return ALNNLS_ENODEV;  // sm_100a code only
+  auto* c = new alnnls_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  c->cc_major = prop.major;
+  c->cc_minor = prop.minor;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return ALNNLS_ENODEV;
+  }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  *out = c;
+  return ALNNLS_OK;
+}
+
+void alnnls_destroy(alnnls_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  DevBuf* bufs[] = {&ctx->A,      &ctx->b,     &ctx->Q,       &ctx->q,     &ctx->x,    &ctx->g,
+                    &ctx->y_out,  &ctx->u,     &ctx->gd,      &ctx->mask,  &ctx->gP,   &ctx->chg,
+                    &ctx->dC,     &ctx->candC, &ctx->gC,      &ctx->prod0, &ctx->prod1, &ctx->prod2,
+                    &ctx->diag,   &ctx->pos,   &ctx->scale,   &ctx->retained, &ctx->mscalar,
+                    &ctx->trace,  &ctx->mults, &ctx->ctrl,    &ctx->list,  &ctx->vals, &ctx->ax,
+                    &ctx->resid,  &ctx->flag,  &ctx->H,       &ctx->hvec,  &ctx->start, &ctx->bcols,
+                    &ctx->X};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* alnnls_last_error(const alnnls_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+int alnnls_device_info(alnnls_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor) {
+  if (!ctx) return ALNNLS_EINVAL;
+  if (sm_count) *sm_count = ctx->sm_count;
+  if (cc_major) *cc_major = ctx->cc_major;
+  if (cc_minor) *cc_minor = ctx->cc_minor;
+  return ALNNLS_OK;
+}
+
+int alnnls_solve_nnls_device(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA,
+                             uint64_t lda, const double* db, const alnnls_config* cfg,
+                             alnnls_summary* out) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!cfg || !dA || !db) return set_err(ctx, ALNNLS_EINVAL, "solve_nnls: null argument");
+  if (d < 1 || n < 1) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  if (lda < d) return set_err(ctx, ALNNLS_EINVAL, "solve_nnls: lda < rows");
+  int st__ = ALNNLS_OK;
+  int* flag = ENSURE(int, flag, 1);
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+  CK(launch_check_finite(dA, d, n, lda, flag, ctx->stream));
+  CK(launch_check_finite(db, d, 1, d, flag, ctx->stream));
+  int hf = 0;
+  if ((rc = copy_out(ctx, &hf, flag, sizeof(int)))) return rc;
+  if (hf) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
+  // the bulk-copy GEMV on A needs an even lda and 16B-aligned columns
+  if ((lda & 1) || (reinterpret_cast<uintptr_t>(dA) & 15)) {
+    const uint64_t ld = round_up(d, 4);
+    double* dst = ENSURE(double, A, ld * n);
+    CK(launch_copy_pad(dA, lda, dst, ld, d, n, ctx->stream));
+    dA = dst;
+    lda = ld;
+  }
+  return run_nnls(ctx, d, n, dA, lda, db, cfg, out);
+}
+
+int alnnls_solve_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, const double* b,
+                      const alnnls_config* cfg, alnnls_summary* out) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!cfg || !A || !b) return set_err(ctx, ALNNLS_EINVAL, "solve_nnls: null argument");
+  if (d < 1 || n < 1) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  // DenseMatrix / Vector construction validates finiteness (linalg.hpp:42-52, :84)
+  if (!all_finite(A, d * n)) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
+  if (!all_finite(b, d)) return set_err(ctx, ALNNLS_EINVAL, "Vector: non-finite entry");
+  int st__ = ALNNLS_OK;
+  uint64_t lda = 0;
+  if ((rc = upload_matrix(ctx, ctx->A, d, n, A, &lda))) return rc;
+  double* db = ENSURE(double, b, d);
+  CK(cudaMemcpyAsync(db, b, sizeof(double) * d, cudaMemcpyHostToDevice, ctx->stream));
+  return run_nnls(ctx, d, n, static_cast<double*>(ctx->A.p), lda, db, cfg, out);
+}
+
+int alnnls_solve_nqp_device(alnnls_ctx* ctx, uint64_t m, const double* dQ, uint64_t ldq,
+                            const double* dq, const double* dstart, const alnnls_config* cfg,
+                            alnnls_summary* out) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!cfg || !dQ || !dq) return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: null argument");
+  if (m < 1) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  Resolved r;
+  if ((rc = resolve(ctx, cfg, m, &r))) return rc;
+  int st__ = ALNNLS_OK;
+  const uint64_t ld = round_up(m, 32);
+  double* Qd = ENSURE(double, Q, ld * m);
+  CK(launch_copy_pad(dQ, ldq, Qd, ld, m, m, ctx->stream));
+  ctx->ldq = ld;
+  double* qd = ENSURE(double, q, m + 8);
+  CK(cudaMemcpyAsync(qd, dq, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->last_nnls = false;
+  ctx->last_n = m;
+  ctx->last_m = m;
+  alnnls_summary sum{};
+  rc = run_nqp(ctx, m, r, cfg, dstart, &sum);
+  sum.n = m;
+  ctx->last = sum;
+  if (out) *out = sum;
+  return rc;
+}
+
+int alnnls_solve_nqp(alnnls_ctx* ctx, uint64_t m, const double* Q, const double* q,
+                     const double* start, const alnnls_config* cfg, alnnls_summary* out) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!cfg || !Q || !q) return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: null argument");
+  if (m < 1) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  if (!all_finite(Q, m * m)) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
+  if (!all_finite(q, m)) return set_err(ctx, ALNNLS_EINVAL, "Vector: non-finite entry");
+  for (uint64_t j = 0; j < m; ++j)  // NqpProblem (nqp.hpp:37-41)
+    for (uint64_t i = 0; i < j; ++i)
+      if (!(Q[j * m + i] == Q[i * m + j]))
+        return set_err(ctx, ALNNLS_EINVAL, "NqpProblem: Q must be symmetric");
+  Resolved r;
+  if ((rc = resolve(ctx, cfg, m, &r))) return rc;
+  if (start) {
+    if (!all_finite(start, m)) return set_err(ctx, ALNNLS_EINVAL, "Vector: non-finite entry");
+    for (uint64_t i = 0; i < m; ++i)  // nqp.hpp:227-230
+      if (!(start[i] >= 0.0))
+        return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: start must be nonnegative");
+  }
+  int st__ = ALNNLS_OK;
+  uint64_t ld = 0;
+  (void)ld;
+  const uint64_t ldq = round_up(m, 32);
+  double* Qd = ENSURE(double, Q, ldq * m);
+  CK(cudaMemcpy2DAsync(Qd, ldq * sizeof(double), Q, m * sizeof(double), m * sizeof(double), m,
+                       cudaMemcpyHostToDevice, ctx->stream));
+  ctx->ldq = ldq;
+  double* qd = ENSURE(double, q, m + 8);
+  CK(cudaMemcpyAsync(qd, q, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+  double* ds = nullptr;
+  if (start) {
+    ds = ENSURE(double, start, m);
+    CK(cudaMemcpyAsync(ds, start, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  ctx->last_nnls = false;
+  ctx->last_n = m;
+  ctx->last_m = m;
+  alnnls_summary sum{};
+  rc = run_nqp(ctx, m, r, cfg, ds, &sum);
+  sum.n = m;
+  sum.t_total_s = sum.t_loop_s;
+  ctx->last = sum;
+  if (out) *out = sum;
+  return rc;
+}
+
+int alnnls_get_x(alnnls_ctx* ctx, double* x, uint64_t len) {
+  if (!ctx || !x) return ALNNLS_EINVAL;
+  const uint64_t n = ctx->last_nnls ? ctx->last_n : ctx->last_m;
+  if (len < n) return set_err(ctx, ALNNLS_ECAPACITY, "get_x: buffer too small");
+  const void* src = ctx->last_nnls ? ctx->X.p : ctx->x.p;
+  return copy_out(ctx, x, src, sizeof(double) * n);
+}
+
+int alnnls_get_inner_x(alnnls_ctx* ctx, double* y, uint64_t len) {
+  if (!ctx || !y) return ALNNLS_EINVAL;
+  if (len < ctx->last_m) return set_err(ctx, ALNNLS_ECAPACITY, "get_inner_x: buffer too small");
+  return copy_out(ctx, y, ctx->last_nnls ? ctx->y_out.p : ctx->x.p, sizeof(double) * ctx->last_m);
+}
+
+int alnnls_get_final_grad(alnnls_ctx* ctx, double* g, uint64_t len) {
+  if (!ctx || !g) return ALNNLS_EINVAL;
+  if (len < ctx->last_m) return set_err(ctx, ALNNLS_ECAPACITY, "get_final_grad: buffer too small");
+  return copy_out(ctx, g, ctx->g.p, sizeof(double) * ctx->last_m);
+}
+
+int alnnls_get_trace(alnnls_ctx* ctx, alnnls_iter_record* rec, uint64_t cap) {
+  if (!ctx || !rec) return ALNNLS_EINVAL;
+  const uint64_t n = ctx->last.trace_len;
+  if (cap < n) return set_err(ctx, ALNNLS_ECAPACITY, "get_trace: buffer too small");
+  return copy_out(ctx, rec, ctx->trace.p, sizeof(alnnls_iter_record) * n);
+}
+
+int alnnls_get_multiplies(alnnls_ctx* ctx, uint64_t* mults, uint64_t cap) {
+  if (!ctx || !mults) return ALNNLS_EINVAL;
+  const uint64_t n = ctx->last.mult_len;
+  if (cap < n) return set_err(ctx, ALNNLS_ECAPACITY, "get_multiplies: buffer too small");
+  return copy_out(ctx, mults, ctx->mults.p, sizeof(uint64_t) * n);
+}
+
+int alnnls_get_scale(alnnls_ctx* ctx, double* scale, uint64_t cap) {
+  if (!ctx || !scale) return ALNNLS_EINVAL;
+  if (cap < ctx->last_m) return set_err(ctx, ALNNLS_ECAPACITY, "get_scale: buffer too small");
+  return copy_out(ctx, scale, ctx->scale.p, sizeof(double) * ctx->last_m);
+}
+
+int alnnls_get_retained(alnnls_ctx* ctx, uint64_t* idx, uint64_t cap) {
+  if (!ctx || !idx) return ALNNLS_EINVAL;
+  const uint64_t m = ctx->last_m;
+  if (cap < m) return set_err(ctx, ALNNLS_ECAPACITY, "get_retained: buffer too small");
+  std::vector<uint32_t> tmp(m);
+  int rc = copy_out(ctx, tmp.data(), ctx->retained.p, sizeof(uint32_t) * m);
+  for (uint64_t i = 0; i < m; ++i) idx[i] = tmp[i];
+  return rc;
+}
+
+int alnnls_get_dropped(alnnls_ctx* ctx, uint64_t* idx, uint64_t cap) {
+  if (!ctx || !idx) return ALNNLS_EINVAL;
+  const uint64_t n = ctx->last_n, m = ctx->last_m;
+  if (cap < n - m) return set_err(ctx, ALNNLS_ECAPACITY, "get_dropped: buffer too small");
+  std::vector<int> pos(n);
+  int rc = copy_out(ctx, pos.data(), ctx->pos.p, sizeof(int) * n);
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < n; ++i)
+    if (pos[i] < 0) idx[k++] = i;
+  return rc;
+}
+
+int alnnls_setup(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, const double* b,
+                 alnnls_summary* out) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!A || !b) return set_err(ctx, ALNNLS_EINVAL, "setup: null argument");
+  if (d < 1 || n < 1) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  if (!all_finite(A, d * n) || !all_finite(b, d))
+    return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
+  int st__ = ALNNLS_OK;
+  uint64_t lda = 0;
+  if ((rc = upload_matrix(ctx, ctx->A, d, n, A, &lda))) return rc;
+  double* db = ENSURE(double, b, d);
+  CK(cudaMemcpyAsync(db, b, sizeof(double) * d, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  uint64_t m = 0;
+  if ((rc = run_setup(ctx, d, n, static_cast<double*>(ctx->A.p), lda, db, &m))) return rc;
+  CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+  ctx->last_nnls = true;
+  ctx->last_n = n;
+  ctx->last_m = m;
+  ctx->last = alnnls_summary{};
+  ctx->last.n = n;
+  ctx->last.m = m;
+  ctx->last.n_dropped = n - m;
+  ctx->last.t_setup_s = ms * 1e-3;
+  if (out) *out = ctx->last;
+  return ALNNLS_OK;
+}
+
+int alnnls_get_Q(alnnls_ctx* ctx, double* Q, uint64_t cap) {
+  if (!ctx || !Q) return ALNNLS_EINVAL;
+  const uint64_t m = ctx->last_m;
+  if (cap < m * m) return set_err(ctx, ALNNLS_ECAPACITY, "get_Q: buffer too small");
+  if (m == 0) return ALNNLS_OK;
+  CK(cudaMemcpy2DAsync(Q, m * sizeof(double), ctx->Q.p, ctx->ldq * sizeof(double),
+                       m * sizeof(double), m, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ALNNLS_OK;
+}
+
+int alnnls_get_q(alnnls_ctx* ctx, double* q, uint64_t cap) {
+  if (!ctx || !q) return ALNNLS_EINVAL;
+  if (cap < ctx->last_m) return set_err(ctx, ALNNLS_ECAPACITY, "get_q: buffer too small");
+  return copy_out(ctx, q, ctx->q.p, sizeof(double) * ctx->last_m);
+}
+
+int alnnls_rescale(alnnls_ctx* ctx, uint64_t n, const double* H, const double* h,
+                   alnnls_summary* out) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!H || !h || n < 1) return set_err(ctx, ALNNLS_EINVAL, "rescale: bad argument");
+  for (uint64_t j = 0; j < n; ++j)  // nnls.hpp:45-49
+    for (uint64_t i = 0; i < j; ++i)
+      if (!(H[j * n + i] == H[i * n + j]))
+        return set_err(ctx, ALNNLS_EINVAL, "rescale: H must be symmetric");
+  for (uint64_t i = 0; i < n; ++i)  // nnls.hpp:55
+    if (!(H[i * n + i] >= 0.0)) return set_err(ctx, ALNNLS_EINVAL, "rescale: negative diagonal entry");
+  int st__ = ALNNLS_OK;
+  cudaStream_t s = ctx->stream;
+  double* dH = ENSURE(double, H, n * n);
+  double* dh = ENSURE(double, hvec, n);
+  CK(cudaMemcpyAsync(dH, H, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dh, h, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  std::vector<double> diag(n);
+  for (uint64_t i = 0; i < n; ++i) diag[i] = H[i * n + i];
+  double* ddiag = ENSURE(double, diag, n);
+  CK(cudaMemcpyAsync(ddiag, diag.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  SetupArgs sa{};
+  sa.n = (int)n;
+  sa.diag = ddiag;
+  sa.pos = ENSURE(int, pos, n);
+  sa.scale = ENSURE(double, scale, n);
+  sa.retained = ENSURE(uint32_t, retained, n);
+  sa.m_out = ENSURE(int, mscalar, 4);
+  CK(launch_retained(sa, s));
+  int hm = 0;
+  if ((rc = copy_out(ctx, &hm, sa.m_out, sizeof(int)))) return rc;
+  const uint64_t m = (uint64_t)hm;
+  ctx->ldq = round_up(m > 0 ? m : 1, 32);
+  double* Qd = ENSURE(double, Q, ctx->ldq * (m > 0 ? m : 1));
+  double* qd = ENSURE(double, q, m + 8);
+  CK(launch_rescale_from_h(dH, dh, (int)n, sa.pos, sa.scale, Qd, ctx->ldq, qd, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->last_nnls = true;
+  ctx->last_n = n;
+  ctx->last_m = m;
+  ctx->last = alnnls_summary{};
+  ctx->last.n = n;
+  ctx->last.m = m;
+  ctx->last.n_dropped = n - m;
+  if (out) *out = ctx->last;
+  return ALNNLS_OK;
+}
+
+int alnnls_gram(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, double* H) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!A || !H || d < 1 || n < 1) return set_err(ctx, ALNNLS_EINVAL, "gram: bad argument");
+  int st__ = ALNNLS_OK;
+  uint64_t lda = 0;
+  if ((rc = upload_matrix(ctx, ctx->A, d, n, A, &lda))) return rc;
+  double* dH = ENSURE(double, H, n * n);
+  SetupArgs sa{};
+  sa.A = static_cast<double*>(ctx->A.p);
+  sa.lda = lda;
+  sa.b = nullptr;
+  sa.d = (int)d;
+  sa.n = (int)n;
+  sa.H = dH;
+  CK(launch_syrk(sa, 0, ctx->stream));
+  return copy_out(ctx, H, dH, sizeof(double) * n * n);
+}
+
+int alnnls_transpose_matvec(alnnls_ctx* ctx, uint64_t rows, uint64_t cols, const double* M,
+                            const double* v, double* y) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!M || !v || !y || rows < 1 || cols < 1)
+    return set_err(ctx, ALNNLS_EINVAL, "transpose_matvec: bad argument");
+  int st__ = ALNNLS_OK;
+  uint64_t ld = 0;
+  if ((rc = upload_matrix(ctx, ctx->A, rows, cols, M, &ld))) return rc;
+  double* dv = ENSURE(double, b, rows);
+  double* dy = ENSURE(double, ax, cols);
+  CK(cudaMemcpyAsync(dv, v, sizeof(double) * rows, cudaMemcpyHostToDevice, ctx->stream));
+  CK(launch_coldot(static_cast<double*>(ctx->A.p), ld, (int)rows, (int)cols, dv, dy, ctx->stream));
+  return copy_out(ctx, y, dy, sizeof(double) * cols);
+}
+
+int alnnls_masked_matvec(alnnls_ctx* ctx, uint64_t rows, uint64_t cols, const double* M,
+                         const double* v, const uint64_t* mask, uint64_t mask_len, double* y,
+                         uint64_t* multiply_count) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!M || !v || !y || rows < 1 || cols < 1 || (mask_len && !mask))
+    return set_err(ctx, ALNNLS_EINVAL, "masked_matvec: bad argument");
+  for (uint64_t t = 0; t < mask_len; ++t)  // linalg.hpp:199
+    if (mask[t] >= cols) return set_err(ctx, ALNNLS_ERANGE, "masked_matvec: mask index out of range");
+  int st__ = ALNNLS_OK;
+  uint64_t ld = 0;
+  if ((rc = upload_matrix(ctx, ctx->A, rows, cols, M, &ld))) return rc;
+  std::vector<uint32_t> lst(mask_len + 1);
+  std::vector<double> vv(mask_len + 2, 0.0);
+  for (uint64_t t = 0; t < mask_len; ++t) {
+    lst[t] = (uint32_t)mask[t];
+    vv[t] = v[mask[t]];
+  }
+  uint32_t* dl = ENSURE(uint32_t, list, mask_len + 1);
+  double* dvals = ENSURE(double, vals, mask_len + 8);
+  double* dy = ENSURE(double, ax, rows);
+  CK(cudaMemcpyAsync(dl, lst.data(), sizeof(uint32_t) * (mask_len + 1), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(dvals, vv.data(), sizeof(double) * (mask_len + 2), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(launch_masked_gemv(static_cast<double*>(ctx->A.p), ld, (int)rows, dl, dvals, (int)mask_len,
+                        dy, ctx->sm_count, ctx->stream));
+  rc = copy_out(ctx, y, dy, sizeof(double) * rows);
+  if (rc == ALNNLS_OK && multiply_count) *multiply_count += rows * mask_len;
+  return rc;
+}
+
+int alnnls_matvec(alnnls_ctx* ctx, uint64_t rows, uint64_t cols, const double* M,
+                  const double* v, double* y) {
+  std::vector<uint64_t> all(cols);
+  for (uint64_t j = 0; j < cols; ++j) all[j] = j;
+  return alnnls_masked_matvec(ctx, rows, cols, M, v, all.data(), cols, y, nullptr);
+}
+
+int alnnls_solve_nnls_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A,
+                              uint64_t nrhs, const double* B, const alnnls_config* cfg, double* X,
+                              alnnls_column_result* cols, alnnls_summary* out) {
+  (void)d; (void)n; (void)A; (void)nrhs; (void)B; (void)cfg; (void)X; (void)cols; (void)out;
+  return set_err(ctx, ALNNLS_EINVAL, "batched solve not built yet");
+}
+
+int alnnls_solve_nnls_batched_device(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA,
+                                     uint64_t nrhs, const double* dB, const alnnls_config* cfg,
+                                     double* dX, alnnls_column_result* cols, alnnls_summary* out) {
+  (void)d; (void)n; (void)dA; (void)nrhs; (void)dB; (void)cfg; (void)dX; (void)cols; (void)out;
+  return set_err(ctx, ALNNLS_EINVAL, "batched solve not built yet");
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// kernels.cuh — host-visible launch interface of the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/alnnls.h"
+
+namespace alnnls {
+
+// Device-resident control block of one NQP solve (written by the loop kernel).
+struct LoopCtrl {
+  int stop;
+  int mask_len;
+  int chg_len;
+  int accept;
+  double alpha;
+  int termination;
+  int numeric_failure;
+  unsigned long long iterations;
+  unsigned long long trace_len;
+  unsigned long long mult_len;
+  unsigned long long mult_total;
+  double min_iterate;
+  double f_final;
+  double gbs_final;
+};
+
+struct LoopArgs {
+  const double* Q;  // m x m, column-major, leading dimension ldq
+  uint64_t ldq;
+  const double* q;
+  int m;
+  double* x;        // iterate (m)
+  double* g;        // maintained gradient (m)
+  double* u;        // Q g_bar (m)
+  double* gd;       // Q delta (m)
+  uint32_t* mask;   // passive set, ascending (m)
+  double* gP;       // g on the mask (m + 2)
+  uint32_t* chg;    // changed set, ascending (m)
+  double* dC;       // delta on the changed set (m + 2)
+  double* candC;    // candidate x on the changed set (m)
+  double* gC;       // g on the changed set (m)
+  double* prod0;    // chain scratch (m + 2)
+  double* prod1;
+  double* prod2;
+  // resolved SolverConfig (nqp.hpp:219-222)
+  double eps;
+  uint64_t max_iters;
+  int has_time_cap;
+  double time_cap_s;
+  uint64_t stall_window;
+  uint64_t trace_every;
+  alnnls_iter_record* trace;
+  uint64_t trace_cap;
+  uint64_t* mults;  // may be null
+  uint64_t mults_cap;
+  LoopCtrl* ctrl;
+  int rows_per_cta;
+};
+
+// Exact device-resident solve_nqp loop (nqp.hpp:249-334). One cooperative
+// launch for the whole solve; returns the launch status.
+cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream);
+int nqp_rows_per_cta(int m, int sm_count);
+size_t nqp_loop_smem_bytes();
+
+// Exact masked GEMV over a row range: y[i] = sum_t M[i, list[t]] * vals[t].
+cudaError_t launch_masked_gemv(const double* M, uint64_t ld, int rows, const uint32_t* list,
+                               const double* vals, int len, double* y, int sm_count,
+                               cudaStream_t stream);
+
+// Setup (K1-K3): D_i^2 = H_ii chains, retained compaction, fused SYRK+rescale.
+struct SetupArgs {
+  const double* A;  // d x n, lda
+  uint64_t lda;
+  const double* b;  // d
+  int d;
+  int n;
+  double* diag;     // n: H_ii
+  int* pos;         // n: retained position or -1
+  double* scale;    // m: D_a = sqrt(H_ii)
+  uint32_t* retained; // m
+  int* m_out;       // device scalar
+  double* Q;        // m x m, ldq
+  uint64_t ldq;
+  double* q;        // m
+  double* H;        // optional: raw gram output (n x n, ld n), nullptr when fusing rescale
+  double* hvec;     // optional: raw -A^T b (n)
+};
+cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream);
+cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream);
+// mode 0: write H (and -A^T b into hvec when b != nullptr); mode 1: fused rescale into Q, q.
+cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream);
+// Rescale from a given H (n x n) and h (n) on device (nnls.hpp:41-83).
+cudaError_t launch_rescale_from_h(const double* H, const double* h, int n, const int* pos,
+                                  const double* scale_full, double* Q, uint64_t ldq, double* q,
+                                  cudaStream_t stream);
+
+// K7: x = y / D scattered to the original columns (nnls.hpp:87-96).
+cudaError_t launch_unscale(const double* y, const double* scale, const uint32_t* retained, int m,
+                           double* x, int n, cudaStream_t stream);
+// residual_norm_sq (nnls.hpp:115-123): r_i = (A x)_i - b_i, s = sum r_i^2 in order.
+cudaError_t launch_residual(const double* ax, const double* b, int d, double* prod, double* out,
+                            cudaStream_t stream);
+// Compaction of the support of x (x_j != 0, ascending) for matvec(A, x).
+cudaError_t launch_support(const double* x, int n, uint32_t* list, double* vals, int* len,
+                           cudaStream_t stream);
+// transpose_matvec: y_j = sum_i M[i,j] v_i (linalg.hpp:209-219)
+cudaError_t launch_coldot(const double* M, uint64_t ld, int rows, int cols, const double* v,
+                          double* y, cudaStream_t stream);
+// g = y + q (warm start, nqp.hpp:232-233)
+cudaError_t launch_add(const double* y, const double* q, double* g, int m, cudaStream_t stream);
+// any non-finite entry among `count` doubles (strided columns) -> *flag = 1
+cudaError_t launch_check_finite(const double* p, uint64_t rows, uint64_t cols, uint64_t ld,
+                                int* flag, cudaStream_t stream);
+// pads: copy a rows x cols col-major block into a buffer with leading dimension ld_dst.
+cudaError_t launch_copy_pad(const double* src, uint64_t ld_src, double* dst, uint64_t ld_dst,
+                            uint64_t rows, uint64_t cols, cudaStream_t stream);
+
+// Batched multi-RHS exact solve (K8).
+struct BatchArgs {
+  const double* Q;     // m x m (ldq)
+  uint64_t ldq;
+  int m;
+  const double* qcols; // m x ncols: per-column linear term q (ld m)
+  int ncols;
+  double* Y;           // m x ncols solution (rescaled space)
+  alnnls_column_result* res;  // per column
+  double eps;
+  uint64_t max_iters;
+  uint64_t stall_window;
+  int* next_col;       // work counter
+};
+cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream);
+
+}  // namespace alnnls
