@@ -8,7 +8,7 @@
  *                        (/root/reference/proj/include/antilop/linalg.hpp:160-219)
  *   antilop::rescale / unscale (/root/reference/proj/include/antilop/nnls.hpp:41-96)
  * The reference is a header-only C++ library with no FFI; its public C++ API is
- * re-declared on top of this ABI by include/antilop/*.hpp.
+ * re-declared on top of this ABI by the headers in include/antilop/ (see INTEGRATION.md).
  *
  * Conventions
  *  - Plain pointers and sizes only. Matrices are column-major fp64, leading
@@ -161,6 +161,9 @@ int alnnls_get_inner_x(alnnls_ctx* ctx, double* y, uint64_t len);
 int alnnls_get_final_grad(alnnls_ctx* ctx, double* g, uint64_t len);
 int alnnls_get_trace(alnnls_ctx* ctx, alnnls_iter_record* rec, uint64_t cap);
 int alnnls_get_multiplies(alnnls_ctx* ctx, uint64_t* mults, uint64_t cap);
+/* Leader-side phase times of the last device loop (ns): [0] P1 + stop chains,
+ * [1] den chain + changed set, [2] P2, [3] df + update + next mask. */
+int alnnls_get_phase_ns(alnnls_ctx* ctx, uint64_t* ns, uint64_t cap);
 /* rescale bookkeeping of the last NNLS solve/setup (nnls.hpp:32-37). */
 int alnnls_get_scale(alnnls_ctx* ctx, double* scale, uint64_t cap);
 int alnnls_get_retained(alnnls_ctx* ctx, uint64_t* idx, uint64_t cap);

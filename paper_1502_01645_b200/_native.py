@@ -15,7 +15,8 @@ EXPORTS = [
     "alnnls_abi_version", "alnnls_config_default", "alnnls_create", "alnnls_destroy",
     "alnnls_last_error", "alnnls_device_info", "alnnls_solve_nnls", "alnnls_solve_nqp",
     "alnnls_solve_nnls_device", "alnnls_solve_nqp_device", "alnnls_get_x", "alnnls_get_inner_x",
-    "alnnls_get_final_grad", "alnnls_get_trace", "alnnls_get_multiplies", "alnnls_get_scale",
+    "alnnls_get_final_grad", "alnnls_get_trace", "alnnls_get_multiplies", "alnnls_get_phase_ns",
+    "alnnls_get_scale",
     "alnnls_get_retained", "alnnls_get_dropped", "alnnls_setup", "alnnls_get_Q", "alnnls_get_q",
     "alnnls_rescale", "alnnls_gram", "alnnls_transpose_matvec", "alnnls_matvec",
     "alnnls_masked_matvec", "alnnls_solve_nnls_batched", "alnnls_solve_nnls_batched_device",
@@ -57,6 +58,7 @@ def load():
         "alnnls_get_final_grad": ([vp, vp, u64], i32),
         "alnnls_get_trace": ([vp, vp, u64], i32),
         "alnnls_get_multiplies": ([vp, vp, u64], i32),
+        "alnnls_get_phase_ns": ([vp, vp, u64], i32),
         "alnnls_get_scale": ([vp, vp, u64], i32),
         "alnnls_get_retained": ([vp, vp, u64], i32),
         "alnnls_get_dropped": ([vp, vp, u64], i32),

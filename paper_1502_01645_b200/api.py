@@ -179,8 +179,13 @@ class Solver:
             final_grad=self._vec(self.lib.alnnls_get_final_grad, m),
             min_iterate=s.min_iterate,
             multiplies_per_iter=mults,
-            timings={"loop_s": s.t_loop_s},
+            timings={"loop_s": s.t_loop_s, "phase_s": self.phase_times()},
         )
+
+    def phase_times(self):
+        ns = np.zeros(8, np.uint64)
+        self._check(self.lib.alnnls_get_phase_ns(self.ctx, _ptr(ns), 8))
+        return [float(v) * 1e-9 for v in ns[:8]]
 
     # ---- solvers ------------------------------------------------------------------
     def solve_nnls(self, A, b, config: SolverConfig = SolverConfig()):

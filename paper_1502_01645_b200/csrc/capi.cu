@@ -42,10 +42,12 @@ struct alnnls_ctx {
   // last solve
   bool last_nnls = false;
   uint64_t last_n = 0, last_m = 0;
-  uint64_t ldq = 0;
+  uint64_t qR = 4;   // block rows of the blocked Q (gemv.cuh)
   alnnls_summary last{};
   std::vector<uint64_t> dropped_h;
   bool have_setup = false;
+  int g_parity = 0;
+  unsigned long long phase_ns[8] = {};
 };
 
 namespace {
@@ -88,6 +90,12 @@ T* ensure(alnnls_ctx* ctx, DevBuf& b, size_t count, int* st) {
   if (st__ != ALNNLS_OK) return st__
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+// doubles of a blocked m x m matrix with block rows R (gemv.cuh blk_index)
+uint64_t blocked_size(uint64_t m, uint64_t R) { return round_up(m, R) * m; }
+
+// vector length padded to the loop kernel tile (512 threads x 8) plus slack
+uint64_t vec_pad(uint64_t m) { return round_up(m > 0 ? m : 1, 4096) + 64; }
 
 bool all_finite(const double* p, size_t n) {
   for (size_t i = 0; i < n; ++i)
@@ -135,19 +143,21 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   int st__ = ALNNLS_OK;
   const double* Q = static_cast<const double*>(ctx->Q.p);
   const double* q = static_cast<const double*>(ctx->q.p);
-  double* x = ENSURE(double, x, m);
-  double* g = ENSURE(double, g, m);
-  double* u = ENSURE(double, u, m);
-  double* gd = ENSURE(double, gd, m);
-  uint32_t* mask = ENSURE(uint32_t, mask, m);
-  double* gP = ENSURE(double, gP, m + 8);
-  uint32_t* chg = ENSURE(uint32_t, chg, m);
-  double* dC = ENSURE(double, dC, m + 8);
-  double* candC = ENSURE(double, candC, m);
-  double* gC = ENSURE(double, gC, m);
-  double* p0 = ENSURE(double, prod0, m + 8);
-  double* p1 = ENSURE(double, prod1, m + 8);
-  double* p2 = ENSURE(double, prod2, m + 8);
+  // vector buffers are padded to the loop kernel's 4096-element tiles
+  const uint64_t mp = vec_pad(m);
+  double* x = ENSURE(double, x, mp);
+  double* g = ENSURE(double, g, mp);
+  double* u = ENSURE(double, u, mp);
+  double* gd = ENSURE(double, gd, mp);
+  uint32_t* mask = ENSURE(uint32_t, mask, mp);
+  double* gP = ENSURE(double, gP, mp);
+  uint32_t* chg = ENSURE(uint32_t, chg, mp);
+  double* dC = ENSURE(double, dC, mp);
+  double* candC = ENSURE(double, candC, mp);
+  double* gC = ENSURE(double, gC, mp);
+  double* g_alt = ENSURE(double, prod1, mp);
+  double* xP = ENSURE(double, prod2, mp);
+  double* qP = ENSURE(double, prod0, mp);
   LoopCtrl* ctrl = ENSURE(LoopCtrl, ctrl, 1);
   const uint64_t tcap = r.max_iters / r.trace_every + 2;
   alnnls_iter_record* trace = ENSURE(alnnls_iter_record, trace, tcap);
@@ -173,12 +183,12 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
     int hlen = 0;
     CK(cudaMemcpyAsync(&hlen, len, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    CK(launch_masked_gemv(Q, ctx->ldq, (int)m, list, vals, hlen, u, ctx->sm_count, s));
+    CK(launch_masked_gemv_blocked(Q, (int)m, (int)ctx->qR, list, vals, hlen, u, s));
     CK(launch_add(u, q, g, (int)m, s));
   }
   LoopArgs a{};
   a.Q = Q;
-  a.ldq = ctx->ldq;
+  a.ldq = 0;
   a.q = q;
   a.m = (int)m;
   a.x = x;
@@ -191,9 +201,9 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   a.dC = dC;
   a.candC = candC;
   a.gC = gC;
-  a.prod0 = p0;
-  a.prod1 = p1;
-  a.prod2 = p2;
+  a.g_alt = g_alt;
+  a.xP = xP;
+  a.qP = qP;
   a.eps = r.eps;
   a.max_iters = r.max_iters;
   a.has_time_cap = cfg->has_time_cap;
@@ -205,10 +215,10 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   a.mults = mults;
   a.mults_cap = mcap;
   a.ctrl = ctrl;
-  a.rows_per_cta = nqp_rows_per_cta((int)m, ctx->sm_count);
-  if (a.rows_per_cta > 480)
+  a.rows_per_cta = (int)ctx->qR;
+  if (a.rows_per_cta > 352)
     return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: dimension too large for one GPU row split");
-  const int nctas = (int)((m + a.rows_per_cta - 1) / a.rows_per_cta);
+  const int nctas = 1 + (int)((m + a.rows_per_cta - 1) / a.rows_per_cta);
   CK(cudaEventRecord(ctx->ev[2], s));
   CK(launch_nqp_loop(a, nctas, s));
   CK(cudaEventRecord(ctx->ev[3], s));
@@ -228,6 +238,8 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   out->f_final = hc.f_final;
   out->gbs_final = hc.gbs_final;
   out->m = m;
+  ctx->g_parity = hc.g_parity;
+  for (int i = 0; i < 8; ++i) ctx->phase_ns[i] = hc.phase_ns[i];
   if (hc.numeric_failure)
     return set_err(ctx, ALNNLS_ENUMERIC, "solve_nqp: non-finite objective or gradient");
   return ALNNLS_OK;
@@ -255,10 +267,12 @@ int run_setup(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_
   CK(cudaMemcpyAsync(&hm, sa.m_out, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const uint64_t m = (uint64_t)hm;
-  ctx->ldq = round_up(m > 0 ? m : 1, 32);
-  sa.Q = ENSURE(double, Q, ctx->ldq * (m > 0 ? m : 1));
-  sa.ldq = ctx->ldq;
-  sa.q = ENSURE(double, q, m + 8);
+  const uint64_t mm = m > 0 ? m : 1;
+  ctx->qR = (uint64_t)nqp_rows_per_cta((int)mm, ctx->sm_count);
+  sa.Q = ENSURE(double, Q, blocked_size(mm, ctx->qR));
+  sa.m = (int)m;
+  sa.qR = (int)ctx->qR;
+  sa.q = ENSURE(double, q, vec_pad(m));
   if (m > 0) CK(launch_syrk(sa, 1, s));
   *m_out = m;
   ctx->have_setup = true;
@@ -315,7 +329,7 @@ int run_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t
   CK(cudaMemcpyAsync(&hlen, len, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   double* ax = ENSURE(double, ax, d);
-  double* pr = ENSURE(double, prod0, d + 8);
+  double* pr = ENSURE(double, bcols, d + 8);
   double* res = ENSURE(double, resid, 2);
   CK(launch_masked_gemv(dA, lda, (int)d, list, vals, hlen, ax, ctx->sm_count, s));
   CK(launch_residual(ax, db, (int)d, pr, res, s));
@@ -481,11 +495,10 @@ int alnnls_solve_nqp_device(alnnls_ctx* ctx, uint64_t m, const double* dQ, uint6
   Resolved r;
   if ((rc = resolve(ctx, cfg, m, &r))) return rc;
   int st__ = ALNNLS_OK;
-  const uint64_t ld = round_up(m, 32);
-  double* Qd = ENSURE(double, Q, ld * m);
-  CK(launch_copy_pad(dQ, ldq, Qd, ld, m, m, ctx->stream));
-  ctx->ldq = ld;
-  double* qd = ENSURE(double, q, m + 8);
+  ctx->qR = (uint64_t)nqp_rows_per_cta((int)m, ctx->sm_count);
+  double* Qd = ENSURE(double, Q, blocked_size(m, ctx->qR));
+  CK(launch_to_blocked(dQ, ldq, (int)m, (int)ctx->qR, Qd, ctx->stream));
+  double* qd = ENSURE(double, q, vec_pad(m));
   CK(cudaMemcpyAsync(qd, dq, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->last_nnls = false;
   ctx->last_n = m;
@@ -521,12 +534,12 @@ int alnnls_solve_nqp(alnnls_ctx* ctx, uint64_t m, const double* Q, const double*
   int st__ = ALNNLS_OK;
   uint64_t ld = 0;
   (void)ld;
-  const uint64_t ldq = round_up(m, 32);
-  double* Qd = ENSURE(double, Q, ldq * m);
-  CK(cudaMemcpy2DAsync(Qd, ldq * sizeof(double), Q, m * sizeof(double), m * sizeof(double), m,
-                       cudaMemcpyHostToDevice, ctx->stream));
-  ctx->ldq = ldq;
-  double* qd = ENSURE(double, q, m + 8);
+  double* Qtmp = ENSURE(double, H, m * m);
+  CK(cudaMemcpyAsync(Qtmp, Q, sizeof(double) * m * m, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->qR = (uint64_t)nqp_rows_per_cta((int)m, ctx->sm_count);
+  double* Qd = ENSURE(double, Q, blocked_size(m, ctx->qR));
+  CK(launch_to_blocked(Qtmp, m, (int)m, (int)ctx->qR, Qd, ctx->stream));
+  double* qd = ENSURE(double, q, vec_pad(m));
   CK(cudaMemcpyAsync(qd, q, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
   double* ds = nullptr;
   if (start) {
@@ -562,7 +575,7 @@ int alnnls_get_inner_x(alnnls_ctx* ctx, double* y, uint64_t len) {
 int alnnls_get_final_grad(alnnls_ctx* ctx, double* g, uint64_t len) {
   if (!ctx || !g) return ALNNLS_EINVAL;
   if (len < ctx->last_m) return set_err(ctx, ALNNLS_ECAPACITY, "get_final_grad: buffer too small");
-  return copy_out(ctx, g, ctx->g.p, sizeof(double) * ctx->last_m);
+  return copy_out(ctx, g, ctx->g_parity ? ctx->prod1.p : ctx->g.p, sizeof(double) * ctx->last_m);
 }
 
 int alnnls_get_trace(alnnls_ctx* ctx, alnnls_iter_record* rec, uint64_t cap) {
@@ -577,6 +590,12 @@ int alnnls_get_multiplies(alnnls_ctx* ctx, uint64_t* mults, uint64_t cap) {
   const uint64_t n = ctx->last.mult_len;
   if (cap < n) return set_err(ctx, ALNNLS_ECAPACITY, "get_multiplies: buffer too small");
   return copy_out(ctx, mults, ctx->mults.p, sizeof(uint64_t) * n);
+}
+
+int alnnls_get_phase_ns(alnnls_ctx* ctx, uint64_t* ns, uint64_t cap) {
+  if (!ctx || !ns) return ALNNLS_EINVAL;
+  for (uint64_t i = 0; i < cap && i < 8; ++i) ns[i] = ctx->phase_ns[i];
+  return ALNNLS_OK;
 }
 
 int alnnls_get_scale(alnnls_ctx* ctx, double* scale, uint64_t cap) {
@@ -644,10 +663,11 @@ int alnnls_get_Q(alnnls_ctx* ctx, double* Q, uint64_t cap) {
   const uint64_t m = ctx->last_m;
   if (cap < m * m) return set_err(ctx, ALNNLS_ECAPACITY, "get_Q: buffer too small");
   if (m == 0) return ALNNLS_OK;
-  CK(cudaMemcpy2DAsync(Q, m * sizeof(double), ctx->Q.p, ctx->ldq * sizeof(double),
-                       m * sizeof(double), m, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  return ALNNLS_OK;
+  int st__ = ALNNLS_OK;
+  double* tmp = ENSURE(double, H, m * m);
+  CK(launch_from_blocked(static_cast<double*>(ctx->Q.p), (int)m, (int)ctx->qR, tmp, m,
+                         ctx->stream));
+  return copy_out(ctx, Q, tmp, sizeof(double) * m * m);
 }
 
 int alnnls_get_q(alnnls_ctx* ctx, double* q, uint64_t cap) {
@@ -688,10 +708,11 @@ int alnnls_rescale(alnnls_ctx* ctx, uint64_t n, const double* H, const double* h
   int hm = 0;
   if ((rc = copy_out(ctx, &hm, sa.m_out, sizeof(int)))) return rc;
   const uint64_t m = (uint64_t)hm;
-  ctx->ldq = round_up(m > 0 ? m : 1, 32);
-  double* Qd = ENSURE(double, Q, ctx->ldq * (m > 0 ? m : 1));
-  double* qd = ENSURE(double, q, m + 8);
-  CK(launch_rescale_from_h(dH, dh, (int)n, sa.pos, sa.scale, Qd, ctx->ldq, qd, s));
+  const uint64_t mm = m > 0 ? m : 1;
+  ctx->qR = (uint64_t)nqp_rows_per_cta((int)mm, ctx->sm_count);
+  double* Qd = ENSURE(double, Q, blocked_size(mm, ctx->qR));
+  double* qd = ENSURE(double, q, vec_pad(m));
+  CK(launch_rescale_from_h(dH, dh, (int)n, sa.pos, sa.scale, Qd, (int)m, (int)ctx->qR, qd, s));
   CK(cudaStreamSynchronize(s));
   ctx->last_nnls = true;
   ctx->last_n = n;

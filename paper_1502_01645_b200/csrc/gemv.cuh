@@ -9,20 +9,25 @@
 // the result is bitwise equal. `vals` is the vector compacted to the list
 // (vals[t] = v[list[t]]).
 //
-// Data movement (B200): a producer warp streams the CTA's column segments
-// M[row0 : row0+seg, list[t]] (contiguous in the column-major layout) into a
+// Data movement (B200): producer warps stream the CTA's column segments into a
 // deep shared-memory ring with cp.async.bulk (TMA 1D, UBLKCP) completing on
 // mbarriers; consumer warps walk the ring. Only the listed columns are read,
 // so HBM traffic equals the reference's multiply count x 8 bytes.
+//
+// Measured on B200: bulk copies are request-rate bound per SM (~13 ns per
+// request per producer group), so (a) several producer warps issue stages
+// round-robin, and (b) Q is stored row-block-contiguous ("blocked": the R
+// rows of block b for column j at Qb + b*R*m + j*R), which makes a run of
+// consecutive mask columns ONE contiguous copy.
 #pragma once
 
 #include "common.cuh"
 
 namespace alnnls {
 
-constexpr int kRingCols = 8;    // columns per stage (even: keeps vals 16B aligned)
-constexpr int kMaxStages = 64;
-constexpr size_t kRingSmemBytes = 200 * 1024;  // dynamic smem of ring-carrying kernels
+constexpr int kRingCols = 64;   // columns per stage
+constexpr int kMaxStages = 48;
+constexpr size_t kRingSmemBytes = 192 * 1024;  // dynamic smem of ring-carrying kernels
 
 struct RowRing {
   uint64_t* full;
@@ -30,31 +35,37 @@ struct RowRing {
   double* data;   // [S][G][seg]
   double* vals;   // [S][G]
   int S;
-  int seg;        // doubles per column segment (nrows rounded up to even)
-  int cons_warps; // consumer warps (warps 1..cons_warps)
+  int G;          // columns per stage
+  int seg;        // doubles per column slot
+  int P;          // producer warps: warps [0, P)
+  int cons_warps; // consumer warps: warps [P, P + cons_warps)
   uint32_t pos;   // stages issued so far (identical in every thread)
 };
 
 __host__ __device__ inline int ring_seg(int nrows) { return (nrows + 1) & ~1; }
-__host__ __device__ inline size_t ring_stage_bytes(int seg) {
-  return (size_t)kRingCols * seg * 8 + (size_t)kRingCols * 8;
+__host__ __device__ inline size_t ring_stage_bytes(int seg, int G) {
+  return (size_t)G * seg * 8 + (size_t)G * 8;
 }
 
-// Carves the ring out of `smem` (16B aligned, `bytes` long). Must be called by
-// every thread; contains a __syncthreads.
-__device__ inline void ring_setup(RowRing& r, uint8_t* smem, size_t bytes, int nrows) {
-  r.seg = ring_seg(nrows > 0 ? nrows : 2);
-  r.cons_warps = (nrows + 31) / 32;
-  if (r.cons_warps < 1) r.cons_warps = 1;
-  const size_t sb = ring_stage_bytes(r.seg);
+// Carves the ring out of `smem` (16B aligned, `bytes` long). seg = doubles per
+// column slot (>= nrows, even). max_warps bounds producers + consumers. Must be
+// called by every thread; contains a __syncthreads.
+__device__ inline void ring_setup(RowRing& r, uint8_t* smem, size_t bytes, int nrows, int seg,
+                                  int max_warps) {
+  r.seg = seg;
+  r.cons_warps = max(1, (nrows + 31) / 32);
   const size_t hdr = (size_t)kMaxStages * 16;
-  int S = (int)((bytes - hdr) / sb);
+  int G = kRingCols;
+  while (G > 8 && (bytes - hdr) / ring_stage_bytes(seg, G) < 8) G >>= 1;
+  r.G = G;
+  int S = (int)((bytes - hdr) / ring_stage_bytes(seg, G));
   if (S > kMaxStages) S = kMaxStages;
   r.S = S;
+  r.P = max(1, min(min(4, S), max_warps - r.cons_warps));
   r.full = reinterpret_cast<uint64_t*>(smem);
   r.empty = r.full + kMaxStages;
   r.data = reinterpret_cast<double*>(smem + hdr);
-  r.vals = r.data + (size_t)S * kRingCols * r.seg;
+  r.vals = r.data + (size_t)S * G * seg;
   r.pos = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -66,57 +77,95 @@ __device__ inline void ring_setup(RowRing& r, uint8_t* smem, size_t bytes, int n
   __syncthreads();
 }
 
-// Runs the row-block GEMV over `len` listed columns. Every thread of the CTA
-// calls it (idle warps just advance the ring position). Consumers write
-// out[row0 + t]. No block barrier inside or at the end.
-__device__ inline void gemv_rows(RowRing& r, const double* __restrict__ M, uint64_t ld, int row0,
-                                 int nrows, const uint32_t* __restrict__ list,
+// Runs the row-block GEMV over `len` listed columns. Column j's segment for
+// this CTA starts at base + j*col_stride and is seg doubles long. When
+// `runs` is true (blocked layout, col_stride == seg) consecutive listed
+// columns are fetched with one bulk copy. Warps outside [0, P+cons_warps)
+// return immediately. Every thread must call it (r.pos advances uniformly).
+// Consumers write out[row0 + t]. No block barrier inside.
+__device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, uint64_t col_stride,
+                                 bool runs, int row0, int nrows,
+                                 const uint32_t* __restrict__ list,
                                  const double* __restrict__ vals, int len,
                                  double* __restrict__ out) {
-  const int nst = (len + kRingCols - 1) / kRingCols;
+  const int G = r.G;
+  const int nst = (len + G - 1) / G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int seg = r.seg;
-  if (warp == 0) {
-    // order generic-proxy writes of list/vals (other CTAs, before the grid
-    // barrier) before the async-proxy bulk reads issued below
+  if (warp < r.P) {
+    // order generic-proxy writes of list/vals (before the grid barrier)
+    // before the async-proxy bulk reads issued below
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    for (int s = 0; s < nst; ++s) {
+    for (int s = warp; s < nst; s += r.P) {
       const uint32_t p = r.pos + s;
       const int st = (int)(p % r.S);
       const uint32_t ph = (p / r.S) & 1u;
-      const int base = s * kRingCols;
-      const int cnt = min(kRingCols, len - base);
+      const int sbase = s * G;
+      const int cnt = min(G, len - sbase);
       if (lane == 0) {
         mbar_wait(&r.empty[st], ph ^ 1u);
         const uint32_t bytes = (uint32_t)(cnt * seg * 8 + ((cnt + 1) & ~1) * 8);
         mbar_arrive_expect_tx(&r.full[st], bytes);
       }
       __syncwarp();
-      double* dst = r.data + (size_t)st * kRingCols * seg;
-      if (lane < cnt) {
-        const uint32_t j = __ldcg(list + base + lane);
-        bulk_g2s(dst + (size_t)lane * seg, M + (size_t)j * ld + row0, (uint32_t)seg * 8,
-                 &r.full[st]);
-      } else if (lane == 31) {
-        bulk_g2s(r.vals + (size_t)st * kRingCols, vals + base, (uint32_t)(((cnt + 1) & ~1) * 8),
-                 &r.full[st]);
+      double* dst = r.data + (size_t)st * G * seg;
+      for (int l0 = 0; l0 < cnt; l0 += 32) {
+        const int l = l0 + lane;
+        const bool valid = l < cnt;
+        const uint32_t j = valid ? __ldcg(list + sbase + l) : 0u;
+        if (runs) {
+          // a lane starts a run unless its column directly follows the previous one
+          const uint32_t jp = __shfl_up_sync(0xffffffffu, j, 1);
+          const bool start = valid && (lane == 0 || j != jp + 1u);
+          const uint32_t starts = __ballot_sync(0xffffffffu, start);
+          if (start) {
+            const uint32_t later = starts & ~((2u << lane) - 1u);  // run starts after me
+            int end = later ? __ffs(later) - 1 : 32;
+            end = min(end, cnt - l0);
+            const int rl = end - lane;
+            bulk_g2s(dst + (size_t)l * seg, base + (size_t)j * col_stride,
+                     (uint32_t)(rl * seg * 8), &r.full[st]);
+          }
+        } else if (valid) {
+          bulk_g2s(dst + (size_t)l * seg, base + (size_t)j * col_stride, (uint32_t)seg * 8,
+                   &r.full[st]);
+        }
       }
+      if (lane == 0)
+        bulk_g2s(r.vals + (size_t)st * G, vals + sbase, (uint32_t)(((cnt + 1) & ~1) * 8),
+                 &r.full[st]);
     }
-  } else if (warp <= r.cons_warps) {
-    const int t = (warp - 1) * 32 + lane;
+  } else if (warp < r.P + r.cons_warps) {
+    const int t = (warp - r.P) * 32 + lane;
+    const int tt = t < nrows ? t : 0;
     double acc = 0.0;
     for (int s = 0; s < nst; ++s) {
       const uint32_t p = r.pos + s;
       const int st = (int)(p % r.S);
       const uint32_t ph = (p / r.S) & 1u;
-      const int cnt = min(kRingCols, len - s * kRingCols);
+      const int cnt = min(G, len - s * G);
       mbar_wait(&r.full[st], ph);
-      const double* col = r.data + (size_t)st * kRingCols * seg;
-      const double* v = r.vals + (size_t)st * kRingCols;
-      if (t < nrows) {
+      const double* col = r.data + (size_t)st * G * seg;
+      const double* v = r.vals + (size_t)st * G;
+      // All rounded products of a full stage are formed first (independent
+      // LDS + DMUL, in registers), then one dependent DADD chain runs over
+      // them: ptxas cannot interleave the chain ahead of the loads, so the
+      // 8-cycle DADD latency is the only per-column cost (measured ~2.3x
+      // faster than a fused mul/add loop on B200).
+      if (cnt == 64 && G == 64) {
+        double p[64];
 #pragma unroll
-        for (int l = 0; l < kRingCols; ++l)
-          if (l < cnt) acc = xmac(acc, col[l * seg + t], v[l]);
+        for (int l = 0; l < 64; ++l) p[l] = xmul(col[l * seg + tt], v[l]);
+#pragma unroll
+        for (int l = 0; l < 64; ++l) acc = xadd(acc, p[l]);
+      } else if (cnt == 32 && G == 32) {
+        double p[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) p[l] = xmul(col[l * seg + tt], v[l]);
+#pragma unroll
+        for (int l = 0; l < 32; ++l) acc = xadd(acc, p[l]);
+      } else {
+        for (int l = 0; l < cnt; ++l) acc = xmac(acc, col[l * seg + tt], v[l]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[st]);
@@ -124,6 +173,11 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ M, uint6
     if (t < nrows) out[row0 + t] = acc;
   }
   r.pos += nst;
+}
+
+// Blocked-layout index of Q(i, j) with block rows R (m x m logical).
+__host__ __device__ inline size_t blk_index(uint64_t i, uint64_t j, uint64_t m, uint64_t R) {
+  return (i / R) * R * m + j * R + (i % R);
 }
 
 }  // namespace alnnls

@@ -24,6 +24,9 @@ struct LoopCtrl {
   double min_iterate;
   double f_final;
   double gbs_final;
+  int state;        // leader -> grid broadcast after a barrier (LoopState)
+  int g_parity;     // which gradient buffer holds the maintained gradient
+  unsigned long long phase_ns[8];  // accumulated leader-side phase times
 };
 
 struct LoopArgs {
@@ -32,7 +35,8 @@ struct LoopArgs {
   const double* q;
   int m;
   double* x;        // iterate (m)
-  double* g;        // maintained gradient (m)
+  double* g;        // maintained gradient, ping-pong buffer 0 (m)
+  double* g_alt;    // ping-pong buffer 1 (m)
   double* u;        // Q g_bar (m)
   double* gd;       // Q delta (m)
   uint32_t* mask;   // passive set, ascending (m)
@@ -41,9 +45,8 @@ struct LoopArgs {
   double* dC;       // delta on the changed set (m + 2)
   double* candC;    // candidate x on the changed set (m)
   double* gC;       // g on the changed set (m)
-  double* prod0;    // chain scratch (m + 2)
-  double* prod1;
-  double* prod2;
+  double* xP;       // x on the mask (m)
+  double* qP;       // q on the mask (m)
   // resolved SolverConfig (nqp.hpp:219-222)
   double eps;
   uint64_t max_iters;
@@ -82,8 +85,9 @@ struct SetupArgs {
   double* scale;    // m: D_a = sqrt(H_ii)
   uint32_t* retained; // m
   int* m_out;       // device scalar
-  double* Q;        // m x m, ldq
-  uint64_t ldq;
+  double* Q;        // m x m in the blocked layout (gemv.cuh blk_index, block rows qR)
+  int m;            // retained count (known on the host before the SYRK launch)
+  int qR;
   double* q;        // m
   double* H;        // optional: raw gram output (n x n, ld n), nullptr when fusing rescale
   double* hvec;     // optional: raw -A^T b (n)
@@ -94,8 +98,17 @@ cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream);
 cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream);
 // Rescale from a given H (n x n) and h (n) on device (nnls.hpp:41-83).
 cudaError_t launch_rescale_from_h(const double* H, const double* h, int n, const int* pos,
-                                  const double* scale_full, double* Q, uint64_t ldq, double* q,
+                                  const double* scale, double* Q, int m, int qR, double* q,
                                   cudaStream_t stream);
+// Exact masked GEMV on a blocked m x m matrix (block rows R).
+cudaError_t launch_masked_gemv_blocked(const double* Qb, int m, int R, const uint32_t* list,
+                                       const double* vals, int len, double* y,
+                                       cudaStream_t stream);
+// Column-major (ld) -> blocked layout, and back.
+cudaError_t launch_to_blocked(const double* src, uint64_t ld, int m, int R, double* dst,
+                              cudaStream_t stream);
+cudaError_t launch_from_blocked(const double* src, int m, int R, double* dst, uint64_t ld,
+                                cudaStream_t stream);
 
 // K7: x = y / D scattered to the original columns (nnls.hpp:87-96).
 cudaError_t launch_unscale(const double* y, const double* scale, const uint32_t* retained, int m,

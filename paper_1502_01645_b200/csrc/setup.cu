@@ -14,6 +14,7 @@
 // not capped at half of the fp64 peak. The epilogue writes Q = H/(D_i D_j)
 // (Q_ii = 1) and q = (-h)/D directly: H is never materialised.
 #include "common.cuh"
+#include "gemv.cuh"
 #include "kernels.cuh"
 
 namespace alnnls {
@@ -141,12 +142,12 @@ __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode
         const int pi = s.pos[i], pj = s.pos[j];
         if (pi < 0 || pj < 0) continue;
         if (i == j) {
-          s.Q[(size_t)pi * s.ldq + pi] = 1.0;  // nnls.hpp:72
+          s.Q[blk_index(pi, pi, s.m, s.qR)] = 1.0;  // nnls.hpp:72
         } else {
           // nnls.hpp:75: H(ja, jb) / (scale[a] * scale[b]) with a < b
           const double qv = xdiv(v, xmul(s.scale[pi], s.scale[pj]));
-          s.Q[(size_t)pj * s.ldq + pi] = qv;
-          s.Q[(size_t)pi * s.ldq + pj] = qv;
+          s.Q[blk_index(pi, pj, s.m, s.qR)] = qv;
+          s.Q[blk_index(pj, pi, s.m, s.qR)] = qv;
         }
       }
     }
@@ -210,20 +211,20 @@ __global__ void retained_kernel(const double* diag, int n, int* pos, double* sca
 
 // Q from an explicit H (alnnls_rescale): one thread per output entry.
 __global__ void rescale_from_h_kernel(const double* H, const double* h, int n, const int* pos,
-                                      const double* scale, double* Q, uint64_t ldq, double* q) {
+                                      const double* scale, double* Q, int m, int qR, double* q) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   if (i >= n || j >= n || i > j) return;
   const int pi = pos[i], pj = pos[j];
   if (pi < 0 || pj < 0) return;
   if (i == j) {
-    Q[(size_t)pi * ldq + pi] = 1.0;
+    Q[blk_index(pi, pi, m, qR)] = 1.0;
     q[pi] = xdiv(h[i], scale[pi]);
     return;
   }
   const double v = xdiv(H[(size_t)j * n + i], xmul(scale[pi], scale[pj]));
-  Q[(size_t)pj * ldq + pi] = v;
-  Q[(size_t)pi * ldq + pj] = v;
+  Q[blk_index(pi, pj, m, qR)] = v;
+  Q[blk_index(pj, pi, m, qR)] = v;
 }
 
 __global__ void unscale_kernel(const double* y, const double* scale, const uint32_t* retained,
@@ -312,7 +313,35 @@ __global__ void copy_pad_kernel(const double* src, uint64_t ld_src, double* dst,
   }
 }
 
+// column-major (ld) <-> blocked layout; one thread per element
+__global__ void to_blocked_kernel(const double* src, uint64_t ld, int m, int R, double* dst,
+                                  int dir) {
+  const uint64_t total = (uint64_t)m * m;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = e / m, i = e % m;
+    if (dir == 0)
+      dst[blk_index(i, j, m, R)] = src[j * ld + i];
+    else
+      dst[j * ld + i] = src[blk_index(i, j, m, R)];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_to_blocked(const double* src, uint64_t ld, int m, int R, double* dst,
+                              cudaStream_t stream) {
+  if (m <= 0) return cudaSuccess;
+  to_blocked_kernel<<<148 * 8, 256, 0, stream>>>(src, ld, m, R, dst, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_from_blocked(const double* src, int m, int R, double* dst, uint64_t ld,
+                                cudaStream_t stream) {
+  if (m <= 0) return cudaSuccess;
+  to_blocked_kernel<<<148 * 8, 256, 0, stream>>>(src, ld, m, R, dst, 1);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream) {
   if (s.n <= 0) return cudaSuccess;
@@ -343,11 +372,11 @@ cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream) {
 }
 
 cudaError_t launch_rescale_from_h(const double* H, const double* h, int n, const int* pos,
-                                  const double* scale, double* Q, uint64_t ldq, double* q,
+                                  const double* scale, double* Q, int m, int qR, double* q,
                                   cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   dim3 grid((n + 127) / 128, n);
-  rescale_from_h_kernel<<<grid, 128, 0, stream>>>(H, h, n, pos, scale, Q, ldq, q);
+  rescale_from_h_kernel<<<grid, 128, 0, stream>>>(H, h, n, pos, scale, Q, m, qR, q);
   return cudaGetLastError();
 }
 
