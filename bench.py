@@ -1,0 +1,399 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200-native anti-lopsided NNLS hot path (solve_nnls).
+
+A "step" is one full solve_nnls (Gram + cosine rescale + device-resident
+projected-gradient loop + unscale + residual; nnls.hpp:129-144) of the
+BASELINE.json workload, default c2 = configs[1] (d=8192, n=4096, N(0,1),
+eps 1e-8; seeded synthetic inputs, see paper_1502_01645_b200/instances.py).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2]
+  python bench.py --impl reference ...   # the reference CPU solver (oracle/_ref)
+
+Prints ONE JSON line on rank 0. `value` is whole-job solves/s with A, b already
+in HBM (device-pointer C-ABI entry); `e2e` is the same metric through the
+host-buffer public API with the H2D copy of A, b and the D2H of the result in
+the timed region. Timing: CUDA events on the library's stream, max over ranks.
+N > 1 runs one independent replica per GPU ("replicas only": one solve's
+iteration loop does not shard).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1502_01645_b200 import abi, instances  # noqa: E402
+
+METRIC = "solve_nnls time-to-KKT-tol throughput (solves/s)"
+UNIT = "solves/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# fp64 peaks measured on this pool's B200 by tools/microbench/fp64_probe.cu
+# (profiles/r01_fp64_probe.txt): DMMA 37.0 TFLOP/s; the bit-exact profile needs a
+# separate DMUL and DADD per product on the FP64 pipe, capping it at half: 18.5.
+FP64_PEAK_TFLOPS = 37.0
+FP64_EXACT_CAP_TFLOPS = 18.5
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist  # noqa
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local, dist
+
+
+def solver_config(inst):
+    from paper_1502_01645_b200.api import SolverConfig
+    # stall off like the reference's own benchmark convention (acceptance.cpp:73-88)
+    return SolverConfig(epsilon=inst["epsilon"], max_iters=inst["max_iters"], stall_window=10**9)
+
+
+def traffic_from_profiles(workload, kernel):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(workload, {}).get(kernel)
+
+
+# ---- reference CPU solver timing ----------------------------------------------------------
+def cpu_reference_step(ora, inst, cfg_abi, H, sample_rows):
+    """One bounded sample of the reference CPU pipeline (nnls.hpp:129-144):
+    gram on `sample_rows` rows of A, scaled linearly in d (the gram inner loop is
+    one dot over k, linalg.hpp:168), plus transpose_matvec, rescale, solve_nqp,
+    unscale and the residual run for real on the full problem (H supplied)."""
+    A, b = inst["A"], inst["b"]
+    d, n = A.shape
+    ds = min(d, sample_rows)
+    As = np.asfortranarray(A[:ds, :])
+    t = time.perf_counter()
+    ora.gram(As)
+    t_gram = (time.perf_counter() - t) * d / ds
+    t = time.perf_counter()
+    atb = ora.transpose_matvec(A, b)
+    t_tmv = time.perf_counter() - t
+    t = time.perf_counter()
+    sys_ = ora.rescale(H, -atb)
+    t_rescale = time.perf_counter() - t
+    t = time.perf_counter()
+    res = ora.solve_nqp(sys_["Q"], sys_["q"], cfg_abi) if len(sys_["q"]) else None
+    t_loop = time.perf_counter() - t
+    t = time.perf_counter()
+    x = np.zeros(n)
+    if res is not None:
+        x[sys_["retained"].astype(np.int64)] = res["x"] / sys_["scale"]
+    ax = ora.matvec(A, x)
+    r = ax - b
+    _ = float(np.sum(r * r))
+    t_fin = time.perf_counter() - t
+    total = t_gram + t_tmv + t_rescale + t_loop + t_fin
+    return total, {"gram_extrapolated_s": t_gram, "transpose_matvec_s": t_tmv,
+                   "rescale_s": t_rescale, "solve_nqp_s": t_loop, "finish_s": t_fin,
+                   "iterations": res["iterations"] if res else 0,
+                   "termination": res["termination"] if res else "EmptyPassiveSet"}
+
+
+def reference_gram_parallel(ora, A, threads):
+    """Untimed: the reference's own gram(), driven over column-block pairs on all
+    host threads; every entry is the same k-ascending chain, so H is bitwise gram(A)."""
+    from concurrent.futures import ThreadPoolExecutor
+    d, n = A.shape
+    nb = max(1, min(16, threads))
+    bs = (n + nb - 1) // nb
+    blocks = [(i * bs, min(n, (i + 1) * bs)) for i in range(nb) if i * bs < n]
+    H = np.zeros((n, n), order="F")
+
+    def work(pair):
+        (a0, a1), (b0, b1) = pair
+        if (a0, a1) == (b0, b1):
+            Hb = ora.gram(np.asfortranarray(A[:, a0:a1]))
+            H[a0:a1, a0:a1] = Hb
+        else:
+            cols = np.concatenate([np.arange(a0, a1), np.arange(b0, b1)])
+            Hb = ora.gram(np.asfortranarray(A[:, cols]))
+            k = a1 - a0
+            H[a0:a1, b0:b1] = Hb[:k, k:]
+            H[b0:b1, a0:a1] = Hb[k:, :k]
+
+    pairs = [(blocks[i], blocks[j]) for i in range(len(blocks)) for j in range(i, len(blocks))]
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(work, pairs))
+    return H
+
+
+def ref_oracle():
+    from oracle.oracle import Oracle, available
+    if available("ref"):
+        return Oracle("ref"), "reference"
+    return Oracle("oracle"), "port"
+
+
+def sample_rows_for(inst):
+    d, n = inst["A"].shape
+    # ~4 GFLOP of gram per sample (~3 s on one core at the reference's 1.4 GFLOP/s)
+    return int(max(16, min(d, 4.0e9 / max(1.0, n * (n + 1.0)))))
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return 0
+    inst = instances.make_config(args.workload)
+    cfg = solver_config(inst).to_abi()
+    ora, kind = ref_oracle()
+    threads = os.cpu_count() or 1
+    t = time.perf_counter()
+    H = reference_gram_parallel(ora, inst["A"], threads)
+    t_pre = time.perf_counter() - t
+    rows = sample_rows_for(inst)
+    for _ in range(args.warmup):
+        cpu_reference_step(ora, inst, cfg, H, rows)
+    times, detail = [], None
+    for _ in range(args.steps):
+        tt, detail = cpu_reference_step(ora, inst, cfg, H, rows)
+        times.append(tt)
+    per = float(np.mean(times))
+    value = 1.0 / per
+    d, n = inst["A"].shape
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64, BASELINE.json configs)",
+        "config": {"workload": f"{args.workload}: d={d}, n={n}", "eps": inst["epsilon"],
+                   "stall_window": "off"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": (f"reference gram on {rows} of {d} rows scaled linearly in d; "
+                                    "transpose_matvec, rescale, solve_nqp, unscale, residual on "
+                                    "the full problem (single thread; the reference is "
+                                    f"single-threaded per solve). Untimed H precompute {t_pre:.1f}s "
+                                    f"on {threads} threads"),
+                         "breakdown": detail},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- our GPU path ---------------------------------------------------------------------------
+def run_ours(args, ws, rank, local, dist):
+    import torch
+    from paper_1502_01645_b200.api import Solver
+    torch.cuda.set_device(local)
+    inst = instances.make_config(args.workload)
+    A, b = inst["A"], inst["b"]
+    d, n = A.shape
+    cfg = solver_config(inst)
+    s = Solver(local)
+    # inputs resident in HBM: column-major A == row-major (n, d) tensor
+    dA = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    db = torch.from_numpy(b).cuda()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        s.solve_nnls_device(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
+    summ = s.last_summary()
+    iters = int(summ.iterations)
+    mults = int(summ.multiplies_total)
+
+    barrier()
+    torch.cuda.synchronize()
+    l0 = s.launch_count()
+    with ClockSampler(local) as clk:
+        s.timer_start()
+        t_setup = t_loop = 0.0
+        for _ in range(args.steps):
+            s.solve_nnls_device(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
+            sm = s.last_summary()
+            t_setup += sm.t_setup_s
+            t_loop += sm.t_loop_s
+        t = s.timer_stop()
+    torch.cuda.synchronize()
+    barrier()
+    launches = (s.launch_count() - l0) // max(1, args.steps)
+    t_max = t
+    if dist is not None:
+        tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = ws * args.steps / t_max
+
+    # e2e: host-buffer public API, pinned host inputs, result read back each step
+    pA = torch.empty((n, d), dtype=torch.float64, pin_memory=True)
+    pA.copy_(torch.from_numpy(np.ascontiguousarray(A.T)))
+    pb = torch.empty(d, dtype=torch.float64, pin_memory=True)
+    pb.copy_(torch.from_numpy(b))
+    hA = pA.numpy().T  # Fortran-ordered (d, n) view of pinned memory
+    hb = pb.numpy()
+    res = s.solve_nnls(hA, hb, cfg)  # warm
+    barrier()
+    s.timer_start()
+    for _ in range(args.steps):
+        res = s.solve_nnls(hA, hb, cfg)
+    te = s.timer_stop()
+    if dist is not None:
+        tt = torch.tensor([te], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+    m = len(res.inner.x)
+    d2h = 8 * (n + 2 * m + len(res.inner.multiplies_per_iter)) + 56 * len(res.inner.trace)
+    e2e = {"value": ws * args.steps / te, "unit": UNIT, "h2d_bytes_per_step": 8 * (d * n + d),
+           "d2h_bytes_per_step": int(d2h)}
+
+    if rank != 0:
+        return 0
+    hbm, hbm_kind = peaks()
+    per_setup = t_setup / args.steps
+    per_loop = t_loop / args.steps
+    setup_flops = d * n * (n + 1) + 2 * d * n
+    loop_gbs = 8.0 * mults / per_loop / 1e9 if per_loop > 0 else 0.0
+    setup_tf = setup_flops / per_setup / 1e12
+    roof_loop = {"kernel": "nqp_loop_kernel (device-resident iteration loop, masked GEMVs)",
+                 "bound": "hbm", "achieved": loop_gbs, "peak": hbm, "unit": "GB/s",
+                 "frac": loop_gbs / hbm, "peak_source": hbm_kind,
+                 "algorithmic": f"8 B x reference multiply count = {8 * mults} B per launch",
+                 "traffic": traffic_from_profiles(args.workload, "nqp_loop_kernel")}
+    roof_setup = {"kernel": "setup: colchain + syrk_exact + rescale epilogue",
+                  "bound": "fp64", "achieved": setup_tf, "peak": FP64_PEAK_TFLOPS,
+                  "unit": "TFLOP/s", "frac": setup_tf / FP64_PEAK_TFLOPS,
+                  "frac_of_exact_cap": setup_tf / FP64_EXACT_CAP_TFLOPS,
+                  "peak_source": "measured (tools/microbench/fp64_probe.cu, DMMA)",
+                  "algorithmic": f"d*n*(n+1) + 2*d*n = {setup_flops} flop per solve",
+                  "traffic": traffic_from_profiles(args.workload, "syrk_exact_kernel")}
+    dominant = roof_loop if per_loop >= per_setup else roof_setup
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64, BASELINE.json configs)",
+        "config": {"workload": f"{args.workload}: d={d}, n={n}", "eps": inst["epsilon"],
+                   "stall_window": "off", "profile": "exact (bitwise reference trajectory)",
+                   "l2": "inputs larger than L2 (A 268 MB, Q 134 MB at c2)",
+                   "parallelism": f"replicas x{ws}"},
+        "iterations": iters, "time_to_tol_ms": t_max / args.steps * 1e3,
+        "iters_per_s": iters / per_loop if per_loop > 0 else None,
+        "setup_ms": per_setup * 1e3, "loop_ms": per_loop * 1e3,
+        "roofline": dominant, "roofline_other": roof_setup if dominant is roof_loop else roof_loop,
+        "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        ora, kind = ref_oracle()
+        H = s.gram(A)  # bitwise equal to the reference gram (tests/test_gpu_parity.py)
+        rows = sample_rows_for(inst)
+        tt, detail = cpu_reference_step(ora, inst, cfg.to_abi(), H, rows)
+        line["cpu_baseline"] = {
+            "value": 1.0 / tt, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": (f"reference gram on {rows} of {d} rows scaled linearly in d; "
+                       "transpose_matvec, rescale, solve_nqp, unscale, residual on the full "
+                       "problem (H from the bit-identical GPU gram); single thread"),
+            "breakdown": detail}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local, dist = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            return run_reference(args, ws, rank)
+        return run_ours(args, ws, rank, local, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

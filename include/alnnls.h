@@ -161,9 +161,16 @@ int alnnls_get_inner_x(alnnls_ctx* ctx, double* y, uint64_t len);
 int alnnls_get_final_grad(alnnls_ctx* ctx, double* g, uint64_t len);
 int alnnls_get_trace(alnnls_ctx* ctx, alnnls_iter_record* rec, uint64_t cap);
 int alnnls_get_multiplies(alnnls_ctx* ctx, uint64_t* mults, uint64_t cap);
-/* Leader-side phase times of the last device loop (ns): [0] P1 + stop chains,
- * [1] den chain + changed set, [2] P2, [3] df + update + next mask. */
+/* Vector-CTA phase times of the last device loop, accumulated (ns):
+ * [0] stop-test chains, [1] rest of P1 + barrier, [2] den chain, [3] changed set,
+ * [4] barrier + P2 + barrier, [5] df chain, [6] update + next mask, [7] barrier. */
 int alnnls_get_phase_ns(alnnls_ctx* ctx, uint64_t* ns, uint64_t cap);
+/* Device-side timing on the context's stream (CUDA events): start, then stop
+ * returns the elapsed seconds between the two records. */
+int alnnls_timer_start(alnnls_ctx* ctx);
+int alnnls_timer_stop(alnnls_ctx* ctx, double* seconds);
+/* Number of this library's kernels launched on the context so far. */
+uint64_t alnnls_launch_count(const alnnls_ctx* ctx);
 /* rescale bookkeeping of the last NNLS solve/setup (nnls.hpp:32-37). */
 int alnnls_get_scale(alnnls_ctx* ctx, double* scale, uint64_t cap);
 int alnnls_get_retained(alnnls_ctx* ctx, uint64_t* idx, uint64_t cap);

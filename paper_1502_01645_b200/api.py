@@ -182,6 +182,23 @@ class Solver:
             timings={"loop_s": s.t_loop_s, "phase_s": self.phase_times()},
         )
 
+    def timer_start(self):
+        """Records a CUDA event on the context's stream (device-side timing)."""
+        self._check(self.lib.alnnls_timer_start(self.ctx))
+
+    def timer_stop(self):
+        """Seconds between timer_start and now, measured on the device."""
+        out = C.c_double()
+        self._check(self.lib.alnnls_timer_stop(self.ctx, C.byref(out)))
+        return out.value
+
+    def launch_count(self):
+        """Number of this library's kernels launched on the context so far."""
+        return int(self.lib.alnnls_launch_count(self.ctx))
+
+    def last_summary(self):
+        return self._summary
+
     def phase_times(self):
         ns = np.zeros(8, np.uint64)
         self._check(self.lib.alnnls_get_phase_ns(self.ctx, _ptr(ns), 8))

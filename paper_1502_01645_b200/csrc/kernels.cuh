@@ -91,11 +91,14 @@ struct SetupArgs {
   double* q;        // m
   double* H;        // optional: raw gram output (n x n, ld n), nullptr when fusing rescale
   double* hvec;     // optional: raw -A^T b (n)
+  double* hvec_scratch;  // n doubles for A^T b when b is given
 };
 cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream);
 cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream);
 // mode 0: write H (and -A^T b into hvec when b != nullptr); mode 1: fused rescale into Q, q.
 cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream);
+// q (mode 1) or hvec = -(A^T b) (mode 0) from the column chains' A^T b.
+cudaError_t launch_q_from_atb(const SetupArgs& s, int mode, cudaStream_t stream);
 // Rescale from a given H (n x n) and h (n) on device (nnls.hpp:41-83).
 cudaError_t launch_rescale_from_h(const double* H, const double* h, int n, const int* pos,
                                   const double* scale, double* Q, int m, int qR, double* q,

@@ -21,120 +21,122 @@ namespace alnnls {
 
 namespace {
 
-constexpr int BM = 128;           // output tile (square)
-constexpr int BK = 16;            // k slab
-constexpr int TM = 8;             // per-thread register tile TM x TM
-constexpr int NT = (BM / TM) * (BM / TM);  // 256 threads
-constexpr int LDS = BM + 1;       // padded smem row (doubles): conflict-free stores
+constexpr int BM = 128;   // output tile (square)
+constexpr int BK = 16;    // k slab
+constexpr int NT = 512;   // 16 warps: 4 per scheduler to hide the 8-cycle DMUL->DADD latency
+constexpr int LDS = BM + 2;  // padded smem row (doubles): 16B-aligned rows, <=2-way store conflicts
+// thread tile 8 rows x 4 cols: rows 2tx+(r&1)+32(r>>1), cols 2ty+(c&1)+64(c>>1)
+// (each 16B shared load of a row pair is conflict-free across the 16 tx lanes)
 
-__device__ __forceinline__ const double* col_ptr(const SetupArgs& s, int c) {
-  if (c < s.n) return s.A + (size_t)c * s.lda;
-  if (c == s.n && s.b) return s.b;
-  return nullptr;
-}
-
-// Upper-triangular tile index -> (ti, tj), ti <= tj.
-__device__ __forceinline__ void tri_tile(int t, int nt, int& ti, int& tj) {
-  // rows of the upper triangle: tj-major enumeration
+// Upper-triangular tile index -> (ti, tj), ti <= tj (tj-major enumeration).
+__device__ __forceinline__ void tri_tile(int t, int& ti, int& tj) {
   int j = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
   while ((j + 1) * (j + 2) / 2 <= t) ++j;
   while (j * (j + 1) / 2 > t) --j;
   tj = j;
   ti = t - j * (j + 1) / 2;
-  (void)nt;
 }
 
-constexpr size_t kSyrkSmem = 2 * 2 * BK * LDS * sizeof(double);
+constexpr int kStages = 3;
+constexpr size_t kSyrkSmem = (size_t)kStages * 2 * BK * LDS * sizeof(double);
 
-__global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode, int na) {
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode) {
   extern __shared__ __align__(16) double syrk_sm[];
   auto As = reinterpret_cast<double(*)[BK][LDS]>(syrk_sm);
-  auto Bs = reinterpret_cast<double(*)[BK][LDS]>(syrk_sm + 2 * BK * LDS);
-  const int ntile = (na + BM - 1) / BM;
+  auto Bs = reinterpret_cast<double(*)[BK][LDS]>(syrk_sm + kStages * BK * LDS);
   int ti, tj;
-  tri_tile(blockIdx.x, ntile, ti, tj);
+  tri_tile(blockIdx.x, ti, tj);
   const int i0 = ti * BM, j0 = tj * BM;
-  const int tx = threadIdx.x % (BM / TM), ty = threadIdx.x / (BM / TM);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 
-  // loader mapping: element e = threadIdx.x + r*NT, col = e / BK, kk = e % BK
-  const double* pa[8];
-  const double* pb[8];
+  // loader: element e = tid + r*NT (r < 4) of a BK x BM slab: column e/BK, row k0 + e%BK.
+  // Out-of-range elements are zero-filled (src-size 0): adding +0 to a chain is exact
+  // (s + (+0) == s, and s is never -0).
+  const double* pa[4];
+  const double* pb[4];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
+  for (int r = 0; r < 4; ++r) {
     const int e = threadIdx.x + r * NT;
-    pa[r] = col_ptr(s, i0 + e / BK);
-    pb[r] = col_ptr(s, j0 + e / BK);
+    const int ca = i0 + e / BK, cb = j0 + e / BK;
+    pa[r] = ca < s.n ? s.A + (size_t)ca * s.lda : nullptr;
+    pb[r] = cb < s.n ? s.A + (size_t)cb * s.lda : nullptr;
   }
-  double ra[8], rb[8];
-  auto gload = [&](int k0) {
+  auto issue = [&](int kb) {
+    const int buf = kb % kStages;
+    const int k0 = kb * BK;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int kk = (threadIdx.x + r * NT) % BK;
-      const int k = k0 + kk;
-      ra[r] = (pa[r] && k < s.d) ? __ldg(pa[r] + k) : 0.0;
-      rb[r] = (pb[r] && k < s.d) ? __ldg(pb[r] + k) : 0.0;
-    }
-  };
-  auto sstore = [&](int buf) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < 4; ++r) {
       const int e = threadIdx.x + r * NT;
-      As[buf][e % BK][e / BK] = ra[r];
-      Bs[buf][e % BK][e / BK] = rb[r];
+      const int kk = e % BK, k = k0 + kk;
+      const bool va = pa[r] && k < s.d, vb = pb[r] && k < s.d;
+      cp_async8(&As[buf][kk][e / BK], va ? pa[r] + k : s.A, va ? 8u : 0u);
+      cp_async8(&Bs[buf][kk][e / BK], vb ? pb[r] + k : s.A, vb ? 8u : 0u);
     }
   };
 
-  double acc[TM][TM];
+  double acc[8][4];
 #pragma unroll
-  for (int r = 0; r < TM; ++r)
+  for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int c = 0; c < TM; ++c) acc[r][c] = 0.0;
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
 
   const int nk = (s.d + BK - 1) / BK;
-  gload(0);
-  sstore(0);
-  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < kStages - 1; ++p) {
+    if (p < nk) issue(p);
+    cp_async_commit();
+  }
   for (int kb = 0; kb < nk; ++kb) {
-    const int buf = kb & 1;
-    if (kb + 1 < nk) gload((kb + 1) * BK);
+    cp_async_wait<kStages - 2>();  // slab kb has landed (this thread's copies)
+    __syncthreads();               // ... everyone's; and slab kb-1's buffer is free
+    if (kb + kStages - 1 < nk) issue(kb + kStages - 1);
+    cp_async_commit();
+    const int buf = kb % kStages;
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      double a[TM], b[TM];
+      double a[8], b[4];
 #pragma unroll
-      for (int r = 0; r < TM; ++r) a[r] = As[buf][kk][tx + r * (BM / TM)];
+      for (int h = 0; h < 4; ++h) {
+        const double2 v = *reinterpret_cast<const double2*>(&As[buf][kk][2 * tx + 32 * h]);
+        a[2 * h] = v.x;
+        a[2 * h + 1] = v.y;
+      }
 #pragma unroll
-      for (int c = 0; c < TM; ++c) b[c] = Bs[buf][kk][ty + c * (BM / TM)];
+      for (int h = 0; h < 2; ++h) {
+        const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][kk][2 * ty + 64 * h]);
+        b[2 * h] = v.x;
+        b[2 * h + 1] = v.y;
+      }
+      // each output: one chain over k ascending, rounded product then rounded sum
 #pragma unroll
-      for (int r = 0; r < TM; ++r)
+      for (int r = 0; r < 8; ++r) {
+        double p[4];
 #pragma unroll
-        for (int c = 0; c < TM; ++c) acc[r][c] = xmac(acc[r][c], a[r], b[c]);
-    }
-    if (kb + 1 < nk) {
-      sstore(buf ^ 1);
-      __syncthreads();
+        for (int c = 0; c < 4; ++c) p[c] = xmul(a[r], b[c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = xadd(acc[r][c], p[c]);
+      }
     }
   }
 
-  // epilogue
+  // epilogue: upper triangle only, mirrored (exact symmetry, linalg.hpp:169-170)
 #pragma unroll
-  for (int r = 0; r < TM; ++r) {
-    const int i = i0 + tx + r * (BM / TM);
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + 2 * tx + (r & 1) + 32 * (r >> 1);
 #pragma unroll
-    for (int c = 0; c < TM; ++c) {
-      const int j = j0 + ty + c * (BM / TM);
-      if (i > j || i >= s.n || j > s.n) continue;
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + 2 * ty + (c & 1) + 64 * (c >> 1);
+      if (i > j || j >= s.n) continue;
       const double v = acc[r][c];
-      if (j == s.n) {  // column n: (A^T b)_i, h = -(A^T b) (nnls.hpp:133-134)
-        if (!s.b) continue;
-        const double h = -v;
-        if (mode == 0) {
-          if (s.hvec) s.hvec[i] = h;
-        } else {
-          const int pi = s.pos[i];
-          if (pi >= 0) s.q[pi] = xdiv(h, s.scale[pi]);  // nnls.hpp:79
-        }
-        continue;
-      }
       if (mode == 0) {
         s.H[(size_t)j * s.n + i] = v;
         s.H[(size_t)i * s.n + j] = v;
@@ -154,26 +156,73 @@ __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode
   }
 }
 
-// H_ii chain per column (identical to the SYRK diagonal chain).
-__global__ void gram_diag_kernel(SetupArgs s) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= s.n) return;
-  const double* p = s.A + (size_t)c * s.lda;
-  double acc = 0.0;
-  int k = 0;
-  constexpr int B = 8;
-  for (; k + B <= s.d; k += B) {
-    double v[B];
-#pragma unroll
-    for (int t = 0; t < B; ++t) v[t] = __ldg(p + k + t);
-#pragma unroll
-    for (int t = 0; t < B; ++t) acc = xmac(acc, v[t], v[t]);
+// q_b = h(j_b) / D_b with h = -(A^T b) (nnls.hpp:79, :133-134); atb = A^T b.
+__global__ void q_from_atb_kernel(const double* atb, const int* pos, const double* scale, int n,
+                                  double* q, double* hvec) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double h = -atb[j];
+  if (hvec) hvec[j] = h;
+  if (q) {
+    const int p = pos[j];
+    if (p >= 0) q[p] = xdiv(h, scale[p]);
   }
-  for (; k < s.d; ++k) {
-    const double v = __ldg(p + k);
-    acc = xmac(acc, v, v);
+}
+
+// Column chains over A (K1 diagonal + K2): for each column c of a 32-column
+// group, diag_c = sum_k A[k,c]^2 (bitwise the SYRK diagonal / gram (c,c)
+// chain, linalg.hpp:168) and atb_c = sum_k A[k,c] b[k] (transpose_matvec,
+// linalg.hpp:215), each ONE chain in ascending k. Warps 1..7 stream k-tiles
+// of the 32 columns with coalesced loads into a double-buffered shared tile
+// (transposed to [column][k]); lane c of warp 0 runs column c's chains.
+constexpr int kCcKT = 224;                 // k per stage (7 loader warps x 32)
+constexpr int kCcLD = kCcKT + 1;           // odd stride: 2-wavefront reads
+constexpr size_t kColChainSmem = (2 * 32 * kCcLD + 2 * kCcKT) * sizeof(double);
+
+__global__ void __launch_bounds__(256, 1)
+    colchain_kernel(const double* A, uint64_t lda, int d, int n, const double* b, double* diag,
+                    double* atb) {
+  extern __shared__ __align__(16) double cc_sm[];
+  double* tile = cc_sm;                    // [2][32][kCcLD]
+  double* btile = cc_sm + 2 * 32 * kCcLD;  // [2][kCcKT]
+  const int c0 = blockIdx.x * 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nst = (d + kCcKT - 1) / kCcKT;
+  auto load = [&](int st, int buf) {
+    const int kk = (warp - 1) * 32 + lane;
+    const int k = st * kCcKT + kk;
+    double* t = tile + (size_t)buf * 32 * kCcLD;
+#pragma unroll 8
+    for (int c = 0; c < 32; ++c) {
+      const int col = c0 + c;
+      t[c * kCcLD + kk] = (k < d && col < n) ? __ldg(A + (size_t)col * lda + k) : 0.0;
+    }
+    if (b) btile[buf * kCcKT + kk] = k < d ? __ldg(b + k) : 0.0;
+  };
+  double sd = 0.0, sb = 0.0;
+  if (warp > 0) load(0, 0);
+  __syncthreads();
+  for (int st = 0; st < nst; ++st) {
+    const int buf = st & 1;
+    if (warp == 0) {
+      const double* t = tile + (size_t)buf * 32 * kCcLD + lane * kCcLD;
+      const double* bt = btile + buf * kCcKT;
+      // zero padding past d is exact (s + (+0) == s; s is never -0)
+#pragma unroll 8
+      for (int kk = 0; kk < kCcKT; ++kk) {
+        const double v = t[kk];
+        sd = xmac(sd, v, v);
+        if (b) sb = xmac(sb, v, bt[kk]);
+      }
+    } else if (st + 1 < nst) {
+      load(st + 1, buf ^ 1);
+    }
+    __syncthreads();
   }
-  s.diag[c] = acc;
+  if (warp == 0 && c0 + lane < n) {
+    if (diag) diag[c0 + lane] = sd;
+    if (atb) atb[c0 + lane] = sb;
+  }
 }
 
 // rescale bookkeeping (nnls.hpp:53-63): retained ascending, D = sqrt(H_ii).
@@ -345,7 +394,24 @@ cudaError_t launch_from_blocked(const double* src, int m, int R, double* dst, ui
 
 cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream) {
   if (s.n <= 0) return cudaSuccess;
-  gram_diag_kernel<<<(s.n + 127) / 128, 128, 0, stream>>>(s);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(colchain_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kColChainSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  colchain_kernel<<<(s.n + 31) / 32, 256, kColChainSmem, stream>>>(
+      s.A, s.lda, s.d, s.n, s.b, s.diag, s.b ? s.hvec_scratch : nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_q_from_atb(const SetupArgs& s, int mode, cudaStream_t stream) {
+  if (!s.b || s.n <= 0) return cudaSuccess;
+  q_from_atb_kernel<<<(s.n + 255) / 256, 256, 0, stream>>>(s.hvec_scratch, s.pos, s.scale, s.n,
+                                                           mode == 1 ? s.q : nullptr,
+                                                           mode == 0 ? s.hvec : nullptr);
   return cudaGetLastError();
 }
 
@@ -356,8 +422,7 @@ cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream) {
 }
 
 cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream) {
-  const int na = s.n + (s.b ? 1 : 0);
-  const int nt = (na + BM - 1) / BM;
+  const int nt = (s.n + BM - 1) / BM;
   const int tiles = nt * (nt + 1) / 2;
   if (tiles == 0) return cudaSuccess;
   static bool attr = false;
@@ -367,7 +432,7 @@ cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  syrk_exact_kernel<<<tiles, NT, kSyrkSmem, stream>>>(s, mode, na);
+  syrk_exact_kernel<<<tiles, NT, kSyrkSmem, stream>>>(s, mode);
   return cudaGetLastError();
 }
 

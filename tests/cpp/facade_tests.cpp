@@ -1,0 +1,207 @@
+// C++ facade tests: the reference's own unit-test cases (tests/test_{linalg,
+// nqp,nnls}.cpp under /root/reference/proj), restated against the B200
+// facade include/antilop/*.hpp. Code is written against the same API the
+// reference exposes; every hot-path call runs on the GPU through the C ABI.
+// Needs a GPU: run by tests/test_facade_cpp.py (pytest -m gpu).
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <limits>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "antilop/nnls.hpp"
+
+using namespace antilop;
+
+namespace {
+
+int g_fail = 0, g_pass = 0;
+std::string g_case;
+
+#define REQUIRE(cond)                                                                 \
+  do {                                                                                \
+    if (!(cond)) {                                                                    \
+      std::printf("FAIL [%s] %s:%d: %s\n", g_case.c_str(), __FILE__, __LINE__, #cond); \
+      ++g_fail;                                                                       \
+      return;                                                                         \
+    }                                                                                 \
+  } while (0)
+
+template <class E, class F>
+bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+bool near(double a, double b, double tol) { return std::abs(a - b) <= tol; }
+
+void run(const char* name, const std::function<void()>& f) {
+  g_case = name;
+  const int before = g_fail;
+  try {
+    f();
+  } catch (const std::exception& e) {
+    std::printf("FAIL [%s] unexpected exception: %s\n", name, e.what());
+    ++g_fail;
+  }
+  if (g_fail == before) {
+    ++g_pass;
+    std::printf("PASS [%s]\n", name);
+  }
+}
+
+NqpProblem coupled() { return NqpProblem(DenseMatrix(2, 2, {1.0, 1.0 / 30.0, 1.0 / 30.0, 1.0}), Vector{-4.0, -5.0 / 3.0}); }
+NqpProblem lopsided() { return NqpProblem(DenseMatrix(2, 2, {1.0, 0.1, 0.1, 9.0}), Vector{-4.0, -5.0}); }
+
+}  // namespace
+
+int main() {
+  run("gram fixed examples", [] {  // test_linalg.cpp:57-81
+    const DenseMatrix h = gram(DenseMatrix::from_rows({{1.0, 1.0}, {0.0, 1.0}}));
+    REQUIRE(h(0, 0) == 1.0 && h(0, 1) == 1.0 && h(1, 0) == 1.0 && h(1, 1) == 2.0);
+    const DenseMatrix z = gram(DenseMatrix::from_rows({{1.0, 0.0}, {2.0, 0.0}}));
+    REQUIRE(z(0, 1) == 0.0 && z(1, 0) == 0.0 && z(1, 1) == 0.0 && z(0, 0) == 5.0);
+  });
+  run("masked matvec", [] {  // test_linalg.cpp:114-155
+    const DenseMatrix h = DenseMatrix::from_rows({{1.0, 1.0}, {1.0, 2.0}});
+    const std::vector<std::size_t> mask{1};
+    const Vector y = masked_matvec(h, Vector{0.0, 2.0}, mask);
+    REQUIRE(y[0] == 2.0 && y[1] == 4.0);
+    const std::vector<std::size_t> bad{2};
+    REQUIRE(throws<std::out_of_range>([&] { masked_matvec(h, Vector{1.0, 2.0}, bad); }));
+    std::size_t cnt = 7;
+    masked_matvec(h, Vector{1.0, 2.0}, mask, &cnt);
+    REQUIRE(cnt == 7 + 2);
+    REQUIRE(throws<std::invalid_argument>([&] { matvec(h, Vector{1.0, 2.0, 3.0}); }));
+  });
+  run("transpose matvec", [] {  // test_linalg.cpp:157-163
+    const Vector y = transpose_matvec(DenseMatrix::from_rows({{1.0, 1.0}, {0.0, 1.0}}), Vector{2.0, -1.0});
+    REQUIRE(y[0] == 2.0 && y[1] == 1.0);
+  });
+  run("exact step", [] {  // test_nqp.cpp:65-103
+    REQUIRE(*exact_step(DenseMatrix::identity(2), Vector{1.0, 2.0}) == 1.0);
+    REQUIRE(*exact_step(DenseMatrix(2, 2, {2.0, 0.0, 0.0, 2.0}), Vector{1.0, 2.0}) == 0.5);
+    const auto a3 = exact_step(DenseMatrix(2, 2, {1.0, 1.0 / 30.0, 1.0 / 30.0, 1.0}), Vector{-4.0, -5.0 / 3.0});
+    REQUIRE(a3 && near(*a3, 169.0 / 173.0, 1e-15));
+    REQUIRE(!exact_step(DenseMatrix(2, 2, 0.0), Vector{1.0, 1.0}));
+  });
+  run("identity one step", [] {  // test_nqp.cpp:123-133
+    const auto res = solve_nqp(NqpProblem(DenseMatrix::identity(2), Vector{-1.0, -2.0}));
+    REQUIRE(res.termination == Termination::GradientBelowEpsilon && res.iterations() == 1);
+    REQUIRE(res.x[0] == 1.0 && res.x[1] == 2.0 && res.final_grad[0] == 0.0);
+  });
+  run("origin stop", [] {  // test_nqp.cpp:135-144
+    const auto res = solve_nqp(NqpProblem(DenseMatrix::identity(2), Vector{3.0, 4.0}));
+    REQUIRE(res.termination == Termination::EmptyPassiveSet && res.iterations() == 0);
+    REQUIRE(res.trace.size() == 1 && !res.trace.back().alpha);
+  });
+  run("coupled optimum", [] {  // test_nqp.cpp:146-156
+    SolverConfig c;
+    c.epsilon = 1e-22;
+    const auto res = solve_nqp(coupled(), c);
+    REQUIRE(res.termination == Termination::GradientBelowEpsilon);
+    REQUIRE(near(res.x[0], 3550.0 / 899.0, 1e-9) && near(res.x[1], 1380.0 / 899.0, 1e-9));
+  });
+  run("warm start", [] {  // test_nqp.cpp:158-177
+    const NqpProblem p(DenseMatrix::identity(2), Vector{-1.0, -2.0});
+    const auto at = solve_nqp(p, {}, Vector{1.0, 2.0});
+    REQUIRE(at.termination == Termination::GradientBelowEpsilon && at.iterations() == 0);
+    REQUIRE(throws<std::invalid_argument>([&] { solve_nqp(p, {}, Vector{-0.5, 0.0}); }));
+    REQUIRE(throws<std::invalid_argument>([&] { solve_nqp(p, {}, Vector{1.0}); }));
+    SolverConfig t;
+    t.epsilon = 1e-10;
+    t.max_iters = 100000;
+    const auto far = solve_nqp(lopsided(), t, Vector{30.0, 2.0});
+    REQUIRE(far.termination == Termination::GradientBelowEpsilon);
+    REQUIRE(near(far.x[0], 35.5 / 8.99, 1e-4) && near(far.x[1], 4.6 / 8.99, 1e-4));
+  });
+  run("terminations", [] {  // test_nqp.cpp:179-215
+    SolverConfig c;
+    c.epsilon = 1e-30;
+    c.max_iters = 3;
+    c.stall_window = 1000;
+    REQUIRE(solve_nqp(lopsided(), c).termination == Termination::MaxIters);
+    SolverConfig tc;
+    tc.time_cap = std::chrono::duration<double>(0.0);
+    REQUIRE(solve_nqp(NqpProblem(DenseMatrix::identity(2), Vector{-1.0, -2.0}), tc).termination == Termination::TimeCap);
+    SolverConfig st;
+    st.epsilon = std::numeric_limits<double>::denorm_min();
+    st.max_iters = 1000000;
+    st.stall_window = 5;
+    const auto s = solve_nqp(coupled(), st);
+    REQUIRE(s.termination == Termination::Stalled && near(s.x[0], 3550.0 / 899.0, 1e-9));
+    REQUIRE(solve_nqp(NqpProblem(DenseMatrix(2, 2, 0.0), Vector{-1.0, -1.0})).termination == Termination::ZeroCurvature);
+  });
+  run("numeric failure", [] {  // test_nqp.cpp:217-226
+    bool caught = false;
+    try {
+      solve_nqp(NqpProblem(DenseMatrix::identity(2), Vector{-1e308, -1.0}));
+    } catch (const NumericFailure& e) {
+      caught = e.trace().empty() && std::string(e.what()).find("non-finite") != std::string::npos;
+    }
+    REQUIRE(caught);
+  });
+  run("halving safeguard", [] {  // test_nqp.cpp:349-389
+    const NqpProblem p(DenseMatrix(2, 2, {1.0, 0.9, 0.9, 1.0}), Vector{1.49, -2.69});
+    SolverConfig c;
+    c.epsilon = 1e-18;
+    c.max_iters = 10000;
+    c.stall_window = 1000000;
+    const auto res = solve_nqp(p, c, Vector{0.52, 0.35});
+    REQUIRE(res.termination == Termination::GradientBelowEpsilon && res.x[0] == 0.0);
+    REQUIRE(near(res.x[1], 2.69, 1e-9) && near(objective(p, res.x), -3.61805, 1e-9));
+    for (std::size_t k = 1; k < res.trace.size(); ++k)
+      REQUIRE(res.trace[k].f <= res.trace[k - 1].f + 1e-12 * std::max(1.0, std::abs(res.trace[k - 1].f)));
+  });
+  run("trace csv", [] {  // test_nqp.cpp:298-320
+    const auto res = solve_nqp(NqpProblem(DenseMatrix::identity(2), Vector{-1.0, -2.0}));
+    std::ostringstream os;
+    write_trace_csv(os, res.trace);
+    std::istringstream is(os.str());
+    std::string line;
+    std::getline(is, line);
+    REQUIRE(line == "iter,elapsed_ms,f,grad_bar_sq,passive_count,alpha");
+    std::vector<std::string> rows;
+    while (std::getline(is, line)) rows.push_back(line);
+    REQUIRE(rows.size() == 2 && rows[0].substr(rows[0].size() - 2) == ",1" && rows[1].back() == ',');
+    REQUIRE(rows[1].find(",-2.5,") != std::string::npos);
+  });
+  run("rescale cosine system", [] {  // test_nnls.cpp:48-78
+    const auto sys = rescale(DenseMatrix(2, 2, {1.0, 0.1, 0.1, 9.0}), Vector{-4.0, -5.0});
+    REQUIRE(sys.problem && sys.dropped.empty() && sys.scale[0] == 1.0 && sys.scale[1] == 3.0);
+    REQUIRE(sys.problem->Q(0, 1) == 0.1 / 3.0 && sys.problem->q[1] == -5.0 / 3.0);
+    REQUIRE(throws<std::invalid_argument>([] { rescale(DenseMatrix(2, 3), Vector{1.0, 2.0}); }));
+    REQUIRE(throws<std::invalid_argument>([] { rescale(DenseMatrix(2, 2, {1.0, 0.2, 0.1, 1.0}), Vector{1.0, 2.0}); }));
+    REQUIRE(throws<std::invalid_argument>([] { rescale(DenseMatrix(2, 2, {-1.0, 0.0, 0.0, 1.0}), Vector{1.0, 2.0}); }));
+  });
+  run("zero column dropped", [] {  // test_nnls.cpp:80-101
+    const auto res = solve_nnls(DenseMatrix(2, 2, {1.0, 0.0, 0.0, 0.0}), Vector{3.0, 1.0});
+    REQUIRE(near(res.x[0], 3.0, 1e-12) && res.x[1] == 0.0);
+    REQUIRE(res.dropped_columns == std::vector<std::size_t>{1} && near(res.residual_sq, 1.0, 1e-12));
+  });
+  run("all-zero matrix", [] {  // test_nnls.cpp:103-111
+    const auto res = solve_nnls(DenseMatrix(3, 2, 0.0), Vector{1.0, 2.0, 3.0});
+    REQUIRE(res.x[0] == 0.0 && res.x[1] == 0.0 && res.inner.termination == Termination::EmptyPassiveSet);
+    REQUIRE(res.dropped_columns == (std::vector<std::size_t>{0, 1}) && near(res.residual_sq, 14.0, 1e-13));
+  });
+  run("frozen small systems", [] {  // test_nnls.cpp:178-194
+    const auto r = solve_nnls(DenseMatrix::identity(2), Vector{3.0, -1.0});
+    REQUIRE(near(r.x[0], 3.0, 1e-10) && r.x[1] == 0.0 && near(r.residual_sq, 1.0, 1e-10));
+    REQUIRE(throws<std::invalid_argument>([] { solve_nnls(DenseMatrix::identity(2), Vector{1.0, 2.0, 3.0}); }));
+  });
+  run("result summary json", [] {  // test_nnls.cpp:220-228
+    const std::string js = result_summary_json(solve_nnls(DenseMatrix::identity(2), Vector{3.0, -1.0}));
+    REQUIRE(js.find("\"termination\":\"GradientBelowEpsilon\"") != std::string::npos);
+    REQUIRE(js.find("\"dropped_columns\":[]") != std::string::npos);
+  });
+  std::printf("facade_tests: %d passed, %d failed\n", g_pass, g_fail);
+  return g_fail ? 1 : 0;
+}

@@ -1,0 +1,111 @@
+"""Golden fixtures (tests/golden/*.npz, produced by the reference compiled from
+its own headers, tests/golden/make_golden.py): the CPU oracle (CPU test) and
+the CUDA path (GPU test) must reproduce them bit for bit."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from paper_1502_01645_b200 import abi, instances
+from tests.parity import same_bits
+
+GOLD = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+def load(path):
+    z = np.load(path, allow_pickle=False)
+    return {k: z[k] for k in z.files}
+
+
+def inputs_of(name, g):
+    """Regenerates the inputs of a fixture (or takes the stored ones)."""
+    if "A" in g:
+        return g["A"], g["b"]
+    if name == "c1_full":
+        inst = instances.make_config("c1")
+    elif name == "c5_defaults_400x200":
+        inst = instances.make_config("c5", d=400, n=200, seed=77)
+    else:
+        cfgname, _, shape = name.split("_")
+        d, n = (int(v) for v in shape.split("x"))
+        inst = instances.make_config(cfgname, d=d, n=n)
+    return inst["A"], inst["b"]
+
+
+def cfg_of(g):
+    kw = dict(eval(str(g["cfg"])))  # repr of sorted (key, value) pairs written by make_golden
+    return abi.make_config(**kw)
+
+
+def check_trace(tr, g):
+    assert len(tr) == len(g["tr_f"])
+    for k, r in enumerate(tr):
+        it = r["iter"] if isinstance(r, dict) else r.iter
+        f = r["f"] if isinstance(r, dict) else r.f
+        gb = r["grad_bar_sq"] if isinstance(r, dict) else r.grad_bar_sq
+        pc = r["passive_count"] if isinstance(r, dict) else r.passive_count
+        al = r["alpha"] if isinstance(r, dict) else r.alpha
+        assert it == int(g["tr_iter"][k]) and pc == int(g["tr_pc"][k])
+        assert same_bits([f], [g["tr_f"][k]]) and same_bits([gb], [g["tr_gbs"][k]])
+        if bool(g["tr_has_alpha"][k]):
+            assert al is not None and same_bits([al], [g["tr_alpha"][k]])
+        else:
+            assert al is None
+
+
+def check_nnls(res_x, res_inner_x, res_grad, resid, iters, term, trace, g):
+    assert iters == int(g["iterations"]) and str(term) == str(g["termination"])
+    assert same_bits(res_x, g["x"])
+    assert same_bits(res_inner_x, g["inner_x"])
+    assert same_bits(res_grad, g["final_grad"])
+    assert same_bits([resid], [g["residual_sq"]])
+    check_trace(trace, g)
+
+
+@pytest.mark.parametrize("path", GOLD, ids=[os.path.basename(p)[:-4] for p in GOLD])
+def test_oracle_matches_reference_golden(path, oracle):
+    g = load(path)
+    name = os.path.basename(path)[:-4]
+    cfg = cfg_of(g)
+    if str(g["kind"]) == "nnls":
+        A, b = inputs_of(name, g)
+        assert instances.sha256(np.asfortranarray(A), b) == str(g["input_sha256"]), \
+            "seeded generator drifted from the fixture"
+        r = oracle.solve_nnls(A, b, cfg)
+        check_nnls(r["x"], r["inner_x"], r["final_grad"], r["residual_sq"], r["iterations"],
+                   r["termination"], r["trace"], g)
+    else:
+        start = g["start"] if "start" in g else None
+        r = oracle.solve_nqp(g["Q"], g["q"], cfg, start=start)
+        assert r["iterations"] == int(g["iterations"]) and r["termination"] == str(g["termination"])
+        assert same_bits(r["x"], g["x"]) and same_bits(r["final_grad"], g["final_grad"])
+        assert np.array_equal(r["mults"], g["mults"])
+        check_trace(r["trace"], g)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", GOLD, ids=[os.path.basename(p)[:-4] for p in GOLD])
+def test_gpu_matches_reference_golden(path, solver):
+    from paper_1502_01645_b200.api import SolverConfig
+    g = load(path)
+    name = os.path.basename(path)[:-4]
+    kw = dict(eval(str(g["cfg"])))
+    config = SolverConfig(epsilon=kw.get("epsilon"), max_iters=kw.get("max_iters"),
+                          stall_window=kw.get("stall_window", 50),
+                          trace_every=kw.get("trace_every", 1))
+    if str(g["kind"]) == "nnls":
+        A, b = inputs_of(name, g)
+        if instances.sha256(np.asfortranarray(A), b) != str(g["input_sha256"]):
+            pytest.skip("libm on this host draws different normals; inputs differ from fixture")
+        r = solver.solve_nnls(A, b, config)
+        check_nnls(r.x, r.inner.x, r.inner.final_grad, r.residual_sq, r.inner.iterations(),
+                   r.inner.termination, r.inner.trace, g)
+        assert [int(v) for v in g["dropped"]] == r.dropped_columns
+    else:
+        start = g["start"] if "start" in g else None
+        r = solver.solve_nqp(g["Q"], g["q"], config, start=start)
+        assert r.iterations() == int(g["iterations"]) and r.termination == str(g["termination"])
+        assert same_bits(r.x, g["x"]) and same_bits(r.final_grad, g["final_grad"])
+        assert np.array_equal(r.multiplies_per_iter, g["mults"])
+        check_trace(r.trace, g)
