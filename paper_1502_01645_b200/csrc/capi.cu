@@ -163,7 +163,8 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   double* g_alt = ENSURE(double, prod1, mp);
   double* xP = ENSURE(double, prod2, mp);
   double* qP = ENSURE(double, prod0, mp);
-  LoopCtrl* ctrl = ENSURE(LoopCtrl, ctrl, 1);
+  LoopCtrl* ctrl = ENSURE(LoopCtrl, ctrl, 2);  // [1] holds the grid-barrier words
+  unsigned int* bar = reinterpret_cast<unsigned int*>(ctrl + 1);
   const uint64_t tcap = r.max_iters / r.trace_every + 2;
   alnnls_iter_record* trace = ENSURE(alnnls_iter_record, trace, tcap);
   uint64_t mcap = 0;
@@ -220,6 +221,8 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   a.mults = mults;
   a.mults_cap = mcap;
   a.ctrl = ctrl;
+  a.bar = bar;
+  CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), ctx->stream));
   a.rows_per_cta = (int)ctx->qR;
   if (a.rows_per_cta > 352)
     return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: dimension too large for one GPU row split");

@@ -73,6 +73,44 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) { return __ldcg(p); }
 
+// ---- grid barrier for a cooperative (co-resident) launch ---------------------------
+// Sense-reversing barrier on two words in global memory ({count, generation}).
+// Waiters back off with __nanosleep so 147 spinning CTAs do not hammer the L2
+// slice the vector CTA also uses. All threads of every CTA must call it.
+struct GridBarrier {
+  unsigned int* count;
+  unsigned int* gen;
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_barrier(const GridBarrier& b, unsigned int& local_gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g = local_gen;
+    __threadfence();
+    const unsigned int arrived = atomicAdd(b.count, 1u);
+    if (arrived == gridDim.x - 1) {
+      atomicExch(b.count, 0u);
+      __threadfence();
+      atomicExch(b.gen, g + 1u);
+    } else {
+      unsigned int ns = 32;
+      while (ld_acquire_gpu(b.gen) == g) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
+      }
+    }
+    local_gen = g + 1u;
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // ---- block scan (exclusive) of one int per thread -----------------------------
 // Returns the exclusive prefix; *total gets the block sum. Uses `scratch`
 // (>= 33 ints of shared memory). All threads of the block must call it.

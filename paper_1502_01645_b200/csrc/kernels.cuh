@@ -59,6 +59,7 @@ struct LoopArgs {
   uint64_t* mults;  // may be null
   uint64_t mults_cap;
   LoopCtrl* ctrl;
+  unsigned int* bar;  // grid barrier words {count, generation}, zeroed before launch
   int rows_per_cta;
 };
 

@@ -53,6 +53,7 @@ struct LeaderState {
   unsigned long long ph[8];
   double red[kWarps];
   int scan[40];
+  int cnt[8 * kWarps + 1];  // kU x kWarps warp counts / offsets + total
 };
 
 __device__ __forceinline__ void chunk(int len, int& lo, int& hi) {
@@ -137,67 +138,107 @@ __device__ void leader_chains(double* sbuf, size_t sbuf_bytes, LeaderState& L, i
   __syncthreads();
 }
 
+// Ordered block compaction: positions are processed in super-rounds of kU
+// rounds x blockDim consecutive positions (thread t takes r*blockDim + t), so a
+// warp's selected entries land at consecutive output positions (coalesced
+// stores); order = ascending position. Warp counts of the kU rounds are
+// scanned together by warp 0.
+constexpr int kU = 8;
+constexpr int kSuper = kLoopThreads * kU;
+
+__device__ __forceinline__ int super_scan(LeaderState& L) {
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    constexpr int N = kU * kWarps;
+    constexpr int PER = (N + 31) / 32;
+    const int lane = threadIdx.x;
+    int v[PER], s = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int idx = lane * PER + j;
+      v[j] = idx < N ? L.cnt[idx] : 0;
+      s += v[j];
+    }
+    int incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int ex = incl - s;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int idx = lane * PER + j;
+      if (idx < N) {
+        L.cnt[idx] = ex;
+        ex += v[j];
+      }
+    }
+    if (lane == 31) L.cnt[N] = incl;
+  }
+  __syncthreads();
+  return L.cnt[kU * kWarps];
+}
+
 // Passive mask P = {i : x_i > 0 || g_i < 0}, ascending (nqp.hpp:149-157), with
 // g_i = gcur_i (+ gd_i when `gd` is given: the incremental update of
 // nqp.hpp:313 evaluated on the fly). Writes mask, gP, xP, qP and min(x).
-// Tiles of kTile contiguous positions, 8 per thread, loaded with 16-byte loads
-// (all buffers are padded to a multiple of kTile).
-constexpr int kPer = 8;
-constexpr int kTile = kLoopThreads * kPer;
-
-__device__ __forceinline__ void ld8(double (&v)[kPer], const double* p, bool cg) {
-#pragma unroll
-  for (int k = 0; k < kPer; k += 2) {
-    const double2 d = cg ? __ldcg(reinterpret_cast<const double2*>(p + k))
-                         : *reinterpret_cast<const double2*>(p + k);
-    v[k] = d.x;
-    v[k + 1] = d.y;
-  }
-}
-
 __device__ void leader_build_mask(const LoopArgs& a, LeaderState& L, const double* gcur,
                                   const double* gd, double* min_x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
   int bad = 0, base = 0;
   double mn = __longlong_as_double(0x7ff0000000000000LL);
-  for (int tile = 0; tile < a.m; tile += kTile) {
-    const int i0 = tile + threadIdx.x * kPer;
-    double xv[kPer], gv[kPer], dv[kPer], qv[kPer];
-    ld8(xv, a.x + i0, false);
-    ld8(gv, gcur + i0, true);
-    if (gd) ld8(dv, gd + i0, true);
-    ld8(qv, a.q + i0, false);
-    unsigned flags = 0;
+  for (int s0 = 0; s0 < a.m; s0 += kSuper) {
+    double xv[kU], gv[kU], qv[kU];
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      if (i0 + k < a.m) {
-        if (gd) gv[k] = xadd(gv[k], dv[k]);
-        if (!isfinite(gv[k])) bad = 1;
-        mn = fmin(mn, xv[k]);
-        if (xv[k] > 0.0 || gv[k] < 0.0) flags |= 1u << k;
+    for (int k = 0; k < kU; ++k) {
+      const int i = s0 + k * kLoopThreads + threadIdx.x;
+      xv[k] = 0.0;
+      gv[k] = 0.0;
+      qv[k] = 0.0;
+      if (i < a.m) {
+        xv[k] = a.x[i];
+        gv[k] = __ldcg(gcur + i);
+        if (gd) gv[k] = xadd(gv[k], __ldcg(gd + i));
+        qv[k] = __ldg(a.q + i);
       }
     }
-    int total;
-    int off = base + block_exclusive_scan(__popc(flags), L.scan, &total);
+    unsigned sel = 0, wp[kU];
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      if (flags & (1u << k)) {
-        a.mask[off] = (uint32_t)(i0 + k);
-        a.gP[off] = gv[k];
-        a.xP[off] = xv[k];
-        a.qP[off] = qv[k];
-        ++off;
+    for (int k = 0; k < kU; ++k) {
+      const bool valid = s0 + k * kLoopThreads + (int)threadIdx.x < a.m;
+      const bool f = valid && (xv[k] > 0.0 || gv[k] < 0.0);
+      if (valid) {
+        if (!isfinite(gv[k])) bad = 1;
+        mn = fmin(mn, xv[k]);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      wp[k] = __popc(bal & lt);
+      if (lane == 0) L.cnt[k * kWarps + warp] = __popc(bal);
+      if (f) sel |= 1u << k;
+    }
+    const int total = super_scan(L);
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      if (sel & (1u << k)) {
+        const int pos = base + L.cnt[k * kWarps + warp] + (int)wp[k];
+        a.mask[pos] = (uint32_t)(s0 + k * kLoopThreads + threadIdx.x);
+        a.gP[pos] = gv[k];
+        a.xP[pos] = xv[k];
+        a.qP[pos] = qv[k];
       }
     }
     base += total;
+    __syncthreads();
   }
-  const int total = base;
   for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-  if ((threadIdx.x & 31) == 0) L.red[threadIdx.x >> 5] = mn;
+  if (lane == 0) L.red[warp] = mn;
   bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mn = fmin(mn, L.red[w]);
+    for (int w = 1; w < kWarps; ++w) mn = fmin(mn, L.red[w]);
     *min_x = mn;
-    a.ctrl->mask_len = total;
+    a.ctrl->mask_len = base;
     L.nonfinite = bad;
   }
   __syncthreads();
@@ -205,38 +246,54 @@ __device__ void leader_build_mask(const LoopArgs& a, LeaderState& L, const doubl
 
 // Candidate step on the mask and the changed set C (nqp.hpp:294-303).
 __device__ void leader_build_changed(const LoopArgs& a, LeaderState& L, int ml, double alpha) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
   int base = 0;
-  for (int tile = 0; tile < ml; tile += kTile) {
-    const int t0 = tile + threadIdx.x * kPer;
-    double xv[kPer], gv[kPer], cv[kPer];
-    ld8(xv, a.xP + t0, false);
-    ld8(gv, a.gP + t0, false);
-    unsigned flags = 0;
+  for (int s0 = 0; s0 < ml; s0 += kSuper) {
+    double xv[kU], gv[kU], cv[kU];
+    uint32_t iv[kU];
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
+    for (int k = 0; k < kU; ++k) {
+      const int t = s0 + k * kLoopThreads + threadIdx.x;
+      xv[k] = 0.0;
+      gv[k] = 0.0;
+      iv[k] = 0;
+      if (t < ml) {
+        xv[k] = a.xP[t];
+        gv[k] = a.gP[t];
+        iv[k] = a.mask[t];
+      }
+    }
+    unsigned sel = 0, wp[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const bool valid = s0 + k * kLoopThreads + (int)threadIdx.x < ml;
       double xi = xsub(xv[k], xmul(alpha, gv[k]));  // x - (alpha g), nqp.hpp:296
       if (xi < 0.0) xi = 0.0;
       cv[k] = xi;
-      if (t0 + k < ml && xi != xv[k]) flags |= 1u << k;
+      const bool f = valid && xi != xv[k];
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      wp[k] = __popc(bal & lt);
+      if (lane == 0) L.cnt[k * kWarps + warp] = __popc(bal);
+      if (f) sel |= 1u << k;
     }
-    int total;
-    int off = base + block_exclusive_scan(__popc(flags), L.scan, &total);
+    const int total = super_scan(L);
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      if (flags & (1u << k)) {
-        a.chg[off] = a.mask[t0 + k];
-        a.candC[off] = cv[k];
-        a.dC[off] = xsub(cv[k], xv[k]);
-        a.gC[off] = gv[k];
-        ++off;
+    for (int k = 0; k < kU; ++k) {
+      if (sel & (1u << k)) {
+        const int pos = base + L.cnt[k * kWarps + warp] + (int)wp[k];
+        a.chg[pos] = iv[k];
+        a.candC[pos] = cv[k];
+        a.dC[pos] = xsub(cv[k], xv[k]);
+        a.gC[pos] = gv[k];
       }
     }
     base += total;
+    __syncthreads();
   }
-  const int total = base;
   if (threadIdx.x == 0) {
-    a.ctrl->chg_len = total;
-    if (total > 0) L.mults += (unsigned long long)a.m * (unsigned long long)total;
+    a.ctrl->chg_len = base;
+    if (base > 0) L.mults += (unsigned long long)a.m * (unsigned long long)base;
   }
   __syncthreads();
 }
@@ -280,6 +337,8 @@ __device__ void stop_final(const LoopArgs& a, LeaderState& L, unsigned long long
 }
 
 __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
+  // cooperative-groups grid barrier (1.2 us measured; a nanosleep-backoff
+  // barrier in common.cuh measured slower here)
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ LeaderState L;
