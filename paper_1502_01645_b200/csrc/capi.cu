@@ -37,7 +37,7 @@ struct alnnls_ctx {
 
   DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
   DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
-      hvec, start, bcols, X;
+      hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part;
 
   // last solve
   bool last_nnls = false;
@@ -163,6 +163,16 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   double* g_alt = ENSURE(double, prod1, mp);
   double* xP = ENSURE(double, prod2, mp);
   double* qP = ENSURE(double, prod0, mp);
+  double* x_alt = ENSURE(double, x_alt, mp);
+  uint32_t* mask2 = ENSURE(uint32_t, mask2, mp);
+  double* gP2 = ENSURE(double, gP2, mp);
+  double* xP2 = ENSURE(double, xP2, mp);
+  double* qP2 = ENSURE(double, qP2, mp);
+  // per row-CTA partials: cnt (int), badv (int), minx (double)
+  double* part = ENSURE(double, part, 3 * 160);
+  int* cnt = reinterpret_cast<int*>(part);
+  int* badv = cnt + 160;
+  double* minx = part + 160;
   LoopCtrl* ctrl = ENSURE(LoopCtrl, ctrl, 2);  // [1] holds the grid-barrier words
   unsigned int* bar = reinterpret_cast<unsigned int*>(ctrl + 1);
   const uint64_t tcap = r.max_iters / r.trace_every + 2;
@@ -210,6 +220,14 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   a.g_alt = g_alt;
   a.xP = xP;
   a.qP = qP;
+  a.x_alt = x_alt;
+  a.mask2 = mask2;
+  a.gP2 = gP2;
+  a.xP2 = xP2;
+  a.qP2 = qP2;
+  a.cnt = cnt;
+  a.badv = badv;
+  a.minx = minx;
   a.eps = r.eps;
   a.max_iters = r.max_iters;
   a.has_time_cap = cfg->has_time_cap;
@@ -316,7 +334,8 @@ int run_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t
       ctx->last = sum;
       return rc;
     }
-    CK(cudaMemcpyAsync(y, ctx->x.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(y, ctx->g_parity ? ctx->x_alt.p : ctx->x.p, sizeof(double) * m,
+                       cudaMemcpyDeviceToDevice, s));
   } else {
     // detail::empty_solve_result (nnls.hpp:107-113)
     alnnls_iter_record rec{};
@@ -434,7 +453,8 @@ void alnnls_destroy(alnnls_ctx* ctx) {
                     &ctx->diag,   &ctx->pos,   &ctx->scale,   &ctx->retained, &ctx->mscalar,
                     &ctx->trace,  &ctx->mults, &ctx->ctrl,    &ctx->list,  &ctx->vals, &ctx->ax,
                     &ctx->resid,  &ctx->flag,  &ctx->H,       &ctx->hvec,  &ctx->start, &ctx->bcols,
-                    &ctx->X};
+                    &ctx->X,      &ctx->x_alt, &ctx->mask2,   &ctx->gP2,   &ctx->xP2,  &ctx->qP2,
+                    &ctx->part};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
@@ -574,14 +594,16 @@ int alnnls_get_x(alnnls_ctx* ctx, double* x, uint64_t len) {
   if (!ctx || !x) return ALNNLS_EINVAL;
   const uint64_t n = ctx->last_nnls ? ctx->last_n : ctx->last_m;
   if (len < n) return set_err(ctx, ALNNLS_ECAPACITY, "get_x: buffer too small");
-  const void* src = ctx->last_nnls ? ctx->X.p : ctx->x.p;
+  const void* src = ctx->last_nnls ? ctx->X.p : (ctx->g_parity ? ctx->x_alt.p : ctx->x.p);
   return copy_out(ctx, x, src, sizeof(double) * n);
 }
 
 int alnnls_get_inner_x(alnnls_ctx* ctx, double* y, uint64_t len) {
   if (!ctx || !y) return ALNNLS_EINVAL;
   if (len < ctx->last_m) return set_err(ctx, ALNNLS_ECAPACITY, "get_inner_x: buffer too small");
-  return copy_out(ctx, y, ctx->last_nnls ? ctx->y_out.p : ctx->x.p, sizeof(double) * ctx->last_m);
+  return copy_out(ctx, y,
+                  ctx->last_nnls ? ctx->y_out.p : (ctx->g_parity ? ctx->x_alt.p : ctx->x.p),
+                  sizeof(double) * ctx->last_m);
 }
 
 int alnnls_get_final_grad(alnnls_ctx* ctx, double* g, uint64_t len) {

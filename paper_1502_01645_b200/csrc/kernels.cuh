@@ -25,6 +25,8 @@ struct LoopCtrl {
   double f_final;
   double gbs_final;
   int state;        // leader -> grid broadcast after a barrier (LoopState)
+  int act;          // phase-A decision: continue / stop / roll back the pending step
+  int state2;       // phase-B decision: P2 / no move / stop
   int g_parity;     // which gradient buffer holds the maintained gradient
   unsigned long long phase_ns[8];  // accumulated leader-side phase times
 };
@@ -47,6 +49,14 @@ struct LoopArgs {
   double* gC;       // g on the changed set (m)
   double* xP;       // x on the mask (m)
   double* qP;       // q on the mask (m)
+  double* x_alt;    // x ping-pong buffer 1 (row CTAs own x and g)
+  uint32_t* mask2;  // second passive-list set (ping-pong for the speculative step)
+  double* gP2;
+  double* xP2;
+  double* qP2;
+  int* cnt;         // per row-CTA passive counts
+  double* minx;     // per row-CTA min(x)
+  int* badv;        // per row-CTA non-finite gradient flags
   // resolved SolverConfig (nqp.hpp:219-222)
   double eps;
   uint64_t max_iters;

@@ -49,6 +49,7 @@ struct LeaderState {
   unsigned long long mults;
   int nonfinite;
   int tries;
+  int mask_len;
   unsigned long long t_mark;
   unsigned long long ph[8];
   double red[kWarps];
@@ -180,72 +181,12 @@ __device__ __forceinline__ int super_scan(LeaderState& L) {
   return L.cnt[kU * kWarps];
 }
 
-// Passive mask P = {i : x_i > 0 || g_i < 0}, ascending (nqp.hpp:149-157), with
-// g_i = gcur_i (+ gd_i when `gd` is given: the incremental update of
-// nqp.hpp:313 evaluated on the fly). Writes mask, gP, xP, qP and min(x).
-__device__ void leader_build_mask(const LoopArgs& a, LeaderState& L, const double* gcur,
-                                  const double* gd, double* min_x) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  int bad = 0, base = 0;
-  double mn = __longlong_as_double(0x7ff0000000000000LL);
-  for (int s0 = 0; s0 < a.m; s0 += kSuper) {
-    double xv[kU], gv[kU], qv[kU];
-#pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      const int i = s0 + k * kLoopThreads + threadIdx.x;
-      xv[k] = 0.0;
-      gv[k] = 0.0;
-      qv[k] = 0.0;
-      if (i < a.m) {
-        xv[k] = a.x[i];
-        gv[k] = __ldcg(gcur + i);
-        if (gd) gv[k] = xadd(gv[k], __ldcg(gd + i));
-        qv[k] = __ldg(a.q + i);
-      }
-    }
-    unsigned sel = 0, wp[kU];
-#pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      const bool valid = s0 + k * kLoopThreads + (int)threadIdx.x < a.m;
-      const bool f = valid && (xv[k] > 0.0 || gv[k] < 0.0);
-      if (valid) {
-        if (!isfinite(gv[k])) bad = 1;
-        mn = fmin(mn, xv[k]);
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
-      wp[k] = __popc(bal & lt);
-      if (lane == 0) L.cnt[k * kWarps + warp] = __popc(bal);
-      if (f) sel |= 1u << k;
-    }
-    const int total = super_scan(L);
-#pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      if (sel & (1u << k)) {
-        const int pos = base + L.cnt[k * kWarps + warp] + (int)wp[k];
-        a.mask[pos] = (uint32_t)(s0 + k * kLoopThreads + threadIdx.x);
-        a.gP[pos] = gv[k];
-        a.xP[pos] = xv[k];
-        a.qP[pos] = qv[k];
-      }
-    }
-    base += total;
-    __syncthreads();
-  }
-  for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-  if (lane == 0) L.red[warp] = mn;
-  bad = __syncthreads_or(bad);
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < kWarps; ++w) mn = fmin(mn, L.red[w]);
-    *min_x = mn;
-    a.ctrl->mask_len = base;
-    L.nonfinite = bad;
-  }
-  __syncthreads();
-}
-
 // Candidate step on the mask and the changed set C (nqp.hpp:294-303).
-__device__ void leader_build_changed(const LoopArgs& a, LeaderState& L, int ml, double alpha) {
+struct ListSet;
+__device__ void leader_build_changed(const LoopArgs& a, LeaderState& L, int ml, double alpha,
+                                     const struct ListSet& ls);
+__device__ void leader_build_changed_impl(const LoopArgs& a, LeaderState& L, int ml, double alpha,
+                                          const uint32_t* mask, const double* gP, const double* xP) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   int base = 0;
@@ -259,9 +200,9 @@ __device__ void leader_build_changed(const LoopArgs& a, LeaderState& L, int ml, 
       gv[k] = 0.0;
       iv[k] = 0;
       if (t < ml) {
-        xv[k] = a.xP[t];
-        gv[k] = a.gP[t];
-        iv[k] = a.mask[t];
+        xv[k] = xP[t];
+        gv[k] = gP[t];
+        iv[k] = mask[t];
       }
     }
     unsigned sel = 0, wp[kU];
@@ -317,24 +258,210 @@ __device__ void write_record(const LoopArgs& a, unsigned long long k, double f, 
 }
 
 // Stepped-iteration bookkeeping (nqp.hpp:319-326). Vector CTA thread 0.
-__device__ void finish_step(const LoopArgs& a, LeaderState& L, unsigned long long k, int ml,
-                            double min_x) {
-  if (a.m && min_x < a.ctrl->min_iterate) a.ctrl->min_iterate = min_x;
-  if (k % a.trace_every == 0) write_record(a, k, L.f, L.gbs, ml, L.elapsed, L.alpha, 1);
+__device__ void push_step(const LoopArgs& a, unsigned long long k, double f, double gbs, int ml,
+                          double el, double alpha, unsigned long long mults) {
+  if (k % a.trace_every == 0) write_record(a, k, f, gbs, ml, el, alpha, 1);
   const unsigned long long idx = a.ctrl->mult_len;
-  if (a.mults && idx < a.mults_cap) a.mults[idx] = L.mults;
+  if (a.mults && idx < a.mults_cap) a.mults[idx] = mults;
   a.ctrl->mult_len = idx + 1;
-  a.ctrl->mult_total += L.mults;
+  a.ctrl->mult_total += mults;
 }
 
-__device__ void stop_final(const LoopArgs& a, LeaderState& L, unsigned long long k, int ml,
-                           int term) {
-  write_record(a, k, L.f, L.gbs, ml, L.elapsed, 0.0, 0);
+__device__ void stop_final(const LoopArgs& a, unsigned long long k, double f, double gbs, int ml,
+                           double el, int term) {
+  write_record(a, k, f, gbs, ml, el, 0.0, 0);
   a.ctrl->termination = term;
   a.ctrl->iterations = k;
-  a.ctrl->f_final = L.f;
-  a.ctrl->gbs_final = L.gbs;
+  a.ctrl->f_final = f;
+  a.ctrl->gbs_final = gbs;
 }
+
+// ---- row-CTA phases: own x and g, build the passive-mask lists in parallel ----------
+struct ListSet {
+  uint32_t* mask;
+  double* gP;
+  double* xP;
+  double* qP;
+};
+
+__device__ void leader_build_changed(const LoopArgs& a, LeaderState& L, int ml, double alpha,
+                                     const ListSet& ls) {
+  leader_build_changed_impl(a, L, ml, alpha, ls.mask, ls.gP, ls.xP);
+}
+
+struct RowShared {
+  int wc[kWarps + 1];
+  double wm[kWarps];
+  int t_lo, t_hi, base, total;
+};
+
+// Passive flags of own rows of (x, g): count -> cnt[b], min(x) -> minx[b],
+// any non-finite g -> badv[b]. Whole row CTA.
+__device__ void row_count(const LoopArgs& a, RowShared& S, int blk, int row0, int nrows,
+                          const double* x, const double* g) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int c = 0, bad = 0;
+  double mn = __longlong_as_double(0x7ff0000000000000LL);
+  for (int t = threadIdx.x; t < nrows; t += blockDim.x) {
+    const double xi = x[row0 + t], gi = g[row0 + t];
+    c += (xi > 0.0 || gi < 0.0) ? 1 : 0;
+    if (!isfinite(gi)) bad = 1;
+    mn = fmin(mn, xi);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if (lane == 0) {
+    S.wc[warp] = c;
+    S.wm[warp] = mn;
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    double m2 = __longlong_as_double(0x7ff0000000000000LL);
+    for (int w = 0; w < kWarps; ++w) {
+      tot += S.wc[w];
+      m2 = fmin(m2, S.wm[w]);
+    }
+    a.cnt[blk] = tot;
+    a.minx[blk] = m2;
+    a.badv[blk] = bad;
+  }
+}
+
+// Speculative update of own rows (nqp.hpp:309-313): x_next = x with x[C] = cand,
+// g_next = g + gd; then row_count on the result.
+__device__ void row_apply(const LoopArgs& a, RowShared& S, int blk, int row0, int nrows,
+                          const double* xc, const double* gc, double* xn, double* gn, int cl) {
+  for (int t = threadIdx.x; t < nrows; t += blockDim.x) {
+    const int i = row0 + t;
+    gn[i] = xadd(gc[i], a.gd[i]);
+    xn[i] = xc[i];
+  }
+  if (threadIdx.x == 0) {  // own range of the ascending changed list
+    int lo = 0, hi = cl;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)__ldcg(a.chg + mid) < row0) lo = mid + 1; else hi = mid;
+    }
+    int lo2 = lo, hi2 = cl;
+    while (lo2 < hi2) {
+      const int mid = (lo2 + hi2) >> 1;
+      if ((int)__ldcg(a.chg + mid) < row0 + nrows) lo2 = mid + 1; else hi2 = mid;
+    }
+    S.t_lo = lo;
+    S.t_hi = lo2;
+  }
+  __syncthreads();
+  for (int t = S.t_lo + threadIdx.x; t < S.t_hi; t += blockDim.x)
+    xn[__ldcg(a.chg + t)] = __ldcg(a.candC + t);
+  __syncthreads();
+  row_count(a, S, blk, row0, nrows, xn, gn);
+}
+
+// Writes own rows' entries of the ascending passive list at the global offset
+// sum(cnt[0..blk)). Returns the list length (sum of all cnt). Whole row CTA.
+__device__ int row_lists(const LoopArgs& a, RowShared& S, int blk, int nblk, int row0, int nrows,
+                         const double* x, const double* g, const ListSet& L) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    int before = 0, all = 0;
+    for (int b = lane; b < nblk; b += 32) {
+      const int c = __ldcg(a.cnt + b);
+      all += c;
+      if (b < blk) before += c;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      before += __shfl_xor_sync(0xffffffffu, before, o);
+      all += __shfl_xor_sync(0xffffffffu, all, o);
+    }
+    if (lane == 0) {
+      S.base = before;
+      S.total = all;
+    }
+  }
+  // one round: nrows <= blockDim.x (checked on the host)
+  const int t = threadIdx.x;
+  double xi = 0.0, gi = 0.0;
+  bool f = false;
+  if (t < nrows) {
+    xi = x[row0 + t];
+    gi = g[row0 + t];
+    f = xi > 0.0 || gi < 0.0;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, f);
+  if (lane == 0) S.wc[warp] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = S.base;
+    for (int w = 0; w < kWarps; ++w) {
+      const int c = S.wc[w];
+      S.wc[w] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (f) {
+    const int pos = S.wc[warp] + __popc(bal & ((1u << lane) - 1u));
+    L.mask[pos] = (uint32_t)(row0 + t);
+    L.gP[pos] = gi;
+    L.xP[pos] = xi;
+    L.qP[pos] = __ldg(a.q + row0 + t);
+  }
+  return S.total;
+}
+
+// ---- vector-CTA chains with per-chain lengths ------------------------------------------
+template <int K, class F>
+__device__ void leader_chains_var(double* sbuf, size_t sbuf_bytes, LeaderState& L,
+                                  const int (&len)[K], F prod) {
+  const int CH = min(1024, (int)(sbuf_bytes / (2 * K * sizeof(double))) & ~1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int mx = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) mx = max(mx, len[k]);
+  const int nch = (mx + CH - 1) / CH;
+  auto produce = [&](int c, int buf, int first_thread) {
+    const int b0 = c * CH;
+    double* dst = sbuf + (size_t)buf * K * CH;
+    for (int i = (int)threadIdx.x - first_thread; i < CH; i += blockDim.x - first_thread) {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (b0 + i < len[k]) dst[(size_t)k * CH + i] = prod(k, b0 + i);
+    }
+  };
+  double s = 0.0;
+  if (nch > 0) produce(0, 0, 0);
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    if (warp < K) {
+      if (lane == 0) {
+        const int cnt = max(0, min(CH, len[warp] - c * CH));
+        s = smem_chain(s, sbuf + (size_t)(c & 1) * K * CH + (size_t)warp * CH, cnt);
+      }
+    } else if (c + 1 < nch) {
+      produce(c + 1, (c + 1) & 1, K * 32);
+    }
+    __syncthreads();
+  }
+  if (warp < K && lane == 0) L.res[warp] = s;
+  __syncthreads();
+}
+
+enum LoopAct { kActCont = 1, kActStop = 2, kActRollback = 3 };
+enum LoopState2 { kS2P2 = 1, kS2NoMove = 2, kS2Stop = 3 };
+
+// Speculation state of the vector CTA: the last stepped iteration is applied
+// before its df (nqp.hpp:307-308) is known; df runs during the next P1 and a
+// rejection (rare: the halving safeguard) rolls the step back.
+struct Pending {
+  int on;
+  unsigned long long k;
+  double f, gbs, el, alpha;
+  int ml, cl, tries;
+  unsigned long long mults;
+};
 
 __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
   // cooperative-groups grid barrier (1.2 us measured; a nanosleep-backoff
@@ -342,9 +469,12 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ LeaderState L;
+  __shared__ Pending PD;
+  __shared__ RowShared RS;
   __shared__ double s_min_x;
   const bool leader = blockIdx.x == 0;
   const int R = a.rows_per_cta;
+  const int nblk = (int)gridDim.x - 1;
   const int blk = (int)blockIdx.x - 1;
   const int row0 = leader ? 0 : blk * R;
   const int nrows = leader ? 0 : max(0, min(a.m - row0, R));
@@ -353,62 +483,94 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
   if (!leader) ring_setup(ring, smem, kRingSmemBytes, nrows, R, kWarps);
   double* sbuf = reinterpret_cast<double*>(smem);
   volatile LoopCtrl* vc = a.ctrl;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* gbuf[2] = {a.g, a.g_alt};
-  int par = 0;
+  double* xb[2] = {a.x, a.x_alt};
+  double* gb[2] = {a.g, a.g_alt};
+  const ListSet ls[2] = {{a.mask, a.gP, a.xP, a.qP}, {a.mask2, a.gP2, a.xP2, a.qP2}};
+  int xp = 0, lp = 0;      // state / list parity (identical in every CTA)
+  int ml_l[2] = {0, 0};    // list lengths per parity (row CTAs)
 
+  // ---- prologue: passive lists of the start point ---------------------------------------
   const uint64_t t0 = globaltimer_ns();
-  if (leader) {
-    if (threadIdx.x == 0) {
-      a.ctrl->trace_len = 0;
-      a.ctrl->mult_len = 0;
-      a.ctrl->mult_total = 0;
-      a.ctrl->numeric_failure = 0;
-      a.ctrl->stop = 0;
-      a.ctrl->g_parity = 0;
-      L.best_gbs = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-      L.since_best = 0;
-      L.t_mark = t0;
-      for (int i = 0; i < 8; ++i) L.ph[i] = 0;
-    }
-    leader_build_mask(a, L, gbuf[0], nullptr, &s_min_x);
-    if (threadIdx.x == 0) a.ctrl->min_iterate = a.m ? s_min_x : 0.0;  // nqp.hpp:237
-    __threadfence();
+  if (!leader) row_count(a, RS, blk, row0, nrows, xb[0], gb[0]);
+  grid.sync();
+  if (!leader) ml_l[0] = row_lists(a, RS, blk, nblk, row0, nrows, xb[0], gb[0], ls[0]);
+  if (leader && threadIdx.x == 0) {
+    a.ctrl->trace_len = 0;
+    a.ctrl->mult_len = 0;
+    a.ctrl->mult_total = 0;
+    a.ctrl->numeric_failure = 0;
+    a.ctrl->g_parity = 0;
+    L.best_gbs = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    L.since_best = 0;
+    L.t_mark = t0;
+    for (int i = 0; i < 8; ++i) L.ph[i] = 0;
+    PD.on = 0;
   }
   grid.sync();
+  if (leader && threadIdx.x == 0) {  // min_iterate starts at min(start) (nqp.hpp:237)
+    double mn = __longlong_as_double(0x7ff0000000000000LL);
+    for (int b = 0; b < nblk; ++b) mn = fmin(mn, __ldcg(a.minx + b));
+    a.ctrl->min_iterate = a.m ? mn : 0.0;
+  }
 
-  for (unsigned long long k = 0;; ++k) {
-    const int ml = vc->mask_len;
-    // ---- P1 (row CTAs) || stop-test chains (vector CTA) ----------------------------------
+  unsigned long long k = 0;  // iteration whose stop test runs next (vector CTA)
+  for (;;) {
+    // ===== phase A: P1 (row CTAs) || stop-test chains + pending df (vector CTA) =====
     if (!leader) {
-      gemv_rows(ring, qblk, R, true, row0, nrows, a.mask, a.gP, ml, a.u);
+      gemv_rows(ring, qblk, R, true, row0, nrows, ls[lp].mask, ls[lp].gP, ml_l[lp], a.u);
     } else {
-      const double *gP = a.gP, *xP = a.xP, *qP = a.qP;
-      leader_chains<3>(sbuf, kRingSmemBytes, L, ml, [&](int c, int t) {
-        // gbs: g_i^2; dot(x, grad): x_i g_i; dot(q, x): q_i x_i (terms off the
-        // mask are exact zeros since x_i = 0 there)
-        return c == 0 ? xmul(gP[t], gP[t]) : (c == 1 ? xmul(xP[t], gP[t]) : xmul(qP[t], xP[t]));
+      __shared__ int s_ml, s_bad;
+      __shared__ double s_mn;
+      if (threadIdx.x < 32) {  // gather the row CTAs' partials of the current state
+        int c = 0, bd = 0;
+        double mn = __longlong_as_double(0x7ff0000000000000LL);
+        for (int b = threadIdx.x; b < nblk; b += 32) {
+          c += __ldcg(a.cnt + b);
+          bd |= __ldcg(a.badv + b);
+          mn = fmin(mn, __ldcg(a.minx + b));
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          c += __shfl_xor_sync(0xffffffffu, c, o);
+          bd |= __shfl_xor_sync(0xffffffffu, bd, o);
+          mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        }
+        if (threadIdx.x == 0) {
+          s_ml = c;
+          s_bad = bd;
+          s_mn = mn;
+        }
+      }
+      __syncthreads();
+      const int ml = s_ml;
+      const ListSet cur = ls[lp];
+      const int lens[4] = {ml, ml, ml, PD.on ? PD.cl : 0};
+      const double *gP = cur.gP, *xP = cur.xP, *qP = cur.qP;
+      const double *gC = a.gC, *dC = a.dC, *gd = a.gd;
+      const uint32_t* chg = a.chg;
+      // gbs: g_i^2; dot(x, grad): x_i g_i; dot(q, x): q_i x_i (terms off the mask are
+      // exact zeros since x_i = 0 there); df of the pending step (nqp.hpp:307)
+      leader_chains_var<4>(sbuf, kRingSmemBytes, L, lens, [&](int c, int t) {
+        if (c == 0) return xmul(gP[t], gP[t]);
+        if (c == 1) return xmul(xP[t], gP[t]);
+        if (c == 2) return xmul(qP[t], xP[t]);
+        return xmul(xadd(gC[t], xmul(0.5, __ldcg(gd + chg[t]))), dC[t]);
       });
       if (threadIdx.x == 0) {
-        L.gbs = L.res[0];
+        const double gbs = L.res[0];
         const double f = xmul(0.5, xadd(L.res[1], L.res[2]));
-        const double gbs = L.gbs;
-        const double elapsed = (double)(globaltimer_ns() - t0) * 1e-9;
-        L.f = f;
-        L.elapsed = elapsed;
-        L.mults = 0;
-        L.tries = 0;
+        const double el = (double)(globaltimer_ns() - t0) * 1e-9;
+        const double best0 = L.best_gbs;
+        const unsigned long long since0 = L.since_best;
         int stop = -1;
-        if (L.nonfinite || !isfinite(f) || !isfinite(gbs)) {
-          a.ctrl->numeric_failure = 1;
-          stop = 100;
+        if (s_bad || !isfinite(f) || !isfinite(gbs)) {
+          stop = 100;  // NumericFailure (nqp.hpp:257-259)
         } else if (ml == 0) {
           stop = ALNNLS_EMPTY_PASSIVE_SET;
         } else if (gbs < a.eps) {
           stop = ALNNLS_GRADIENT_BELOW_EPSILON;
         } else if (k >= a.max_iters) {
           stop = ALNNLS_MAX_ITERS;
-        } else if (a.has_time_cap && elapsed >= a.time_cap_s) {
+        } else if (a.has_time_cap && el >= a.time_cap_s) {
           stop = ALNNLS_TIME_CAP;
         } else if (gbs < L.best_gbs) {
           L.best_gbs = gbs;
@@ -417,113 +579,136 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
           stop = ALNNLS_STALLED;
         }
         if (stop < 0 && !(gbs != 0.0)) stop = ALNNLS_ZERO_CURVATURE;  // num == 0 (nqp.hpp:167)
-        if (stop >= 0 && stop != 100) stop_final(a, L, k, ml, stop);
-        a.ctrl->stop = stop >= 0 ? 1 : 0;
-        phase_mark(L, 0);  // [0] stop-test chains
+        int act = stop >= 0 ? kActStop : kActCont;
+        if (PD.on) {
+          const double df = L.res[3];
+          if (!(df <= 0.0 || PD.tries >= 60)) {  // reject: roll back (nqp.hpp:316-317)
+            L.best_gbs = best0;
+            L.since_best = since0;
+            PD.alpha = xmul(PD.alpha, 0.5);
+            ++PD.tries;
+            act = kActRollback;
+          } else {  // accept the pending step: its bookkeeping is now final
+            if (a.m && s_mn < a.ctrl->min_iterate) a.ctrl->min_iterate = s_mn;
+            push_step(a, PD.k, PD.f, PD.gbs, PD.ml, PD.el, PD.alpha, PD.mults);
+            PD.on = 0;
+          }
+        }
+        if (act == kActStop) {
+          if (stop == 100) a.ctrl->numeric_failure = 1;
+          else stop_final(a, k, f, gbs, ml, el, stop);
+        }
+        L.f = f;
+        L.gbs = gbs;
+        L.elapsed = el;
+        L.mask_len = ml;
+        a.ctrl->act = act;
+        phase_mark(L, 0);
         __threadfence();
       }
     }
-    grid.sync();
-    if (leader && threadIdx.x == 0) phase_mark(L, 1);  // [1] rest of P1 + barrier
-    if (vc->stop) break;
+    grid.sync();  // B1
+    const int act = vc->act;
+    if (act == kActStop) break;
+    if (act == kActRollback) {  // back to the state before the rejected step
+      xp ^= 1;
+      lp ^= 1;
+    }
+    if (leader && threadIdx.x == 0) phase_mark(L, 1);
 
-    // ---- D/C: den chain, alpha, changed set (vector CTA) --------------------------------
+    // ===== phase B (vector CTA): den chain, alpha, changed set ==========================
     if (leader) {
-      const double *gP = a.gP, *u = a.u;
-      const uint32_t* mask = a.mask;
-      leader_chains<1>(sbuf, kRingSmemBytes, L, ml,
-                       [&](int, int t) { return xmul(gP[t], __ldcg(u + mask[t])); });
-      if (threadIdx.x == 0) {
-        const double den = L.res[0];
-        L.mults += (unsigned long long)a.m * (unsigned long long)ml;
-        if (!(den > 0.0)) {
-          stop_final(a, L, k, ml, ALNNLS_ZERO_CURVATURE);
-          L.alpha = -1.0;
-        } else {
-          L.alpha = xdiv(L.gbs, den);
+      const ListSet cur = ls[lp];
+      __shared__ int s_zc;
+      if (act == kActCont) {
+        const int ml = L.mask_len;
+        const double* gP = cur.gP;
+        const uint32_t* mask = cur.mask;
+        const double* u = a.u;
+        leader_chains<1>(sbuf, kRingSmemBytes, L, ml,
+                         [&](int, int t) { return xmul(gP[t], __ldcg(u + mask[t])); });
+        if (threadIdx.x == 0) {
+          const double den = L.res[0];
+          L.mults = (unsigned long long)a.m * (unsigned long long)ml;
+          L.tries = 0;
+          s_zc = !(den > 0.0);
+          if (s_zc) stop_final(a, k, L.f, L.gbs, ml, L.elapsed, ALNNLS_ZERO_CURVATURE);
+          else L.alpha = xdiv(L.gbs, den);
+          phase_mark(L, 2);
         }
-        phase_mark(L, 2);  // [2] den chain
+      } else if (threadIdx.x == 0) {
+        s_zc = 0;
+        L.alpha = PD.alpha;
+        L.mask_len = PD.ml;
       }
       __syncthreads();
-      const bool zc = L.alpha < 0.0;
-      if (!zc) leader_build_changed(a, L, ml, L.alpha);
-      if (threadIdx.x == 0) {
-        a.ctrl->state = zc ? kStateStop : (a.ctrl->chg_len == 0 ? kStateNoMove : kStateP2);
-        phase_mark(L, 3);  // [3] changed set
-        __threadfence();
-      }
-    }
-    grid.sync();
-    int state = vc->state;
-    if (state == kStateStop) break;
-
-    // ---- halving loop: P2, then the df decision -----------------------------------------
-    while (state == kStateP2) {
-      const int cl = vc->chg_len;
-      if (!leader) gemv_rows(ring, qblk, R, true, row0, nrows, a.chg, a.dC, cl, a.gd);
-      grid.sync();
-      if (!leader) {
-        // speculative U on own rows: g_next = g + gd (nqp.hpp:313); harmless if rejected
-        const double* gc = gbuf[par];
-        double* gn = gbuf[par ^ 1];
-        for (int t = threadIdx.x; t < nrows; t += blockDim.x) {
-          const int i = row0 + t;
-          gn[i] = xadd(gc[i], a.gd[i]);
-        }
-      } else {
-        if (threadIdx.x == 0) phase_mark(L, 4);  // [4] barrier + P2 + barrier
-        const double *gC = a.gC, *dC = a.dC, *gd = a.gd;
-        const uint32_t* chg = a.chg;
-        leader_chains<1>(sbuf, kRingSmemBytes, L, cl, [&](int, int t) {
-          return xmul(xadd(gC[t], xmul(0.5, __ldcg(gd + chg[t]))), dC[t]);
-        });
-        if (threadIdx.x == 0) {
-          const double df = L.res[0];
-          const int accept = (df <= 0.0 || L.tries >= 60) ? 1 : 0;  // nqp.hpp:308
-          a.ctrl->accept = accept;
-          if (!accept) {
-            L.alpha = xmul(L.alpha, 0.5);  // nqp.hpp:317
-            ++L.tries;
-          }
-          phase_mark(L, 5);  // [5] df chain
+      __shared__ unsigned long long s_m0;
+      if (!s_zc) {
+        if (threadIdx.x == 0) {  // den-pass multiplies; build_changed adds m*|C| to L.mults
+          s_m0 = L.mults;
+          L.mults = 0;
         }
         __syncthreads();
-        if (a.ctrl->accept) {
-          // x[C] = cand (nqp.hpp:309-311); x is private to the vector CTA
-          for (int t = threadIdx.x; t < cl; t += blockDim.x) a.x[a.chg[t]] = a.candC[t];
-          __syncthreads();
-          leader_build_mask(a, L, gbuf[par], a.gd, &s_min_x);
-          if (threadIdx.x == 0) {
-            finish_step(a, L, k, ml, s_min_x);
-            a.ctrl->state = kStateNext;
-          }
-        } else {
-          leader_build_changed(a, L, ml, L.alpha);
-          if (threadIdx.x == 0)
-            a.ctrl->state = a.ctrl->chg_len == 0 ? kStateNoMove : kStateP2;  // nqp.hpp:304
-        }
+        const unsigned long long m0 = s_m0;
+        leader_build_changed(a, L, L.mask_len, L.alpha, cur);
         if (threadIdx.x == 0) {
-          phase_mark(L, 6);  // [6] update + next mask
-          __threadfence();
+          const int cl = a.ctrl->chg_len;
+          if (act == kActCont) {
+            L.mults += m0;
+            if (cl == 0) {  // nothing moved (nqp.hpp:304): step recorded, state unchanged
+              push_step(a, k, L.f, L.gbs, L.mask_len, L.elapsed, L.alpha, L.mults);
+            } else {        // speculate: apply now, check df during the next P1
+              PD.on = 1;
+              PD.k = k;
+              PD.f = L.f;
+              PD.gbs = L.gbs;
+              PD.el = L.elapsed;
+              PD.ml = L.mask_len;
+              PD.alpha = L.alpha;
+              PD.tries = 0;
+              PD.mults = L.mults;
+            }
+            ++k;
+          } else {
+            PD.mults += L.mults;
+            if (cl == 0) {  // halving made the step vanish: record it unchanged
+              push_step(a, PD.k, PD.f, PD.gbs, PD.ml, PD.el, PD.alpha, PD.mults);
+              PD.on = 0;
+            }
+          }
+          PD.cl = cl;
+          a.ctrl->state2 = cl == 0 ? kS2NoMove : kS2P2;
         }
+      } else if (threadIdx.x == 0) {
+        a.ctrl->state2 = kS2Stop;
       }
-      grid.sync();
-      if (leader && threadIdx.x == 0) phase_mark(L, 7);  // [7] final barrier
-      state = vc->state;
-      if (state == kStateNext) par ^= 1;
-    }
-    if (state == kStateNoMove) {
-      // no coordinate moved: x and g are unchanged, so the mask lists stay valid
-      if (leader && threadIdx.x == 0) {
-        finish_step(a, L, k, ml, a.ctrl->min_iterate);
-        a.ctrl->mask_len = ml;
+      if (threadIdx.x == 0) {
+        phase_mark(L, 3);
         __threadfence();
       }
-      grid.sync();
     }
+    grid.sync();  // B_C
+    const int st2 = vc->state2;
+    if (st2 == kS2Stop) break;
+    if (st2 == kS2NoMove) continue;
+
+    // ===== P2, speculative update, next passive lists ====================================
+    const int cl = vc->chg_len;
+    if (!leader) gemv_rows(ring, qblk, R, true, row0, nrows, a.chg, a.dC, cl, a.gd);
+    grid.sync();  // B2
+    if (leader && threadIdx.x == 0) phase_mark(L, 4);
+    if (!leader) row_apply(a, RS, blk, row0, nrows, xb[xp], gb[xp], xb[xp ^ 1], gb[xp ^ 1], cl);
+    grid.sync();  // B_cnt
+    if (leader && threadIdx.x == 0) phase_mark(L, 5);
+    if (!leader)
+      ml_l[lp ^ 1] = row_lists(a, RS, blk, nblk, row0, nrows, xb[xp ^ 1], gb[xp ^ 1], ls[lp ^ 1]);
+    grid.sync();  // B0
+    if (leader && threadIdx.x == 0) phase_mark(L, 6);
+    xp ^= 1;
+    lp ^= 1;
   }
   if (leader && threadIdx.x == 0) {
-    a.ctrl->g_parity = par;
+    a.ctrl->g_parity = xp;
     for (int i = 0; i < 8; ++i) a.ctrl->phase_ns[i] = L.ph[i];
   }
 }

@@ -20,10 +20,33 @@ __global__ void __launch_bounds__(384, 1) k(const double* Qb, int m, int R, cons
   double* vb = data + (size_t)S * G * seg;
   const int cw = (nrows + 31) / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) { for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], cw); mbar_init(&mfull[s], 12 - P - cw); } fence_mbar_init(); }
+  if (threadIdx.x == 0) { for (int s = 0; s < S; ++s) { mbar_init(&full[s], MODE == 7 ? 32 : 1); mbar_init(&empty[s], cw); mbar_init(&mfull[s], 12 - P - cw); } fence_mbar_init(); }
   __syncthreads();
   const int nst = (len + G - 1) / G;
-  if (MODE == 6 && warp < P) {
+  if (MODE == 7 && warp < P) {
+    // cp.async 16B producers on the blocked layout; one warp per stage; completion via
+    // cp.async.mbarrier.arrive.noinc (full barrier count = 32 lanes x producing warps)
+    const int ch = seg / 2;
+    for (int s = warp; s < nst; s += P) {
+      const int st = s % S; const uint32_t ph = (s / S) & 1u;
+      const int sbase = s * G; const int cnt = min(G, len - sbase);
+      uint32_t j0 = lane < cnt ? __ldg(list + sbase + lane) : 0u;
+      uint32_t j1 = lane + 32 < cnt ? __ldg(list + sbase + lane + 32) : 0u;
+      if (lane == 0) mbar_wait(&empty[st], ph ^ 1u);
+      __syncwarp();
+      double* dst = data + (size_t)st * G * seg;
+      const int tot = cnt * ch;
+      for (int e = lane; e < tot; e += 32) {
+        const int l = e / ch, c = e - l * ch;
+        const uint32_t jv = __shfl_sync(0xffffffffu, l < 32 ? j0 : j1, l & 31);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + (size_t)l * seg + 2 * c)),
+                     "l"(base + (size_t)jv * seg + 2 * c) : "memory");
+      }
+      if (lane < cnt) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(vb + (size_t)st * G + lane)), "l"(vals + sbase + lane) : "memory");
+      if (lane + 32 < cnt) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(vb + (size_t)st * G + lane + 32)), "l"(vals + sbase + lane + 32) : "memory");
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[st])) : "memory");
+    }
+  } else if (MODE == 6 && warp < P) {
     const int ch = seg / 2;  // 16B chunks per column
     for (int s = warp; s < nst; s += P) {
       const int st = s % S; const uint32_t ph = (s / S) & 1u;
@@ -60,9 +83,9 @@ __global__ void __launch_bounds__(384, 1) k(const double* Qb, int m, int R, cons
     for (int s = warp; s < nst; s += P) {
       const int st = s % S; const uint32_t ph = (s / S) & 1u;
       const int sbase = s * G; const int cnt = min(G, len - sbase);
-      if (lane == 0) { mbar_wait(&empty[st], ph ^ 1u); if (MODE == 2) mbar_arrive(&full[st]); else mbar_arrive_expect_tx(&full[st], (uint32_t)(cnt * seg * 8 + ((cnt + 1) & ~1) * 8)); }
+      if (lane == 0) { mbar_wait(&empty[st], ph ^ 1u); if (MODE == 2 || MODE == 8 || MODE == 10) mbar_arrive(&full[st]); else mbar_arrive_expect_tx(&full[st], (uint32_t)(cnt * seg * 8 + ((cnt + 1) & ~1) * 8)); }
       __syncwarp();
-      if (MODE == 2) continue;
+      if (MODE == 2 || MODE == 8 || MODE == 10) continue;
       double* dst = data + (size_t)st * G * seg;
       for (int l0 = 0; l0 < cnt; l0 += 32) {
         const int l = l0 + lane; const bool valid = l < cnt;
@@ -122,7 +145,19 @@ __global__ void __launch_bounds__(384, 1) k(const double* Qb, int m, int R, cons
       mbar_wait(&full[st], ph);
       const double* col = data + (size_t)st * G * seg; const double* v = vb + (size_t)st * G;
       if (MODE != 1) {
-        if ((MODE == 5 || MODE == 6) && cnt == 64) {
+        if ((MODE == 9 || MODE == 10) && cnt == 64) {
+          // pinned-order shared loads: all 64 issued before any product/add
+          const uint32_t cbase = smem_u32(col + tt), vbase = smem_u32(v);
+          double c[64], w[64];
+#pragma unroll
+          for (int l = 0; l < 64; ++l)
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(c[l]) : "r"(cbase + (uint32_t)(l * seg * 8)));
+#pragma unroll
+          for (int l = 0; l < 64; l += 2)
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w[l]), "=d"(w[l + 1]) : "r"(vbase + (uint32_t)(l * 8)));
+#pragma unroll
+          for (int l = 0; l < 64; ++l) acc = xadd(acc, xmul(c[l], w[l]));
+        } else if ((MODE == 5 || MODE == 6 || MODE == 7 || MODE == 8) && cnt == 64) {
           double p[64];
 #pragma unroll
           for (int l = 0; l < 64; ++l) p[l] = xmul(col[l * seg + tt], v[l]);
@@ -181,6 +216,8 @@ int main() {
     run(k<5>, "stage in regs", G, P);
     run(k<1>, "no MACs", G, P);
   }
-  for (int P : {4, 6, 8, 10}) run(k<6>, "ldg producers", 64, P);
+  run(k<8>, "consumer only (regs)", 64, 4);
+  run(k<10>, "consumer only (pinned)", 64, 4);
+  run(k<9>, "full pinned", 64, 4);
   return 0;
 }
