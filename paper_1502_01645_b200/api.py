@@ -241,6 +241,52 @@ class Solver:
                           timings={"setup_s": s.t_setup_s, "loop_s": s.t_loop_s,
                                    "finish_s": s.t_finish_s, "total_s": s.t_total_s})
 
+    def solve_nnls_batched(self, A, B, config: SolverConfig = SolverConfig()):
+        """solve_nnls(A, B[:, j], config) for every column j (bitwise, exact profile).
+        Returns (X (n x nrhs), [per-column dict], summary timings)."""
+        A = _fortran(A)
+        B = _fortran(B)
+        if A.shape[0] != B.shape[0]:
+            raise ValueError("solve_nnls: A and b dimension mismatch")
+        d, n = A.shape
+        k = B.shape[1]
+        X = np.zeros((n, k), order="F")
+        cols = (abi.ColumnResult * k)()
+        self._summary = abi.Summary()
+        cfg = config.to_abi(record_multiplies=False)
+        st = self.lib.alnnls_solve_nnls_batched(self.ctx, d, n, _ptr(A), k, _ptr(B), C.byref(cfg),
+                                                _ptr(X), C.cast(cols, C.c_void_p),
+                                                C.byref(self._summary))
+        if st != abi.OK:
+            self._raise(st, trace=[])
+        return X, [self._col(c) for c in cols], self._timings()
+
+    def solve_nnls_batched_device(self, A_ptr, B_ptr, X_ptr, d, n, nrhs,
+                                  config: SolverConfig = SolverConfig(), fetch_cols=True):
+        """Device-resident batched solve: A (d x n), B (d x nrhs), X (n x nrhs), column-major."""
+        cols = (abi.ColumnResult * nrhs)() if fetch_cols else None
+        self._summary = abi.Summary()
+        cfg = config.to_abi(record_multiplies=False)
+        st = self.lib.alnnls_solve_nnls_batched_device(
+            self.ctx, d, n, C.c_void_p(A_ptr), nrhs, C.c_void_p(B_ptr), C.byref(cfg),
+            C.c_void_p(X_ptr), C.cast(cols, C.c_void_p) if cols is not None else None,
+            C.byref(self._summary))
+        if st != abi.OK:
+            self._raise(st, trace=[])
+        return ([self._col(c) for c in cols] if cols is not None else None), self._timings()
+
+    @staticmethod
+    def _col(c):
+        return {"termination": TERMINATIONS[c.termination], "numeric_failure": bool(c.numeric_failure),
+                "iterations": int(c.iterations), "residual_sq": c.residual_sq, "f_final": c.f_final,
+                "gbs_final": c.gbs_final, "multiplies_total": int(c.multiplies_total)}
+
+    def _timings(self):
+        s = self._summary
+        return {"setup_s": s.t_setup_s, "loop_s": s.t_loop_s, "finish_s": s.t_finish_s,
+                "total_s": s.t_total_s, "multiplies_total": int(s.multiplies_total),
+                "iterations_total": int(s.iterations)}
+
     def solve_nqp(self, Q, q, config: SolverConfig = SolverConfig(), start=None):
         Q = _fortran(Q)
         q = np.ascontiguousarray(_f64(q, "q")).reshape(-1)

@@ -37,7 +37,7 @@ struct alnnls_ctx {
 
   DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
   DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
-      hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part;
+      hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb;
 
   // last solve
   bool last_nnls = false;
@@ -454,7 +454,7 @@ void alnnls_destroy(alnnls_ctx* ctx) {
                     &ctx->trace,  &ctx->mults, &ctx->ctrl,    &ctx->list,  &ctx->vals, &ctx->ax,
                     &ctx->resid,  &ctx->flag,  &ctx->H,       &ctx->hvec,  &ctx->start, &ctx->bcols,
                     &ctx->X,      &ctx->x_alt, &ctx->mask2,   &ctx->gP2,   &ctx->xP2,  &ctx->qP2,
-                    &ctx->part};
+                    &ctx->part,   &ctx->resb,  &ctx->yb,      &ctx->qb};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
@@ -855,18 +855,148 @@ int alnnls_matvec(alnnls_ctx* ctx, uint64_t rows, uint64_t cols, const double* M
   return alnnls_masked_matvec(ctx, rows, cols, M, v, all.data(), cols, y, nullptr);
 }
 
-int alnnls_solve_nnls_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A,
-                              uint64_t nrhs, const double* B, const alnnls_config* cfg, double* X,
-                              alnnls_column_result* cols, alnnls_summary* out) {
-  (void)d; (void)n; (void)A; (void)nrhs; (void)B; (void)cfg; (void)X; (void)cols; (void)out;
-  return set_err(ctx, ALNNLS_EINVAL, "batched solve not built yet");
+}  // extern "C"
+
+namespace {
+
+// K8 pipeline on device A (d x n, lda) and B (d x nrhs, ldb): per column bitwise
+// solve_nnls(A, B[:, j], cfg). X (n x nrhs, ld n) and per-column results.
+int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t lda,
+                uint64_t nrhs, const double* dB, uint64_t ldb, const alnnls_config* cfg,
+                double* dX, alnnls_column_result* cols, alnnls_summary* out) {
+  int st__ = ALNNLS_OK;
+  cudaStream_t s = ctx->stream;
+  alnnls_summary sum{};
+  CK(cudaEventRecord(ctx->ev[0], s));
+  uint64_t m = 0;
+  int rc = run_setup(ctx, d, n, dA, lda, nullptr, &m);  // the shared Gram, once
+  if (rc) return rc;
+  alnnls_column_result* dres = ENSURE(alnnls_column_result, resb, nrhs);
+  std::vector<alnnls_column_result> init(nrhs);
+  for (auto& r : init) {  // empty_solve_result (nnls.hpp:107-113) when every column is dropped
+    std::memset(&r, 0, sizeof(r));
+    r.termination = ALNNLS_EMPTY_PASSIVE_SET;
+  }
+  CK(cudaMemcpyAsync(dres, init.data(), sizeof(alnnls_column_result) * nrhs,
+                     cudaMemcpyHostToDevice, s));
+  double* Y = ENSURE(double, yb, (m ? m : 1) * nrhs);
+  if (m > 0) {
+    Resolved r;
+    if ((rc = resolve(ctx, cfg, m, &r))) return rc;  // solve_nqp validates its config
+    if (batched_cols_per_cta((int)m) == 0)
+      return set_err(ctx, ALNNLS_EINVAL, "solve_nnls_batched: n > 1024 not supported");
+    double* Qc = ENSURE(double, H, m * m);
+    CK(launch_from_blocked(static_cast<double*>(ctx->Q.p), (int)m, (int)ctx->qR, Qc, m, s));
+    double* QB = ENSURE(double, qb, m * nrhs);
+    SetupArgs sa{};
+    sa.A = dA;
+    sa.lda = lda;
+    sa.d = (int)d;
+    sa.n = (int)n;
+    sa.pos = static_cast<int*>(ctx->pos.p);
+    sa.scale = static_cast<double*>(ctx->scale.p);
+    sa.m = (int)m;
+    sa.B = dB;
+    sa.ldb = ldb;
+    sa.nrhs = (int)nrhs;
+    sa.QB = QB;
+    CK(launch_syrk(sa, 2, s));  // q_j = (-(A^T b_j))[retained] / D for every column
+    CK(cudaEventRecord(ctx->ev[1], s));
+    int* counter = ENSURE(int, mscalar, 4);
+    CK(cudaMemsetAsync(counter, 0, sizeof(int), s));
+    BatchArgs ba{};
+    ba.Q = Qc;
+    ba.m = (int)m;
+    ba.QB = QB;
+    ba.ncols = (int)nrhs;
+    ba.Y = Y;
+    ba.res = dres;
+    ba.eps = r.eps;
+    ba.max_iters = r.max_iters;
+    ba.stall_window = cfg->stall_window;
+    ba.next_col = counter;
+    CK(cudaEventRecord(ctx->ev[2], s));
+    CK(launch_batched(ba, ctx->sm_count, s));
+    CK(cudaEventRecord(ctx->ev[3], s));
+  } else {
+    CK(cudaEventRecord(ctx->ev[1], s));
+    CK(cudaEventRecord(ctx->ev[2], s));
+    CK(cudaEventRecord(ctx->ev[3], s));
+  }
+  CK(launch_unscale_batched(Y, (int)m, static_cast<double*>(ctx->scale.p),
+                            static_cast<uint32_t*>(ctx->retained.p), dX, (int)n, (int)nrhs, s));
+  CK(launch_residual_batched(dA, lda, (int)d, (int)n, dX, dB, ldb, (int)nrhs, dres, s));
+  CK(cudaEventRecord(ctx->ev[4], s));
+  if (cols) {
+    CK(cudaMemcpyAsync(cols, dres, sizeof(alnnls_column_result) * nrhs, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  float t01 = 0, t23 = 0, t34 = 0, t04 = 0;
+  cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
+  cudaEventElapsedTime(&t34, ctx->ev[3], ctx->ev[4]);
+  cudaEventElapsedTime(&t04, ctx->ev[0], ctx->ev[4]);
+  sum.t_setup_s = t01 * 1e-3;
+  sum.t_loop_s = t23 * 1e-3;
+  sum.t_finish_s = t34 * 1e-3;
+  sum.t_total_s = t04 * 1e-3;
+  sum.n = n;
+  sum.m = m;
+  sum.n_dropped = n - m;
+  if (cols) {
+    for (uint64_t j = 0; j < nrhs; ++j) {
+      sum.multiplies_total += cols[j].multiplies_total;
+      sum.iterations += cols[j].iterations;  // total iterations over all columns
+      if (cols[j].numeric_failure) sum.numeric_failure = 1;
+    }
+  }
+  ctx->last = sum;
+  if (out) *out = sum;
+  return ALNNLS_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int alnnls_solve_nnls_batched_device(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA,
                                      uint64_t nrhs, const double* dB, const alnnls_config* cfg,
                                      double* dX, alnnls_column_result* cols, alnnls_summary* out) {
-  (void)d; (void)n; (void)dA; (void)nrhs; (void)dB; (void)cfg; (void)dX; (void)cols; (void)out;
-  return set_err(ctx, ALNNLS_EINVAL, "batched solve not built yet");
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!cfg || !dA || !dB || !dX) return set_err(ctx, ALNNLS_EINVAL, "solve_nnls_batched: null argument");
+  if (d < 1 || n < 1 || nrhs < 1)
+    return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  int st__ = ALNNLS_OK;
+  int* flag = ENSURE(int, flag, 1);
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+  CK(launch_check_finite(dA, d, n, d, flag, ctx->stream));
+  CK(launch_check_finite(dB, d, nrhs, d, flag, ctx->stream));
+  int hf = 0;
+  if ((rc = copy_out(ctx, &hf, flag, sizeof(int)))) return rc;
+  if (hf) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
+  return run_batched(ctx, d, n, dA, d, nrhs, dB, d, cfg, dX, cols, out);
+}
+
+int alnnls_solve_nnls_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A,
+                              uint64_t nrhs, const double* B, const alnnls_config* cfg, double* X,
+                              alnnls_column_result* cols, alnnls_summary* out) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!cfg || !A || !B || !X) return set_err(ctx, ALNNLS_EINVAL, "solve_nnls_batched: null argument");
+  if (d < 1 || n < 1 || nrhs < 1)
+    return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  if (!all_finite(A, d * n) || !all_finite(B, d * nrhs))
+    return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
+  int st__ = ALNNLS_OK;
+  uint64_t lda = 0, ldb = 0;
+  if ((rc = upload_matrix(ctx, ctx->A, d, n, A, &lda))) return rc;
+  if ((rc = upload_matrix(ctx, ctx->bcols, d, nrhs, B, &ldb))) return rc;
+  double* dX = ENSURE(double, X, n * nrhs);
+  rc = run_batched(ctx, d, n, static_cast<double*>(ctx->A.p), lda, nrhs,
+                   static_cast<double*>(ctx->bcols.p), ldb, cfg, dX, cols, out);
+  if (rc) return rc;
+  return copy_out(ctx, X, dX, sizeof(double) * n * nrhs);
 }
 
 }  // extern "C"

@@ -103,6 +103,11 @@ struct SetupArgs {
   double* H;        // optional: raw gram output (n x n, ld n), nullptr when fusing rescale
   double* hvec;     // optional: raw -A^T b (n)
   double* hvec_scratch;  // n doubles for A^T b when b is given
+  // mode 2 (batched right-hand sides): QB[:, j] = q of column j of B
+  const double* B;  // d x nrhs, ldb
+  uint64_t ldb;
+  int nrhs;
+  double* QB;       // m x nrhs (ld m)
 };
 cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream);
 cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream);
@@ -147,18 +152,24 @@ cudaError_t launch_copy_pad(const double* src, uint64_t ld_src, double* dst, uin
 
 // Batched multi-RHS exact solve (K8).
 struct BatchArgs {
-  const double* Q;     // m x m (ldq)
-  uint64_t ldq;
+  const double* Q;     // m x m, column-major (ld m)
   int m;
-  const double* qcols; // m x ncols: per-column linear term q (ld m)
+  const double* QB;    // m x ncols: per-column linear term q (ld m)
   int ncols;
   double* Y;           // m x ncols solution (rescaled space)
   alnnls_column_result* res;  // per column
   double eps;
   uint64_t max_iters;
   uint64_t stall_window;
-  int* next_col;       // work counter
+  int* next_col;       // work counter (zeroed before the launch)
 };
 cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream);
+int batched_cols_per_cta(int m);  // 0 when m is too large for the batched kernel
+cudaError_t launch_unscale_batched(const double* Y, int m, const double* scale,
+                                   const uint32_t* retained, double* X, int n, int ncols,
+                                   cudaStream_t stream);
+cudaError_t launch_residual_batched(const double* A, uint64_t lda, int d, int n, const double* X,
+                                    const double* B, uint64_t ldb, int ncols,
+                                    alnnls_column_result* res, cudaStream_t stream);
 
 }  // namespace alnnls

@@ -53,10 +53,20 @@ __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode
   extern __shared__ __align__(16) double syrk_sm[];
   auto As = reinterpret_cast<double(*)[BK][LDS]>(syrk_sm);
   auto Bs = reinterpret_cast<double(*)[BK][LDS]>(syrk_sm + kStages * BK * LDS);
+  // mode 0/1: upper-triangular tiles of A^T A; mode 2: full tiles of A^T B
   int ti, tj;
-  tri_tile(blockIdx.x, ti, tj);
+  if (mode == 2) {
+    const int nti = (s.n + BM - 1) / BM;
+    ti = blockIdx.x % nti;
+    tj = blockIdx.x / nti;
+  } else {
+    tri_tile(blockIdx.x, ti, tj);
+  }
   const int i0 = ti * BM, j0 = tj * BM;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const double* Bop = mode == 2 ? s.B : s.A;
+  const uint64_t ldb = mode == 2 ? s.ldb : s.lda;
+  const int nb = mode == 2 ? s.nrhs : s.n;
 
   // loader: element e = tid + r*NT (r < 4) of a BK x BM slab: column e/BK, row k0 + e%BK.
   // Out-of-range elements are zero-filled (src-size 0): adding +0 to a chain is exact
@@ -68,7 +78,7 @@ __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode
     const int e = threadIdx.x + r * NT;
     const int ca = i0 + e / BK, cb = j0 + e / BK;
     pa[r] = ca < s.n ? s.A + (size_t)ca * s.lda : nullptr;
-    pb[r] = cb < s.n ? s.A + (size_t)cb * s.lda : nullptr;
+    pb[r] = cb < nb ? Bop + (size_t)cb * ldb : nullptr;
   }
   auto issue = [&](int kb) {
     const int buf = kb % kStages;
@@ -135,8 +145,14 @@ __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int j = j0 + 2 * ty + (c & 1) + 64 * (c >> 1);
-      if (i > j || j >= s.n) continue;
       const double v = acc[r][c];
+      if (mode == 2) {  // q_b of RHS column j: (-(A^T b_j))_{j_b} / D_b (nnls.hpp:79, :133-134)
+        if (i >= s.n || j >= s.nrhs) continue;
+        const int pi = s.pos[i];
+        if (pi >= 0) s.QB[(size_t)j * s.m + pi] = xdiv(-v, s.scale[pi]);
+        continue;
+      }
+      if (i > j || j >= s.n) continue;
       if (mode == 0) {
         s.H[(size_t)j * s.n + i] = v;
         s.H[(size_t)i * s.n + j] = v;
@@ -423,7 +439,7 @@ cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream) {
 
 cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream) {
   const int nt = (s.n + BM - 1) / BM;
-  const int tiles = nt * (nt + 1) / 2;
+  const int tiles = mode == 2 ? nt * ((s.nrhs + BM - 1) / BM) : nt * (nt + 1) / 2;
   if (tiles == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
