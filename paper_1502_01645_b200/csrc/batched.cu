@@ -22,9 +22,8 @@ namespace alnnls {
 
 namespace {
 
-constexpr int kBT = 256;          // threads per batched CTA
+constexpr int kBT = 512;          // threads per batched CTA (one warp per column at NB = 16)
 constexpr int kMaxCols = 16;      // NB upper bound (columns per CTA)
-constexpr size_t kBatchSmem = 5 * 256 * kMaxCols * sizeof(double);  // V, U, C, X, G
 
 enum ColPhase { kIdle = 0, kNeedP1 = 1, kNeedP2 = 2 };
 
@@ -40,23 +39,86 @@ struct ColState {
   double best[kMaxCols];
   unsigned long long since[kMaxCols];
   unsigned long long mults[kMaxCols];
-  int queue_done;
 };
 
-// Layout: V[j * NB + b] etc. (row-major over the m rows, NB columns).
+// GEMM operands V, U are row-major m x ld with ld = NB + 2: the GEMM reads a
+// row of V with 16-byte broadcasts, and the padding keeps a warp's per-column
+// walk (lane = row) to 4-way bank sharing. The per-column state (candidate C,
+// iterate X, gradient G, linear term q) lives in contiguous column panels, so
+// the per-column walks are conflict-free.
 struct BatchSmem {
   double* V;  // GEMM input: g_bar (P1) or delta (P2), 0 off the mask / changed set
   double* U;  // GEMM output: Q g_bar or Q delta
-  double* C;  // candidate x
+  int ld;
+  int m;
+  double* C;  // candidate x   (panel b at C + b * m)
   double* X;  // iterate
   double* G;  // maintained gradient
+  double* q;  // linear term
+  __device__ double& v(int i, int b) const { return V[i * ld + b]; }
+  __device__ double& u(int i, int b) const { return U[i * ld + b]; }
+  __device__ double* c(int b) const { return C + b * m; }
+  __device__ double* x(int b) const { return X + b * m; }
+  __device__ double* g(int b) const { return G + b * m; }
+  __device__ double* qc(int b) const { return q + b * m; }
 };
 
-__device__ void finish_col(const BatchArgs& a, ColState& S, const BatchSmem& sm, int NB, int b,
-                           int term, int numeric) {
+__host__ __device__ constexpr int batch_ld(int nb) { return nb + 2; }
+size_t batch_smem_bytes(int m, int nb) {
+  return ((size_t)2 * m * batch_ld(nb) + (size_t)4 * m * nb) * sizeof(double);
+}
+
+// s = ((0 + t(i0)) + t(i1)) + ... over i ascending, skipping the terms with
+// use == false (exact zeros in the reference chain). The terms of the next 8
+// indices are loaded and multiplied while the current 8 are added, so only the
+// DADD latency is on the chain.
+template <class F>
+__device__ __forceinline__ double col_chain(int m, F term) {
+  double s = 0.0;
+  double t[8];
+  bool use[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    use[k] = false;
+    t[k] = 0.0;
+    if (k < m) t[k] = term(k, use[k]);
+  }
+  for (int i0 = 0; i0 < m; i0 += 8) {
+    double tn[8];
+    bool un[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      un[k] = false;
+      tn[k] = 0.0;
+      if (i0 + 8 + k < m) tn[k] = term(i0 + 8 + k, un[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (use[k]) s = xadd(s, t[k]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      t[k] = tn[k];
+      use[k] = un[k];
+    }
+  }
+  return s;
+}
+
+// Strided product chain: sum of a[i*sa] * b[i*sb] over i with u[i*su] != 0.
+__device__ __forceinline__ double prod_chain(int m, const double* a, int sa, const double* b, int sb,
+                                             const double* u, int su) {
+  return col_chain(m, [&](int i, bool& use) {
+    use = u[i * su] != 0.0;
+    return xmul(a[i * sa], b[i * sb]);
+  });
+}
+
+__device__ void finish_col(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b, int term,
+                           int numeric) {
   const int lane = threadIdx.x & 31;
   const int c = S.col[b];
-  for (int i = lane; i < a.m; i += 32) a.Y[(size_t)c * a.m + i] = sm.X[i * NB + b];
+  const double* xb = sm.x(b);
+  for (int i = lane; i < a.m; i += 32) a.Y[(size_t)c * a.m + i] = xb[i];
   if (lane == 0) {
     alnnls_column_result r;
     r.termination = term;
@@ -74,37 +136,33 @@ __device__ void finish_col(const BatchArgs& a, ColState& S, const BatchSmem& sm,
 
 // Top of an iteration for column b (nqp.hpp:250-275): g_bar into V, the gbs /
 // x.g / q.x chains, the ordered stop tests. One warp; returns true if stopped.
-__device__ bool mask_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm, int NB, int b) {
+__device__ bool mask_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b) {
   const int lane = threadIdx.x & 31;
-  const double* q = a.QB + (size_t)S.col[b] * a.m;
+  const double* xb = sm.x(b);
+  const double* gb = sm.g(b);
   int cnt = 0, bad = 0;
   for (int i = lane; i < a.m; i += 32) {
-    const double xi = sm.X[i * NB + b], gi = sm.G[i * NB + b];
+    const double xi = xb[i], gi = gb[i];
     const bool p = xi > 0.0 || gi < 0.0;
     cnt += p;
     if (!isfinite(gi)) bad = 1;
-    sm.V[i * NB + b] = p ? gi : 0.0;  // g_bar
+    sm.v(i, b) = p ? gi : 0.0;  // g_bar
   }
   for (int o = 16; o > 0; o >>= 1) {
     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     bad |= __shfl_xor_sync(0xffffffffu, bad, o);
   }
   __syncwarp();
-  // lanes 0, 1, 2: the three chains in ascending index order; terms off the
-  // mask are exact zeros (g_bar = 0, x = 0) and are skipped
+  // lanes 0, 1, 2 run the three chains side by side (one code path, per-lane
+  // operands), each in ascending index order; terms off the mask are exact
+  // zeros (g_bar = 0, x = 0) and are skipped. q.x uses x*q (same product bits).
   double s = 0.0;
   if (lane < 3) {
-    for (int i = 0; i < a.m; ++i) {
-      const double gb = sm.V[i * NB + b];
-      const double xi = sm.X[i * NB + b];
-      if (lane == 0) {
-        if (gb != 0.0) s = xadd(s, xmul(gb, gb));
-      } else if (lane == 1) {
-        if (xi != 0.0) s = xadd(s, xmul(xi, sm.G[i * NB + b]));
-      } else {
-        if (xi != 0.0) s = xadd(s, xmul(__ldg(q + i), xi));
-      }
-    }
+    const double* pa = lane == 0 ? &sm.v(0, b) : xb;
+    const int sa = lane == 0 ? sm.ld : 1;
+    const double* pb = lane == 0 ? &sm.v(0, b) : (lane == 1 ? gb : sm.qc(b));
+    const int sb = lane == 0 ? sm.ld : 1;
+    s = prod_chain(a.m, pa, sa, pb, sb, pa, sa);
   }
   const double gbs = __shfl_sync(0xffffffffu, s, 0);
   const double xg = __shfl_sync(0xffffffffu, s, 1);
@@ -128,18 +186,21 @@ __device__ bool mask_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm,
     if (stop < 0) S.phase[b] = kNeedP1;
   }
   stop = __shfl_sync(0xffffffffu, stop, 0);
-  if (stop >= 0) finish_col(a, S, sm, NB, b, stop == 100 ? 0 : stop, stop == 100);
+  if (stop >= 0) finish_col(a, S, sm, b, stop == 100 ? 0 : stop, stop == 100);
   return stop >= 0;
 }
 
 // Candidate step and changed set with the column's alpha (nqp.hpp:294-303):
 // C = candidate x, V = delta (0 off the changed set). Returns |changed|.
-__device__ int cand_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm, int NB, int b) {
+__device__ int cand_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b) {
   const int lane = threadIdx.x & 31;
   const double alpha = S.alpha[b];
+  const double* xb = sm.x(b);
+  const double* gb = sm.g(b);
+  double* cb = sm.c(b);
   int cnt = 0;
   for (int i = lane; i < a.m; i += 32) {
-    const double xi = sm.X[i * NB + b], gi = sm.G[i * NB + b];
+    const double xi = xb[i], gi = gb[i];
     double d = 0.0, c = xi;
     if (xi > 0.0 || gi < 0.0) {
       double t = xsub(xi, xmul(alpha, gi));
@@ -150,8 +211,8 @@ __device__ int cand_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm, 
         ++cnt;
       }
     }
-    sm.C[i * NB + b] = c;
-    sm.V[i * NB + b] = d;
+    cb[i] = c;
+    sm.v(i, b) = d;
   }
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   __syncwarp();
@@ -160,22 +221,27 @@ __device__ int cand_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm, 
 
 // Loads the next RHS from the queue into slot b and runs its first stop test
 // (repeats while columns stop immediately). One warp.
-__device__ void refill(const BatchArgs& a, ColState& S, const BatchSmem& sm, int NB, int b) {
+__device__ void refill(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b) {
   const int lane = threadIdx.x & 31;
   for (;;) {
     int c = 0;
     if (lane == 0) c = atomicAdd(a.next_col, 1);
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= a.ncols) {
-      for (int i = lane; i < a.m; i += 32) sm.V[i * NB + b] = 0.0;  // idle slots feed zeros
+      for (int i = lane; i < a.m; i += 32) sm.v(i, b) = 0.0;  // idle slots feed zeros
       if (lane == 0) S.phase[b] = kIdle;
       __syncwarp();
       return;
     }
     const double* q = a.QB + (size_t)c * a.m;
+    double* xb = sm.x(b);
+    double* gb = sm.g(b);
+    double* qb = sm.qc(b);
     for (int i = lane; i < a.m; i += 32) {
-      sm.X[i * NB + b] = 0.0;
-      sm.G[i * NB + b] = __ldg(q + i);  // x = 0, grad = q (nqp.hpp:224-225)
+      const double qi = __ldg(q + i);
+      xb[i] = 0.0;
+      gb[i] = qi;  // x = 0, grad = q (nqp.hpp:224-225)
+      qb[i] = qi;
     }
     if (lane == 0) {
       S.col[b] = c;
@@ -186,7 +252,7 @@ __device__ void refill(const BatchArgs& a, ColState& S, const BatchSmem& sm, int
       S.mults[b] = 0;
     }
     __syncwarp();
-    if (!mask_phase(a, S, sm, NB, b)) return;
+    if (!mask_phase(a, S, sm, b)) return;
   }
 }
 
@@ -195,53 +261,74 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
   extern __shared__ __align__(16) double bsm[];
   __shared__ ColState S;
   const int m = a.m;
+  constexpr int LD = batch_ld(NB);
   BatchSmem sm;
+  sm.ld = LD;
+  sm.m = m;
   sm.V = bsm;
-  sm.U = bsm + (size_t)m * NB;
-  sm.C = bsm + 2 * (size_t)m * NB;
-  sm.X = bsm + 3 * (size_t)m * NB;
-  sm.G = bsm + 4 * (size_t)m * NB;
+  sm.U = bsm + (size_t)m * LD;
+  sm.C = bsm + 2 * (size_t)m * LD;
+  sm.X = sm.C + (size_t)m * NB;
+  sm.G = sm.X + (size_t)m * NB;
+  sm.q = sm.G + (size_t)m * NB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = kBT / 32;
-  for (int b = warp; b < NB; b += nwarps) refill(a, S, sm, NB, b);
+  constexpr int nwarps = kBT / 32;
+  for (int b = warp; b < NB; b += nwarps) refill(a, S, sm, b);
   __syncthreads();
-  constexpr int RPT = 16 / NB;  // rows per thread
+  // GEMM thread mapping: GROUPS groups of CG columns; rows i = trow + r * ROWT
+  constexpr int CG = NB < 8 ? NB : 8;
+  constexpr int GROUPS = NB / CG;
+  constexpr int ROWT = kBT / GROUPS;
+  constexpr int RPT = (4096 / NB + ROWT - 1) / ROWT;  // rows per thread at the largest m (4096/NB)
+  const int grp = threadIdx.x / ROWT, trow = threadIdx.x % ROWT;
   for (;;) {
     // any active column?
     int active = 0;
     for (int b = 0; b < NB; ++b) active |= S.phase[b] != kIdle;
     if (!active) break;
-    // ---- one exact chain GEMM pass: U = Q V (ascending j per output) ----
-    double acc[16];
+    // ---- one exact chain GEMM pass: U = Q V (ascending j per output). Off-mask
+    // entries of V are 0 and their +-0 products are exact no-ops (idle slots too).
+    double acc[RPT * CG];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) acc[t] = 0.0;
-    for (int j = 0; j < m; ++j) {
-      const double* vrow = sm.V + (size_t)j * NB;
-      bool any = false;
-      for (int b = 0; b < NB; ++b) any |= vrow[b] != 0.0;
-      if (!any) continue;  // all-zero input row: every product is an exact +-0
-      const double* qc = a.Q + (size_t)j * m;
-      double vb[NB];
+    for (int t = 0; t < RPT * CG; ++t) acc[t] = 0.0;
+    constexpr int JB = 8;  // Q columns whose loads are in flight together (L2 latency)
+    for (int j0 = 0; j0 < m; j0 += JB) {
+      double qv[RPT][JB];
 #pragma unroll
-      for (int b = 0; b < NB; b += 2) {
-        const double2 t = *reinterpret_cast<const double2*>(vrow + b);
-        vb[b] = t.x;
-        vb[b + 1] = t.y;
+      for (int u = 0; u < JB; ++u) {
+        const double* qc = a.Q + (size_t)(j0 + u) * m;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int i = trow + r * ROWT;
+          qv[r][u] = (j0 + u < m && i < m) ? __ldg(qc + i) : 0.0;
+        }
       }
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const int i = threadIdx.x + r * kBT;
-        const double qv = i < m ? __ldg(qc + i) : 0.0;
+      for (int u = 0; u < JB; ++u) {
+        const int j = j0 + u;
+        if (j >= m) break;
+        const double* vrow = sm.V + (size_t)j * LD + grp * CG;
+        double vb[CG];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) acc[r * NB + b] = xmac(acc[r * NB + b], qv, vb[b]);
+        for (int b = 0; b < CG; b += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(vrow + b);
+          vb[b] = t.x;
+          vb[b + 1] = t.y;
+        }
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+#pragma unroll
+          for (int b = 0; b < CG; ++b) acc[r * CG + b] = xmac(acc[r * CG + b], qv[r][u], vb[b]);
       }
     }
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
-      const int i = threadIdx.x + r * kBT;
+      const int i = trow + r * ROWT;
       if (i < m) {
+        double* urow = sm.U + (size_t)i * LD + grp * CG;
 #pragma unroll
-        for (int b = 0; b < NB; ++b) sm.U[(size_t)i * NB + b] = acc[r * NB + b];
+        for (int b = 0; b < CG; b += 2)
+          *reinterpret_cast<double2*>(urow + b) = make_double2(acc[r * CG + b], acc[r * CG + b + 1]);
       }
     }
     __syncthreads();
@@ -252,16 +339,11 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
       if (ph == kNeedP1) {
         // den = g_bar . (Q g_bar) over the mask (exact_step, nqp.hpp:166-172)
         double den = 0.0;
-        if (lane == 0) {
-          for (int i = 0; i < m; ++i) {
-            const double gb = sm.V[i * NB + b];
-            if (gb != 0.0) den = xadd(den, xmul(gb, sm.U[i * NB + b]));
-          }
-        }
+        if (lane == 0) den = prod_chain(m, &sm.v(0, b), LD, &sm.u(0, b), LD, &sm.v(0, b), LD);
         den = __shfl_sync(0xffffffffu, den, 0);
         if (!(den > 0.0)) {
-          finish_col(a, S, sm, NB, b, ALNNLS_ZERO_CURVATURE, 0);
-          refill(a, S, sm, NB, b);
+          finish_col(a, S, sm, b, ALNNLS_ZERO_CURVATURE, 0);
+          refill(a, S, sm, b);
           continue;
         }
         if (lane == 0) {
@@ -272,22 +354,27 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
         __syncwarp();
       } else {  // kNeedP2: gd = Q delta in U; df chain (nqp.hpp:307)
         double df = 0.0;
+        const double* gb = sm.g(b);
         if (lane == 0) {
-          for (int i = 0; i < m; ++i) {
-            const double d = sm.V[i * NB + b];
-            if (d != 0.0) df = xadd(df, xmul(xadd(sm.G[i * NB + b], xmul(0.5, sm.U[i * NB + b])), d));
-          }
+          df = col_chain(m, [&](int i, bool& use) {
+            const double dd = sm.v(i, b);
+            use = dd != 0.0;
+            return xmul(xadd(gb[i], xmul(0.5, sm.u(i, b))), dd);
+          });
         }
         df = __shfl_sync(0xffffffffu, df, 0);
         const bool accept = df <= 0.0 || S.tries[b] >= 60;
         if (accept) {  // x[C] = cand, grad += gd (nqp.hpp:309-313)
+          double* xb = sm.x(b);
+          double* gw = sm.g(b);
+          const double* cb = sm.c(b);
           for (int i = lane; i < m; i += 32) {
-            sm.X[i * NB + b] = sm.C[i * NB + b];
-            sm.G[i * NB + b] = xadd(sm.G[i * NB + b], sm.U[i * NB + b]);
+            xb[i] = cb[i];
+            gw[i] = xadd(gw[i], sm.u(i, b));
           }
           if (lane == 0) ++S.k[b];
           __syncwarp();
-          if (mask_phase(a, S, sm, NB, b)) refill(a, S, sm, NB, b);
+          if (mask_phase(a, S, sm, b)) refill(a, S, sm, b);
           continue;
         }
         if (lane == 0) {
@@ -297,12 +384,12 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
         __syncwarp();
       }
       // candidate step with the current alpha
-      const int cl = cand_phase(a, S, sm, NB, b);
+      const int cl = cand_phase(a, S, sm, b);
       if (lane == 0) S.cl[b] = cl;
       if (cl == 0) {  // nothing moved (nqp.hpp:304): next iteration on the same state
         if (lane == 0) ++S.k[b];
         __syncwarp();
-        if (mask_phase(a, S, sm, NB, b)) refill(a, S, sm, NB, b);
+        if (mask_phase(a, S, sm, b)) refill(a, S, sm, b);
         continue;
       }
       if (lane == 0) {
@@ -398,8 +485,8 @@ __global__ void __launch_bounds__(256) residual_batched_kernel(const double* A, 
 }  // namespace
 
 int batched_cols_per_cta(int m) {
-  const int rpt = (m + kBT - 1) / kBT;
-  return rpt <= 1 ? 16 : (rpt <= 2 ? 8 : (rpt <= 4 ? 4 : 0));
+  // shared memory holds 5 m x NB panels; the GEMM covers m <= 4096 / NB rows
+  return m <= 256 ? 16 : (m <= 512 ? 8 : (m <= 1024 ? 4 : 0));
 }
 
 cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream) {
@@ -407,18 +494,17 @@ cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream
   if (NB == 0) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
+    const int mx = (int)batch_smem_bytes(1024, 4);  // the largest configuration
     cudaError_t e = cudaFuncSetAttribute(batched_nqp_kernel<16>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBatchSmem);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(batched_nqp_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kBatchSmem);
+      e = cudaFuncSetAttribute(batched_nqp_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(batched_nqp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kBatchSmem);
+      e = cudaFuncSetAttribute(batched_nqp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const size_t smem = 5 * (size_t)a.m * NB * sizeof(double);
+  const size_t smem = batch_smem_bytes(a.m, NB);
   int grid = sm_count;
   const int need = (a.ncols + NB - 1) / NB;
   if (grid > need) grid = need;
