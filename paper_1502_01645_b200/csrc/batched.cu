@@ -32,7 +32,6 @@ struct ColState {
   int col[kMaxCols];
   unsigned long long k[kMaxCols];
   int tries[kMaxCols];
-  int cl[kMaxCols];
   int ml[kMaxCols];
   double alpha[kMaxCols];
   double f[kMaxCols], gbs[kMaxCols];
@@ -41,76 +40,72 @@ struct ColState {
   unsigned long long mults[kMaxCols];
 };
 
-// GEMM operands V, U are row-major m x ld with ld = NB + 2: the GEMM reads a
-// row of V with 16-byte broadcasts, and the padding keeps a warp's per-column
-// walk (lane = row) to 4-way bank sharing. The per-column state (candidate C,
-// iterate X, gradient G, linear term q) lives in contiguous column panels, so
-// the per-column walks are conflict-free.
+// Shared-memory layout of one CTA (mp = m rounded up to 8):
+//  - V, the GEMM input, row-major mp x ld (ld = NB + 2): the GEMM reads a row of
+//    V with 16-byte broadcasts; the padding keeps the per-column writes (lane =
+//    row) at 4-way bank sharing; rows >= m stay zero so the GEMM needs no tail.
+//  - U (GEMM output), C (candidate), X (iterate), G (gradient), q (linear term):
+//    column panels of mp doubles, so the GEMM's stores and every per-column walk
+//    are conflict-free, and a lane can load 8 consecutive entries as 4 x 16 B.
 struct BatchSmem {
-  double* V;  // GEMM input: g_bar (P1) or delta (P2), 0 off the mask / changed set
-  double* U;  // GEMM output: Q g_bar or Q delta
+  double* V;
   int ld;
-  int m;
-  double* C;  // candidate x   (panel b at C + b * m)
-  double* X;  // iterate
-  double* G;  // maintained gradient
-  double* q;  // linear term
+  int m, mp;
+  double* U;
+  double* C;
+  double* X;
+  double* G;
+  double* q;
   __device__ double& v(int i, int b) const { return V[i * ld + b]; }
-  __device__ double& u(int i, int b) const { return U[i * ld + b]; }
-  __device__ double* c(int b) const { return C + b * m; }
-  __device__ double* x(int b) const { return X + b * m; }
-  __device__ double* g(int b) const { return G + b * m; }
-  __device__ double* qc(int b) const { return q + b * m; }
+  __device__ double* u(int b) const { return U + b * mp; }
+  __device__ double* c(int b) const { return C + b * mp; }
+  __device__ double* x(int b) const { return X + b * mp; }
+  __device__ double* g(int b) const { return G + b * mp; }
+  __device__ double* qc(int b) const { return q + b * mp; }
 };
 
 __host__ __device__ constexpr int batch_ld(int nb) { return nb + 2; }
+__host__ __device__ constexpr int round8(int m) { return (m + 7) & ~7; }
 size_t batch_smem_bytes(int m, int nb) {
-  return ((size_t)2 * m * batch_ld(nb) + (size_t)4 * m * nb) * sizeof(double);
+  const size_t mp = (size_t)round8(m);
+  return (mp * batch_ld(nb) + 5 * mp * nb) * sizeof(double);
 }
 
-// s = ((0 + t(i0)) + t(i1)) + ... over i ascending, skipping the terms with
-// use == false (exact zeros in the reference chain). The terms of the next 8
-// indices are loaded and multiplied while the current 8 are added, so only the
-// DADD latency is on the chain.
-template <class F>
-__device__ __forceinline__ double col_chain(int m, F term) {
-  double s = 0.0;
-  double t[8];
-  bool use[8];
+// 8 consecutive doubles (16-byte aligned) from shared memory.
+__device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
+  const double2* w = reinterpret_cast<const double2*>(p);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    use[k] = false;
-    t[k] = 0.0;
-    if (k < m) t[k] = term(k, use[k]);
+  for (int h = 0; h < 4; ++h) {
+    const double2 t = w[h];
+    v[2 * h] = t.x;
+    v[2 * h + 1] = t.y;
   }
-  for (int i0 = 0; i0 < m; i0 += 8) {
-    double tn[8];
-    bool un[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      un[k] = false;
-      tn[k] = 0.0;
-      if (i0 + 8 + k < m) tn[k] = term(i0 + 8 + k, un[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (use[k]) s = xadd(s, t[k]);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      t[k] = tn[k];
-      use[k] = un[k];
-    }
-  }
-  return s;
 }
 
-// Strided product chain: sum of a[i*sa] * b[i*sb] over i with u[i*su] != 0.
-__device__ __forceinline__ double prod_chain(int m, const double* a, int sa, const double* b, int sb,
-                                             const double* u, int su) {
-  return col_chain(m, [&](int i, bool& use) {
-    use = u[i * su] != 0.0;
-    return xmul(a[i * sa], b[i * sb]);
-  });
+// Cross-lane ordered chains. Within a 256-index round, lane L holds the terms of
+// indices base + 8L .. base + 8L + 7 (computed in parallel); the running sums
+// are handed from lane to lane with a shuffle, so each s[k] is the single
+// ascending chain ((0 + t_0) + t_1) + ... of the reference, skipping the terms
+// whose use flag is false (exact zeros). All lanes end with the current sums.
+template <int K>
+__device__ __forceinline__ void lane_chain(double (&s)[K], const double (&t)[K][8],
+                                           const bool (&use)[K][8], int nsteps) {
+  const int lane = threadIdx.x & 31;
+  for (int src = 0; src < nsteps; ++src) {
+    if (lane == src) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if (use[k][e]) s[k] = xadd(s[k], t[k][e]);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) s[k] = __shfl_sync(0xffffffffu, s[k], src);
+  }
+}
+__device__ __forceinline__ int chain_steps(int m, int r0) {
+  const int left = (m - r0 + 7) >> 3;
+  return left < 32 ? left : 32;
 }
 
 __device__ void finish_col(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b, int term,
@@ -140,33 +135,53 @@ __device__ bool mask_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm,
   const int lane = threadIdx.x & 31;
   const double* xb = sm.x(b);
   const double* gb = sm.g(b);
-  int cnt = 0, bad = 0;
+  const double* qb = sm.qc(b);
   for (int i = lane; i < a.m; i += 32) {
     const double xi = xb[i], gi = gb[i];
-    const bool p = xi > 0.0 || gi < 0.0;
-    cnt += p;
-    if (!isfinite(gi)) bad = 1;
-    sm.v(i, b) = p ? gi : 0.0;  // g_bar
+    sm.v(i, b) = (xi > 0.0 || gi < 0.0) ? gi : 0.0;  // g_bar
+  }
+  // the three chains in ascending index order; terms off the mask are exact
+  // zeros (g_bar = 0, x = 0) and are skipped. q.x uses x*q (same product bits).
+  int cnt = 0, bad = 0;
+  double s[3] = {0.0, 0.0, 0.0};
+  for (int r0 = 0; r0 < a.m; r0 += 256) {
+    const int base = r0 + 8 * lane;
+    double t[3][8];
+    bool use[3][8];
+    if (base < a.m) {
+      double xv[8], gv[8], qv[8];
+      load8(xb + base, xv);
+      load8(gb + base, gv);
+      load8(qb + base, qv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool p = xv[e] > 0.0 || gv[e] < 0.0;  // zero beyond m: never passive
+        cnt += p;
+        if (!isfinite(gv[e])) bad = 1;
+        const double gbar = p ? gv[e] : 0.0;
+        use[0][e] = gbar != 0.0;
+        t[0][e] = xmul(gbar, gbar);
+        use[1][e] = xv[e] != 0.0;
+        t[1][e] = xmul(xv[e], gv[e]);
+        use[2][e] = use[1][e];
+        t[2][e] = xmul(xv[e], qv[e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          use[k][e] = false;
+          t[k][e] = 0.0;
+        }
+    }
+    lane_chain<3>(s, t, use, chain_steps(a.m, r0));
   }
   for (int o = 16; o > 0; o >>= 1) {
     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     bad |= __shfl_xor_sync(0xffffffffu, bad, o);
   }
-  __syncwarp();
-  // lanes 0, 1, 2 run the three chains side by side (one code path, per-lane
-  // operands), each in ascending index order; terms off the mask are exact
-  // zeros (g_bar = 0, x = 0) and are skipped. q.x uses x*q (same product bits).
-  double s = 0.0;
-  if (lane < 3) {
-    const double* pa = lane == 0 ? &sm.v(0, b) : xb;
-    const int sa = lane == 0 ? sm.ld : 1;
-    const double* pb = lane == 0 ? &sm.v(0, b) : (lane == 1 ? gb : sm.qc(b));
-    const int sb = lane == 0 ? sm.ld : 1;
-    s = prod_chain(a.m, pa, sa, pb, sb, pa, sa);
-  }
-  const double gbs = __shfl_sync(0xffffffffu, s, 0);
-  const double xg = __shfl_sync(0xffffffffu, s, 1);
-  const double qx = __shfl_sync(0xffffffffu, s, 2);
+  const double gbs = s[0], xg = s[1], qx = s[2];
   int stop = -1;
   if (lane == 0) {
     const double f = xmul(0.5, xadd(xg, qx));
@@ -188,6 +203,78 @@ __device__ bool mask_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm,
   stop = __shfl_sync(0xffffffffu, stop, 0);
   if (stop >= 0) finish_col(a, S, sm, b, stop == 100 ? 0 : stop, stop == 100);
   return stop >= 0;
+}
+
+// den = g_bar . (Q g_bar) over the mask (exact_step, nqp.hpp:166-172).
+__device__ double den_chain(const BatchSmem& sm, int b) {
+  const int lane = threadIdx.x & 31;
+  const double* xb = sm.x(b);
+  const double* gb = sm.g(b);
+  const double* ub = sm.u(b);
+  double s[1] = {0.0};
+  for (int r0 = 0; r0 < sm.m; r0 += 256) {
+    const int base = r0 + 8 * lane;
+    double t[1][8];
+    bool use[1][8];
+    if (base < sm.m) {
+      double xv[8], gv[8], uv[8];
+      load8(xb + base, xv);
+      load8(gb + base, gv);
+      load8(ub + base, uv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double gbar = (xv[e] > 0.0 || gv[e] < 0.0) ? gv[e] : 0.0;
+        use[0][e] = gbar != 0.0;
+        t[0][e] = xmul(gbar, uv[e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        use[0][e] = false;
+        t[0][e] = 0.0;
+      }
+    }
+    lane_chain<1>(s, t, use, chain_steps(sm.m, r0));
+  }
+  return s[0];
+}
+
+// df = sum over the changed set of (g + 0.5 gd) * delta (nqp.hpp:307). The
+// changed set is where the candidate differs from x, and delta = cand - x is
+// recomputed with the same operation cand_phase used.
+__device__ double df_chain(const BatchSmem& sm, int b) {
+  const int lane = threadIdx.x & 31;
+  const double* xb = sm.x(b);
+  const double* gb = sm.g(b);
+  const double* cb = sm.c(b);
+  const double* ub = sm.u(b);
+  double s[1] = {0.0};
+  for (int r0 = 0; r0 < sm.m; r0 += 256) {
+    const int base = r0 + 8 * lane;
+    double t[1][8];
+    bool use[1][8];
+    if (base < sm.m) {
+      double xv[8], gv[8], cv[8], uv[8];
+      load8(xb + base, xv);
+      load8(gb + base, gv);
+      load8(cb + base, cv);
+      load8(ub + base, uv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double dd = cv[e] != xv[e] ? xsub(cv[e], xv[e]) : 0.0;
+        use[0][e] = dd != 0.0;
+        t[0][e] = xmul(xadd(gv[e], xmul(0.5, uv[e])), dd);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        use[0][e] = false;
+        t[0][e] = 0.0;
+      }
+    }
+    lane_chain<1>(s, t, use, chain_steps(sm.m, r0));
+  }
+  return s[0];
 }
 
 // Candidate step and changed set with the column's alpha (nqp.hpp:294-303):
@@ -261,16 +348,23 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
   extern __shared__ __align__(16) double bsm[];
   __shared__ ColState S;
   const int m = a.m;
+  const int mp = round8(m);
   constexpr int LD = batch_ld(NB);
   BatchSmem sm;
   sm.ld = LD;
   sm.m = m;
+  sm.mp = mp;
   sm.V = bsm;
-  sm.U = bsm + (size_t)m * LD;
-  sm.C = bsm + 2 * (size_t)m * LD;
-  sm.X = sm.C + (size_t)m * NB;
-  sm.G = sm.X + (size_t)m * NB;
-  sm.q = sm.G + (size_t)m * NB;
+  sm.U = bsm + (size_t)mp * LD;
+  sm.C = sm.U + (size_t)mp * NB;
+  sm.X = sm.C + (size_t)mp * NB;
+  sm.G = sm.X + (size_t)mp * NB;
+  sm.q = sm.G + (size_t)mp * NB;
+  {  // zero everything once: pads (rows >= m, panel tails) must read as +0
+    const int total = mp * LD + 5 * mp * NB;
+    for (int e = threadIdx.x; e < total; e += kBT) bsm[e] = 0.0;
+  }
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int nwarps = kBT / 32;
   for (int b = warp; b < NB; b += nwarps) refill(a, S, sm, b);
@@ -287,13 +381,14 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
     for (int b = 0; b < NB; ++b) active |= S.phase[b] != kIdle;
     if (!active) break;
     // ---- one exact chain GEMM pass: U = Q V (ascending j per output). Off-mask
-    // entries of V are 0 and their +-0 products are exact no-ops (idle slots too).
+    // entries of V are 0 and their +-0 products are exact no-ops (idle slots,
+    // pad rows j >= m with their zero Q operands too).
     double acc[RPT * CG];
 #pragma unroll
     for (int t = 0; t < RPT * CG; ++t) acc[t] = 0.0;
     constexpr int JB = 8;  // Q columns whose loads are in flight together (L2 latency)
-    for (int j0 = 0; j0 < m; j0 += JB) {
-      double qv[RPT][JB];
+    double qv[RPT][JB];
+    auto load_q = [&](int j0) {
 #pragma unroll
       for (int u = 0; u < JB; ++u) {
         const double* qc = a.Q + (size_t)(j0 + u) * m;
@@ -303,11 +398,18 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
           qv[r][u] = (j0 + u < m && i < m) ? __ldg(qc + i) : 0.0;
         }
       }
+    };
+    load_q(0);
+    for (int j0 = 0; j0 < mp; j0 += JB) {
+      double qn[RPT][JB];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+#pragma unroll
+        for (int u = 0; u < JB; ++u) qn[r][u] = qv[r][u];
+      if (j0 + JB < mp) load_q(j0 + JB);  // next block in flight during this one
 #pragma unroll
       for (int u = 0; u < JB; ++u) {
-        const int j = j0 + u;
-        if (j >= m) break;
-        const double* vrow = sm.V + (size_t)j * LD + grp * CG;
+        const double* vrow = sm.V + (size_t)(j0 + u) * LD + grp * CG;
         double vb[CG];
 #pragma unroll
         for (int b = 0; b < CG; b += 2) {
@@ -318,17 +420,15 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
 #pragma unroll
-          for (int b = 0; b < CG; ++b) acc[r * CG + b] = xmac(acc[r * CG + b], qv[r][u], vb[b]);
+          for (int b = 0; b < CG; ++b) acc[r * CG + b] = xmac(acc[r * CG + b], qn[r][u], vb[b]);
       }
     }
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
       const int i = trow + r * ROWT;
       if (i < m) {
-        double* urow = sm.U + (size_t)i * LD + grp * CG;
 #pragma unroll
-        for (int b = 0; b < CG; b += 2)
-          *reinterpret_cast<double2*>(urow + b) = make_double2(acc[r * CG + b], acc[r * CG + b + 1]);
+        for (int b = 0; b < CG; ++b) sm.U[(size_t)(grp * CG + b) * mp + i] = acc[r * CG + b];
       }
     }
     __syncthreads();
@@ -337,10 +437,7 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
       const int ph = S.phase[b];
       if (ph == kIdle) continue;
       if (ph == kNeedP1) {
-        // den = g_bar . (Q g_bar) over the mask (exact_step, nqp.hpp:166-172)
-        double den = 0.0;
-        if (lane == 0) den = prod_chain(m, &sm.v(0, b), LD, &sm.u(0, b), LD, &sm.v(0, b), LD);
-        den = __shfl_sync(0xffffffffu, den, 0);
+        const double den = den_chain(sm, b);
         if (!(den > 0.0)) {
           finish_col(a, S, sm, b, ALNNLS_ZERO_CURVATURE, 0);
           refill(a, S, sm, b);
@@ -352,25 +449,17 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
           S.mults[b] += (unsigned long long)m * (unsigned long long)S.ml[b];
         }
         __syncwarp();
-      } else {  // kNeedP2: gd = Q delta in U; df chain (nqp.hpp:307)
-        double df = 0.0;
-        const double* gb = sm.g(b);
-        if (lane == 0) {
-          df = col_chain(m, [&](int i, bool& use) {
-            const double dd = sm.v(i, b);
-            use = dd != 0.0;
-            return xmul(xadd(gb[i], xmul(0.5, sm.u(i, b))), dd);
-          });
-        }
-        df = __shfl_sync(0xffffffffu, df, 0);
+      } else {  // kNeedP2: gd = Q delta in U
+        const double df = df_chain(sm, b);
         const bool accept = df <= 0.0 || S.tries[b] >= 60;
         if (accept) {  // x[C] = cand, grad += gd (nqp.hpp:309-313)
           double* xb = sm.x(b);
           double* gw = sm.g(b);
           const double* cb = sm.c(b);
+          const double* ub = sm.u(b);
           for (int i = lane; i < m; i += 32) {
             xb[i] = cb[i];
-            gw[i] = xadd(gw[i], sm.u(i, b));
+            gw[i] = xadd(gw[i], ub[i]);
           }
           if (lane == 0) ++S.k[b];
           __syncwarp();
@@ -385,7 +474,6 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
       }
       // candidate step with the current alpha
       const int cl = cand_phase(a, S, sm, b);
-      if (lane == 0) S.cl[b] = cl;
       if (cl == 0) {  // nothing moved (nqp.hpp:304): next iteration on the same state
         if (lane == 0) ++S.k[b];
         __syncwarp();
