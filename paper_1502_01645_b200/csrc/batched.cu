@@ -15,6 +15,8 @@
 //    columns are replaced from a global queue.
 //  - unscale + residual: x = y / D; ||A x - b||^2 with one ordered chain per
 //    column over the rows (nnls.hpp:87-96, :115-123).
+#include <cstdio>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -86,21 +88,32 @@ __device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
 // indices base + 8L .. base + 8L + 7 (computed in parallel); the running sums
 // are handed from lane to lane with a shuffle, so each s[k] is the single
 // ascending chain ((0 + t_0) + t_1) + ... of the reference, skipping the terms
-// whose use flag is false (exact zeros). All lanes end with the current sums.
+// whose use flag is false (exact zeros). A skipped term is added as -0, which
+// leaves every sum bit-identical (s + -0 = s, +0 included: a chain that starts
+// at +0 never becomes -0), so the chain is pure dependent DADDs with no select.
+// All lanes end with the current sums.
 template <int K>
 __device__ __forceinline__ void lane_chain(double (&s)[K], const double (&t)[K][8],
                                            const bool (&use)[K][8], int nsteps) {
   const int lane = threadIdx.x & 31;
+  double tt[K][8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+#pragma unroll
+    for (int k = 0; k < K; ++k) tt[k][e] = use[k][e] ? t[k][e] : -0.0;
+  // Branch-free hand-off: every lane adds its own 8 terms to the current sums
+  // and the sums of lane `src` (the only ones in index order) are broadcast.
+  (void)lane;
   for (int src = 0; src < nsteps; ++src) {
-    if (lane == src) {
+    double r[K];
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
+    for (int k = 0; k < K; ++k) r[k] = s[k];
 #pragma unroll
-        for (int k = 0; k < K; ++k)
-          if (use[k][e]) s[k] = xadd(s[k], t[k][e]);
-    }
+    for (int e = 0; e < 8; ++e)
 #pragma unroll
-    for (int k = 0; k < K; ++k) s[k] = __shfl_sync(0xffffffffu, s[k], src);
+      for (int k = 0; k < K; ++k) r[k] = xadd(r[k], tt[k][e]);
+#pragma unroll
+    for (int k = 0; k < K; ++k) s[k] = __shfl_sync(0xffffffffu, r[k], src);
   }
 }
 __device__ __forceinline__ int chain_steps(int m, int r0) {
@@ -375,7 +388,20 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
   constexpr int ROWT = kBT / GROUPS;
   constexpr int RPT = (4096 / NB + ROWT - 1) / ROWT;  // rows per thread at the largest m (4096/NB)
   const int grp = threadIdx.x / ROWT, trow = threadIdx.x % ROWT;
+#ifdef ALNNLS_BATCH_PROFILE
+  long long t_gemm = 0, t_cols = 0, npass = 0;
+  long long pt[4] = {0, 0, 0, 0}, pn[4] = {0, 0, 0, 0};
+  long long pc0 = 0;
+#define PROF_T0 pc0 = clock64()
+#define PROF_T1(k) (pt[k] += clock64() - pc0, ++pn[k])
+#else
+#define PROF_T0
+#define PROF_T1(k)
+#endif
   for (;;) {
+#ifdef ALNNLS_BATCH_PROFILE
+    const long long c0 = clock64();
+#endif
     // any active column?
     int active = 0;
     for (int b = 0; b < NB; ++b) active |= S.phase[b] != kIdle;
@@ -386,9 +412,8 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
     double acc[RPT * CG];
 #pragma unroll
     for (int t = 0; t < RPT * CG; ++t) acc[t] = 0.0;
-    constexpr int JB = 8;  // Q columns whose loads are in flight together (L2 latency)
-    double qv[RPT][JB];
-    auto load_q = [&](int j0) {
+    constexpr int JB = 8;  // Q columns per block; two blocks in registers (ping-pong)
+    auto load_q = [&](int j0, double (&qv)[RPT][JB]) {
 #pragma unroll
       for (int u = 0; u < JB; ++u) {
         const double* qc = a.Q + (size_t)(j0 + u) * m;
@@ -399,14 +424,7 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
         }
       }
     };
-    load_q(0);
-    for (int j0 = 0; j0 < mp; j0 += JB) {
-      double qn[RPT][JB];
-#pragma unroll
-      for (int r = 0; r < RPT; ++r)
-#pragma unroll
-        for (int u = 0; u < JB; ++u) qn[r][u] = qv[r][u];
-      if (j0 + JB < mp) load_q(j0 + JB);  // next block in flight during this one
+    auto block = [&](int j0, const double (&qv)[RPT][JB]) {
 #pragma unroll
       for (int u = 0; u < JB; ++u) {
         const double* vrow = sm.V + (size_t)(j0 + u) * LD + grp * CG;
@@ -420,8 +438,17 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
 #pragma unroll
-          for (int b = 0; b < CG; ++b) acc[r * CG + b] = xmac(acc[r * CG + b], qn[r][u], vb[b]);
+          for (int b = 0; b < CG; ++b) acc[r * CG + b] = xmac(acc[r * CG + b], qv[r][u], vb[b]);
       }
+    };
+    double qa[RPT][JB], qb[RPT][JB];
+    load_q(0, qa);
+    for (int j0 = 0; j0 < mp; j0 += 2 * JB) {  // mp is a multiple of JB; V rows >= m are zero
+      const bool two = j0 + JB < mp;
+      if (two) load_q(j0 + JB, qb);
+      block(j0, qa);
+      if (j0 + 2 * JB < mp) load_q(j0 + 2 * JB, qa);
+      if (two) block(j0 + JB, qb);
     }
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
@@ -432,12 +459,19 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
       }
     }
     __syncthreads();
+#ifdef ALNNLS_BATCH_PROFILE
+    const long long c1 = clock64();
+    t_gemm += c1 - c0;
+    ++npass;
+#endif
     // ---- per-column state machines ----
     for (int b = warp; b < NB; b += nwarps) {
       const int ph = S.phase[b];
       if (ph == kIdle) continue;
       if (ph == kNeedP1) {
+        PROF_T0;
         const double den = den_chain(sm, b);
+        PROF_T1(0);
         if (!(den > 0.0)) {
           finish_col(a, S, sm, b, ALNNLS_ZERO_CURVATURE, 0);
           refill(a, S, sm, b);
@@ -450,7 +484,9 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
         }
         __syncwarp();
       } else {  // kNeedP2: gd = Q delta in U
+        PROF_T0;
         const double df = df_chain(sm, b);
+        PROF_T1(1);
         const bool accept = df <= 0.0 || S.tries[b] >= 60;
         if (accept) {  // x[C] = cand, grad += gd (nqp.hpp:309-313)
           double* xb = sm.x(b);
@@ -463,7 +499,9 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
           }
           if (lane == 0) ++S.k[b];
           __syncwarp();
+          PROF_T0;
           if (mask_phase(a, S, sm, b)) refill(a, S, sm, b);
+          PROF_T1(2);
           continue;
         }
         if (lane == 0) {
@@ -473,7 +511,9 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
         __syncwarp();
       }
       // candidate step with the current alpha
+      PROF_T0;
       const int cl = cand_phase(a, S, sm, b);
+      PROF_T1(3);
       if (cl == 0) {  // nothing moved (nqp.hpp:304): next iteration on the same state
         if (lane == 0) ++S.k[b];
         __syncwarp();
@@ -487,7 +527,19 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
       __syncwarp();
     }
     __syncthreads();
+#ifdef ALNNLS_BATCH_PROFILE
+    t_cols += clock64() - c1;
+#endif
   }
+#ifdef ALNNLS_BATCH_PROFILE
+  if (threadIdx.x == 0 && blockIdx.x < 2)
+    printf("batch prof cta %d: passes %lld gemm %lld cyc/pass, cols %lld cyc/pass\n", blockIdx.x, npass,
+           t_gemm / (npass ? npass : 1), t_cols / (npass ? npass : 1));
+  if (threadIdx.x == 0 && blockIdx.x < 2)
+    printf("  warp0: den %lld (n %lld) df %lld (n %lld) mask %lld (n %lld) cand %lld (n %lld)\n",
+           pt[0] / (pn[0] ? pn[0] : 1), pn[0], pt[1] / (pn[1] ? pn[1] : 1), pn[1],
+           pt[2] / (pn[2] ? pn[2] : 1), pn[2], pt[3] / (pn[3] ? pn[3] : 1), pn[3]);
+#endif
 }
 
 // x[retained[a], j] = Y[a, j] / D_a; dropped columns 0 (nnls.hpp:87-96).
