@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <string>
 #include <vector>
 
@@ -406,6 +407,35 @@ int copy_out(alnnls_ctx* ctx, void* dst, const void* src, size_t bytes) {
   return ALNNLS_OK;
 }
 
+// The reference validates finiteness when a DenseMatrix / Vector is built
+// (linalg.hpp:42-52, :84). The host-buffer entries upload first and run that
+// check on the device over the copies (one flag per operand, reported in the
+// reference's construction order), instead of a single-threaded host scan.
+struct FiniteArg {
+  const double* p;
+  uint64_t rows, cols, ld;
+  const char* msg;
+};
+int device_check_finite(alnnls_ctx* ctx, std::initializer_list<FiniteArg> args) {
+  int st__ = ALNNLS_OK;
+  const size_t k = args.size();
+  int* flag = ENSURE(int, flag, 4);
+  CK(cudaMemsetAsync(flag, 0, sizeof(int) * k, ctx->stream));
+  int i = 0;
+  for (const FiniteArg& a : args) {
+    CK(launch_check_finite(a.p, a.rows, a.cols, a.ld, flag + i, ctx->stream));
+    ++i;
+  }
+  int hf[4] = {0, 0, 0, 0};
+  if (int rc = copy_out(ctx, hf, flag, sizeof(int) * k)) return rc;
+  i = 0;
+  for (const FiniteArg& a : args) {
+    if (hf[i]) return set_err(ctx, ALNNLS_EINVAL, a.msg);
+    ++i;
+  }
+  return ALNNLS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -506,15 +536,16 @@ int alnnls_solve_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, 
   if (rc) return rc;
   if (!cfg || !A || !b) return set_err(ctx, ALNNLS_EINVAL, "solve_nnls: null argument");
   if (d < 1 || n < 1) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
-  // DenseMatrix / Vector construction validates finiteness (linalg.hpp:42-52, :84)
-  if (!all_finite(A, d * n)) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
-  if (!all_finite(b, d)) return set_err(ctx, ALNNLS_EINVAL, "Vector: non-finite entry");
   int st__ = ALNNLS_OK;
   uint64_t lda = 0;
   if ((rc = upload_matrix(ctx, ctx->A, d, n, A, &lda))) return rc;
   double* db = ENSURE(double, b, d);
   CK(cudaMemcpyAsync(db, b, sizeof(double) * d, cudaMemcpyHostToDevice, ctx->stream));
-  return run_nnls(ctx, d, n, static_cast<double*>(ctx->A.p), lda, db, cfg, out);
+  double* dA = static_cast<double*>(ctx->A.p);
+  if ((rc = device_check_finite(ctx, {{dA, d, n, lda, "DenseMatrix: non-finite entry"},
+                                      {db, d, 1, d, "Vector: non-finite entry"}})))
+    return rc;
+  return run_nnls(ctx, d, n, dA, lda, db, cfg, out);
 }
 
 int alnnls_solve_nqp_device(alnnls_ctx* ctx, uint64_t m, const double* dQ, uint64_t ldq,
@@ -986,12 +1017,14 @@ int alnnls_solve_nnls_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const dou
   if (!cfg || !A || !B || !X) return set_err(ctx, ALNNLS_EINVAL, "solve_nnls_batched: null argument");
   if (d < 1 || n < 1 || nrhs < 1)
     return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
-  if (!all_finite(A, d * n) || !all_finite(B, d * nrhs))
-    return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
   int st__ = ALNNLS_OK;
   uint64_t lda = 0, ldb = 0;
   if ((rc = upload_matrix(ctx, ctx->A, d, n, A, &lda))) return rc;
   if ((rc = upload_matrix(ctx, ctx->bcols, d, nrhs, B, &ldb))) return rc;
+  if ((rc = device_check_finite(
+           ctx, {{static_cast<double*>(ctx->A.p), d, n, lda, "DenseMatrix: non-finite entry"},
+                 {static_cast<double*>(ctx->bcols.p), d, nrhs, ldb, "DenseMatrix: non-finite entry"}})))
+    return rc;
   double* dX = ENSURE(double, X, n * nrhs);
   rc = run_batched(ctx, d, n, static_cast<double*>(ctx->A.p), lda, nrhs,
                    static_cast<double*>(ctx->bcols.p), ldb, cfg, dX, cols, out);
