@@ -13,7 +13,8 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 # --fmad=false: no FMA contraction anywhere in the exact path
 NVFLAGS := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xptxas -v \
            -Xcompiler -Wall $(EXTRA)
-CU_SRCS := $(PKG)/csrc/nqp.cu $(PKG)/csrc/setup.cu $(PKG)/csrc/capi.cu $(PKG)/csrc/batched.cu
+CU_SRCS := $(PKG)/csrc/nqp.cu $(PKG)/csrc/setup.cu $(PKG)/csrc/capi.cu $(PKG)/csrc/batched.cu \
+           $(PKG)/csrc/dmma.cu
 CU_HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/alnnls.h
 CU_OBJS := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(CU_SRCS))
 

@@ -273,8 +273,10 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
 }
 
 // ---- setup on device A (lda) and b: rescale(gram(A), -A^T b) -> ctx->Q, q ----
+// profile FAST forms the Gram on the fp64 tensor cores (dmma.cu); EXACT (and
+// FAST when the operands are not 16-byte aligned) uses the bitwise chain SYRK.
 int run_setup(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t lda,
-              const double* db, uint64_t* m_out) {
+              const double* db, uint64_t* m_out, int profile = ALNNLS_PROFILE_EXACT) {
   int st__ = ALNNLS_OK;
   cudaStream_t s = ctx->stream;
   SetupArgs sa{};
@@ -302,7 +304,11 @@ int run_setup(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_
   sa.qR = (int)ctx->qR;
   sa.q = ENSURE(double, q, vec_pad(m));
   if (m > 0) {
-    CK(launch_syrk(sa, 1, s));
+    if (profile == ALNNLS_PROFILE_FAST && syrk_dmma_supported(sa, 1)) {
+      CK(launch_syrk_dmma(sa, 1, s));
+    } else {
+      CK(launch_syrk(sa, 1, s));
+    }
     CK(launch_q_from_atb(sa, 1, s));
   }
   *m_out = m;
@@ -318,7 +324,7 @@ int run_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t
   alnnls_summary sum{};
   CK(cudaEventRecord(ctx->ev[0], s));
   uint64_t m = 0;
-  int rc = run_setup(ctx, d, n, dA, lda, db, &m);
+  int rc = run_setup(ctx, d, n, dA, lda, db, &m, cfg->profile);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev[1], s));
   ctx->last_nnls = true;
@@ -900,7 +906,7 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
   alnnls_summary sum{};
   CK(cudaEventRecord(ctx->ev[0], s));
   uint64_t m = 0;
-  int rc = run_setup(ctx, d, n, dA, lda, nullptr, &m);  // the shared Gram, once
+  int rc = run_setup(ctx, d, n, dA, lda, nullptr, &m, cfg->profile);  // the shared Gram, once
   if (rc) return rc;
   alnnls_column_result* dres = ENSURE(alnnls_column_result, resb, nrhs);
   std::vector<alnnls_column_result> init(nrhs);
@@ -931,7 +937,12 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
     sa.ldb = ldb;
     sa.nrhs = (int)nrhs;
     sa.QB = QB;
-    CK(launch_syrk(sa, 2, s));  // q_j = (-(A^T b_j))[retained] / D for every column
+    // q_j = (-(A^T b_j))[retained] / D for every column
+    if (cfg->profile == ALNNLS_PROFILE_FAST && syrk_dmma_supported(sa, 2)) {
+      CK(launch_syrk_dmma(sa, 2, s));
+    } else {
+      CK(launch_syrk(sa, 2, s));
+    }
     CK(cudaEventRecord(ctx->ev[1], s));
     int* counter = ENSURE(int, mscalar, 4);
     CK(cudaMemsetAsync(counter, 0, sizeof(int), s));

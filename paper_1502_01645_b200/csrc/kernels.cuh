@@ -113,6 +113,10 @@ cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream);
 cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream);
 // mode 0: write H (and -A^T b into hvec when b != nullptr); mode 1: fused rescale into Q, q.
 cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream);
+// FAST profile: the same three modes on the fp64 tensor cores (dmma.cu). Needs
+// even leading dimensions and 16-byte aligned operands (syrk_dmma_supported).
+cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream);
+bool syrk_dmma_supported(const SetupArgs& s, int mode);
 // q (mode 1) or hvec = -(A^T b) (mode 0) from the column chains' A^T b.
 cudaError_t launch_q_from_atb(const SetupArgs& s, int mode, cudaStream_t stream);
 // Rescale from a given H (n x n) and h (n) on device (nnls.hpp:41-83).
