@@ -8,7 +8,7 @@ import os
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libalnnls.so")
+LIB_PATH = os.environ.get("ALNNLS_LIB") or os.path.join(HERE, "lib", "libalnnls.so")
 
 # every symbol include/alnnls.h declares (tests check the .so exports them all)
 EXPORTS = [

@@ -38,7 +38,7 @@ struct alnnls_ctx {
 
   DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
   DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
-      hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb;
+      hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb, uP, gdC;
 
   // last solve
   bool last_nnls = false;
@@ -169,6 +169,8 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   double* gP2 = ENSURE(double, gP2, mp);
   double* xP2 = ENSURE(double, xP2, mp);
   double* qP2 = ENSURE(double, qP2, mp);
+  double* uP = ENSURE(double, uP, mp);
+  double* gdC = ENSURE(double, gdC, mp);
   // per row-CTA partials: cnt (int), badv (int), minx (double)
   double* part = ENSURE(double, part, 3 * 160);
   int* cnt = reinterpret_cast<int*>(part);
@@ -226,6 +228,8 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   a.gP2 = gP2;
   a.xP2 = xP2;
   a.qP2 = qP2;
+  a.uP = uP;
+  a.gdC = gdC;
   a.cnt = cnt;
   a.badv = badv;
   a.minx = minx;
@@ -490,7 +494,7 @@ void alnnls_destroy(alnnls_ctx* ctx) {
                     &ctx->trace,  &ctx->mults, &ctx->ctrl,    &ctx->list,  &ctx->vals, &ctx->ax,
                     &ctx->resid,  &ctx->flag,  &ctx->H,       &ctx->hvec,  &ctx->start, &ctx->bcols,
                     &ctx->X,      &ctx->x_alt, &ctx->mask2,   &ctx->gP2,   &ctx->xP2,  &ctx->qP2,
-                    &ctx->part,   &ctx->resb,  &ctx->yb,      &ctx->qb};
+                    &ctx->part,   &ctx->resb,  &ctx->yb,      &ctx->qb,   &ctx->uP,   &ctx->gdC};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)

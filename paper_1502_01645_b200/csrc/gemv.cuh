@@ -82,12 +82,15 @@ __device__ inline void ring_setup(RowRing& r, uint8_t* smem, size_t bytes, int n
 // `runs` is true (blocked layout, col_stride == seg) consecutive listed
 // columns are fetched with one bulk copy. Warps outside [0, P+cons_warps)
 // return immediately. Every thread must call it (r.pos advances uniformly).
-// Consumers write out[row0 + t]. No block barrier inside.
+// Consumers write out[row0 + t], and, when opos is given, also
+// out_c[opos[t]] for rows with opos[t] >= 0 (a compacted copy). No block
+// barrier inside.
 __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, uint64_t col_stride,
                                  bool runs, int row0, int nrows,
                                  const uint32_t* __restrict__ list,
                                  const double* __restrict__ vals, int len,
-                                 double* __restrict__ out) {
+                                 double* __restrict__ out, const int* opos = nullptr,
+                                 double* __restrict__ out_c = nullptr) {
   const int G = r.G;
   const int nst = (len + G - 1) / G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -170,7 +173,10 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[st]);
     }
-    if (t < nrows) out[row0 + t] = acc;
+    if (t < nrows) {
+      out[row0 + t] = acc;
+      if (opos && opos[t] >= 0) out_c[opos[t]] = acc;
+    }
   }
   r.pos += nst;
 }

@@ -54,6 +54,8 @@ struct LoopArgs {
   double* gP2;
   double* xP2;
   double* qP2;
+  double* uP;       // (Q g_bar) compacted to the passive list: uP[t] = u[mask[t]]
+  double* gdC;      // (Q delta) compacted to the changed list: gdC[t] = gd[chg[t]]
   int* cnt;         // per row-CTA passive counts
   double* minx;     // per row-CTA min(x)
   int* badv;        // per row-CTA non-finite gradient flags

@@ -113,13 +113,25 @@ __device__ void leader_chains(double* sbuf, size_t sbuf_bytes, LeaderState& L, i
   const int CH = min(1024, (int)(sbuf_bytes / (2 * K * sizeof(double))) & ~1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = (len + CH - 1) / CH;
+  // 4 positions per thread per round: all their operand loads are in flight
+  // together before the first shared-memory store
   auto produce = [&](int c, int buf, int first_thread) {
     const int b0 = c * CH;
     const int cnt = min(CH, len - b0);
     double* dst = sbuf + (size_t)buf * K * CH;
-    for (int i = (int)threadIdx.x - first_thread; i < cnt; i += blockDim.x - first_thread)
+    const int nthr = (int)blockDim.x - first_thread;
+    for (int i = (int)threadIdx.x - first_thread; i < cnt; i += 4 * nthr) {
+      double v[4][K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) dst[(size_t)k * CH + i] = prod(k, b0 + i);
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[u][k] = i + u * nthr < cnt ? prod(k, b0 + i + u * nthr) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if (i + u * nthr < cnt) dst[(size_t)k * CH + i + u * nthr] = v[u][k];
+    }
   };
   double s = 0.0;
   if (nch > 0) produce(0, 0, 0);
@@ -293,6 +305,7 @@ struct RowShared {
   int wc[kWarps + 1];
   double wm[kWarps];
   int t_lo, t_hi, base, total;
+  int lpos[2][kLoopThreads];  // passive-list position of each own row (-1: not passive), per list parity
 };
 
 // Passive flags of own rows of (x, g): count -> cnt[b], min(x) -> minx[b],
@@ -354,8 +367,11 @@ __device__ void row_apply(const LoopArgs& a, RowShared& S, int blk, int row0, in
     S.t_hi = lo2;
   }
   __syncthreads();
-  for (int t = S.t_lo + threadIdx.x; t < S.t_hi; t += blockDim.x)
-    xn[__ldcg(a.chg + t)] = __ldcg(a.candC + t);
+  for (int t = S.t_lo + threadIdx.x; t < S.t_hi; t += blockDim.x) {
+    const uint32_t j = __ldcg(a.chg + t);
+    xn[j] = __ldcg(a.candC + t);
+    a.gdC[t] = a.gd[j];  // own rows of P2's result, compacted for the next df chain
+  }
   __syncthreads();
   row_count(a, S, blk, row0, nrows, xn, gn);
 }
@@ -363,7 +379,7 @@ __device__ void row_apply(const LoopArgs& a, RowShared& S, int blk, int row0, in
 // Writes own rows' entries of the ascending passive list at the global offset
 // sum(cnt[0..blk)). Returns the list length (sum of all cnt). Whole row CTA.
 __device__ int row_lists(const LoopArgs& a, RowShared& S, int blk, int nblk, int row0, int nrows,
-                         const double* x, const double* g, const ListSet& L) {
+                         const double* x, const double* g, const ListSet& L, int par) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (warp == 0) {
     int before = 0, all = 0;
@@ -408,6 +424,9 @@ __device__ int row_lists(const LoopArgs& a, RowShared& S, int blk, int nblk, int
     L.gP[pos] = gi;
     L.xP[pos] = xi;
     L.qP[pos] = __ldg(a.q + row0 + t);
+    S.lpos[par][t] = pos;
+  } else if (t < nrows) {
+    S.lpos[par][t] = -1;
   }
   return S.total;
 }
@@ -425,10 +444,23 @@ __device__ void leader_chains_var(double* sbuf, size_t sbuf_bytes, LeaderState& 
   auto produce = [&](int c, int buf, int first_thread) {
     const int b0 = c * CH;
     double* dst = sbuf + (size_t)buf * K * CH;
-    for (int i = (int)threadIdx.x - first_thread; i < CH; i += blockDim.x - first_thread) {
+    const int nthr = (int)blockDim.x - first_thread;
+    for (int i = (int)threadIdx.x - first_thread; i < CH; i += 2 * nthr) {
+      double v[2][K];
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-        if (b0 + i < len[k]) dst[(size_t)k * CH + i] = prod(k, b0 + i);
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int ii = i + u * nthr;
+          v[u][k] = ii < CH && b0 + ii < len[k] ? prod(k, b0 + ii) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int ii = i + u * nthr;
+          if (ii < CH && b0 + ii < len[k]) dst[(size_t)k * CH + ii] = v[u][k];
+        }
     }
   };
   double s = 0.0;
@@ -493,7 +525,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
   const uint64_t t0 = globaltimer_ns();
   if (!leader) row_count(a, RS, blk, row0, nrows, xb[0], gb[0]);
   grid.sync();
-  if (!leader) ml_l[0] = row_lists(a, RS, blk, nblk, row0, nrows, xb[0], gb[0], ls[0]);
+  if (!leader) ml_l[0] = row_lists(a, RS, blk, nblk, row0, nrows, xb[0], gb[0], ls[0], 0);
   if (leader && threadIdx.x == 0) {
     a.ctrl->trace_len = 0;
     a.ctrl->mult_len = 0;
@@ -517,7 +549,9 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
   for (;;) {
     // ===== phase A: P1 (row CTAs) || stop-test chains + pending df (vector CTA) =====
     if (!leader) {
-      gemv_rows(ring, qblk, R, true, row0, nrows, ls[lp].mask, ls[lp].gP, ml_l[lp], a.u);
+      // u = Q g_bar over own rows, also compacted to the passive list for den
+      gemv_rows(ring, qblk, R, true, row0, nrows, ls[lp].mask, ls[lp].gP, ml_l[lp], a.u,
+                RS.lpos[lp], a.uP);
     } else {
       __shared__ int s_ml, s_bad;
       __shared__ double s_mn;
@@ -545,15 +579,14 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
       const ListSet cur = ls[lp];
       const int lens[4] = {ml, ml, ml, PD.on ? PD.cl : 0};
       const double *gP = cur.gP, *xP = cur.xP, *qP = cur.qP;
-      const double *gC = a.gC, *dC = a.dC, *gd = a.gd;
-      const uint32_t* chg = a.chg;
+      const double *gC = a.gC, *dC = a.dC, *gdC = a.gdC;
       // gbs: g_i^2; dot(x, grad): x_i g_i; dot(q, x): q_i x_i (terms off the mask are
       // exact zeros since x_i = 0 there); df of the pending step (nqp.hpp:307)
       leader_chains_var<4>(sbuf, kRingSmemBytes, L, lens, [&](int c, int t) {
         if (c == 0) return xmul(gP[t], gP[t]);
         if (c == 1) return xmul(xP[t], gP[t]);
         if (c == 2) return xmul(qP[t], xP[t]);
-        return xmul(xadd(gC[t], xmul(0.5, __ldcg(gd + chg[t]))), dC[t]);
+        return xmul(xadd(gC[t], xmul(0.5, __ldcg(gdC + t))), dC[t]);
       });
       if (threadIdx.x == 0) {
         const double gbs = L.res[0];
@@ -623,10 +656,9 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
       if (act == kActCont) {
         const int ml = L.mask_len;
         const double* gP = cur.gP;
-        const uint32_t* mask = cur.mask;
-        const double* u = a.u;
+        const double* uP = a.uP;
         leader_chains<1>(sbuf, kRingSmemBytes, L, ml,
-                         [&](int, int t) { return xmul(gP[t], __ldcg(u + mask[t])); });
+                         [&](int, int t) { return xmul(gP[t], __ldcg(uP + t)); });
         if (threadIdx.x == 0) {
           const double den = L.res[0];
           L.mults = (unsigned long long)a.m * (unsigned long long)ml;
@@ -701,7 +733,8 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
     grid.sync();  // B_cnt
     if (leader && threadIdx.x == 0) phase_mark(L, 5);
     if (!leader)
-      ml_l[lp ^ 1] = row_lists(a, RS, blk, nblk, row0, nrows, xb[xp ^ 1], gb[xp ^ 1], ls[lp ^ 1]);
+      ml_l[lp ^ 1] = row_lists(a, RS, blk, nblk, row0, nrows, xb[xp ^ 1], gb[xp ^ 1], ls[lp ^ 1],
+                               lp ^ 1);
     grid.sync();  // B0
     if (leader && threadIdx.x == 0) phase_mark(L, 6);
     xp ^= 1;

@@ -11,7 +11,7 @@ __global__ void __launch_bounds__(384, 1) k_blocked(const double* Qb, int m, int
   const int row0 = blockIdx.x * R;
   const int nrows = max(0, min(m - row0, R));
   RowRing ring;
-  ring_setup(ring, smem, kRingSmemBytes, nrows, R, maxw, true);
+  ring_setup(ring, smem, kRingSmemBytes, nrows, R, maxw);
   gemv_rows(ring, Qb + (size_t)blockIdx.x * R * m, R, true, row0, nrows, list, vals, len, y);
 }
 
