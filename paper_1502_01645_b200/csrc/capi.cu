@@ -38,7 +38,7 @@ struct alnnls_ctx {
 
   DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
   DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
-      hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb, uP, gdC;
+      hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb, uP, gdC, skp, skf;
 
   // last solve
   bool last_nnls = false;
@@ -279,9 +279,24 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
 // ---- setup on device A (lda) and b: rescale(gram(A), -A^T b) -> ctx->Q, q ----
 // profile FAST forms the Gram on the fp64 tensor cores (dmma.cu); EXACT (and
 // FAST when the operands are not 16-byte aligned) uses the bitwise chain SYRK.
+// Scratch of the stream-K exact SYRK (setup.cu syrk_streamk_kernel), when the
+// shape uses it.
+int streamk_buffers(alnnls_ctx* ctx, SetupArgs& sa, int mode) {
+  int st__ = ALNNLS_OK;
+  sa.sk_ctas = syrk_streamk_ctas(sa, mode, ctx->sm_count);
+  sa.sk_part = nullptr;
+  sa.sk_flag = nullptr;
+  if (sa.sk_ctas > 0) {
+    sa.sk_part = ENSURE(double, skp, (size_t)sa.sk_ctas * 32 * 512);
+    sa.sk_flag = ENSURE(int, skf, sa.sk_ctas);
+  }
+  return ALNNLS_OK;
+}
+
 int run_setup(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t lda,
               const double* db, uint64_t* m_out, int profile = ALNNLS_PROFILE_EXACT) {
   int st__ = ALNNLS_OK;
+  int rc_sk = ALNNLS_OK;
   cudaStream_t s = ctx->stream;
   SetupArgs sa{};
   sa.A = dA;
@@ -311,6 +326,7 @@ int run_setup(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_
     if (profile == ALNNLS_PROFILE_FAST && syrk_dmma_supported(sa, 1)) {
       CK(launch_syrk_dmma(sa, 1, s));
     } else {
+      if ((rc_sk = streamk_buffers(ctx, sa, 1))) return rc_sk;
       CK(launch_syrk(sa, 1, s));
     }
     CK(launch_q_from_atb(sa, 1, s));
@@ -494,7 +510,8 @@ void alnnls_destroy(alnnls_ctx* ctx) {
                     &ctx->trace,  &ctx->mults, &ctx->ctrl,    &ctx->list,  &ctx->vals, &ctx->ax,
                     &ctx->resid,  &ctx->flag,  &ctx->H,       &ctx->hvec,  &ctx->start, &ctx->bcols,
                     &ctx->X,      &ctx->x_alt, &ctx->mask2,   &ctx->gP2,   &ctx->xP2,  &ctx->qP2,
-                    &ctx->part,   &ctx->resb,  &ctx->yb,      &ctx->qb,   &ctx->uP,   &ctx->gdC};
+                    &ctx->part,   &ctx->resb,  &ctx->yb,      &ctx->qb,   &ctx->uP,   &ctx->gdC,
+                    &ctx->skp,    &ctx->skf};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
@@ -837,6 +854,7 @@ int alnnls_gram(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, double
   sa.d = (int)d;
   sa.n = (int)n;
   sa.H = dH;
+  if ((rc = streamk_buffers(ctx, sa, 0))) return rc;
   CK(launch_syrk(sa, 0, ctx->stream));
   return copy_out(ctx, H, dH, sizeof(double) * n * n);
 }
@@ -945,6 +963,7 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
     if (cfg->profile == ALNNLS_PROFILE_FAST && syrk_dmma_supported(sa, 2)) {
       CK(launch_syrk_dmma(sa, 2, s));
     } else {
+      if ((rc = streamk_buffers(ctx, sa, 2))) return rc;
       CK(launch_syrk(sa, 2, s));
     }
     CK(cudaEventRecord(ctx->ev[1], s));

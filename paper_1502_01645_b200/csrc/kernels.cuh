@@ -110,7 +110,14 @@ struct SetupArgs {
   uint64_t ldb;
   int nrhs;
   double* QB;       // m x nrhs (ld m)
+  // exact SYRK stream-K scheduling (setup.cu): partial chain states [ctas][32][512]
+  // and per-CTA ready flags; sk_ctas = 0 runs one CTA per tile
+  double* sk_part;
+  int* sk_flag;
+  int sk_ctas;
 };
+// CTAs for the stream-K exact SYRK of this shape (0: use one CTA per tile).
+int syrk_streamk_ctas(const SetupArgs& s, int mode, int sm_count);
 cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream);
 cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream);
 // mode 0: write H (and -A^T b into hvec when b != nullptr); mode 1: fused rescale into Q, q.

@@ -49,19 +49,28 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode) {
-  extern __shared__ __align__(16) double syrk_sm[];
-  auto As = reinterpret_cast<double(*)[BK][LDS]>(syrk_sm);
-  auto Bs = reinterpret_cast<double(*)[BK][LDS]>(syrk_sm + kStages * BK * LDS);
-  // mode 0/1: upper-triangular tiles of A^T A; mode 2: full tiles of A^T B
-  int ti, tj;
+// Output tile t -> (ti, tj): upper-triangular tiles of A^T A (modes 0/1), the
+// full grid of A^T B (mode 2).
+__device__ __forceinline__ void tile_of(const SetupArgs& s, int mode, int t, int& ti, int& tj) {
   if (mode == 2) {
     const int nti = (s.n + BM - 1) / BM;
-    ti = blockIdx.x % nti;
-    tj = blockIdx.x / nti;
+    ti = t % nti;
+    tj = t / nti;
   } else {
-    tri_tile(blockIdx.x, ti, tj);
+    tri_tile(t, ti, tj);
   }
+}
+
+// k slabs [kb0, kb1) of output tile (ti, tj). The 32 accumulators of each
+// thread start from +0, or from a partial chain state `pin` ([32][NT]) that
+// another CTA left after slabs [0, kb0); they end in the epilogue, or are
+// stored to `pout` for the CTA that continues the chain. Either way every
+// output is ONE chain over k ascending, bit for bit the same as one CTA doing
+// all slabs.
+__device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double* smem, int ti, int tj,
+                                           int kb0, int kb1, const double* pin, double* pout) {
+  auto As = reinterpret_cast<double(*)[BK][LDS]>(smem);
+  auto Bs = reinterpret_cast<double(*)[BK][LDS]>(smem + kStages * BK * LDS);
   const int i0 = ti * BM, j0 = tj * BM;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const double* Bop = mode == 2 ? s.B : s.A;
@@ -81,7 +90,7 @@ __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode
     pb[r] = cb < nb ? Bop + (size_t)cb * ldb : nullptr;
   }
   auto issue = [&](int kb) {
-    const int buf = kb % kStages;
+    const int buf = (kb - kb0) % kStages;
     const int k0 = kb * BK;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -97,20 +106,20 @@ __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode
 #pragma unroll
   for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+    for (int c = 0; c < 4; ++c) acc[r][c] = pin ? __ldcg(pin + (size_t)(r * 4 + c) * NT + threadIdx.x) : 0.0;
 
-  const int nk = (s.d + BK - 1) / BK;
+  __syncthreads();  // the previous piece's last slab buffers are no longer read
 #pragma unroll
   for (int p = 0; p < kStages - 1; ++p) {
-    if (p < nk) issue(p);
+    if (kb0 + p < kb1) issue(kb0 + p);
     cp_async_commit();
   }
-  for (int kb = 0; kb < nk; ++kb) {
+  for (int kb = kb0; kb < kb1; ++kb) {
     cp_async_wait<kStages - 2>();  // slab kb has landed (this thread's copies)
     __syncthreads();               // ... everyone's; and slab kb-1's buffer is free
-    if (kb + kStages - 1 < nk) issue(kb + kStages - 1);
+    if (kb + kStages - 1 < kb1) issue(kb + kStages - 1);
     cp_async_commit();
-    const int buf = kb % kStages;
+    const int buf = (kb - kb0) % kStages;
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
       double a[8], b[4];
@@ -137,7 +146,15 @@ __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode
       }
     }
   }
+  cp_async_wait<0>();
 
+  if (pout) {  // hand the chain states to the CTA that finishes this tile
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) pout[(size_t)(r * 4 + c) * NT + threadIdx.x] = acc[r][c];
+    return;
+  }
   // epilogue: upper triangle only, mirrored (exact symmetry, linalg.hpp:169-170)
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
@@ -172,6 +189,66 @@ __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode
   }
 }
 
+// One CTA per output tile.
+__global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode) {
+  extern __shared__ __align__(16) double syrk_sm[];
+  int ti, tj;
+  tile_of(s, mode, blockIdx.x, ti, tj);
+  syrk_piece(s, mode, syrk_sm, ti, tj, 0, (s.d + BK - 1) / BK, nullptr, nullptr);
+}
+
+// Stream-K: one persistent CTA per SM takes an equal contiguous share of the
+// (tile, k-slab) sequence, so the last wave is not partly idle. A tile split
+// between CTA c-1 and CTA c is continued from c-1's chain states: CTA c-1 does
+// its trailing partial tile FIRST and publishes it (flag, release), and CTA c
+// takes its leading partial tile LAST (acquire), so nobody waits in practice.
+// Requires every CTA's share to span at least two tiles (checked on the host)
+// and co-residency (cooperative launch).
+__global__ void __launch_bounds__(NT, 1) syrk_streamk_kernel(SetupArgs s, int mode, int tiles) {
+  extern __shared__ __align__(16) double syrk_sm[];
+  const int nk = (s.d + BK - 1) / BK;
+  const long long total = (long long)tiles * nk;
+  const long long per = (total + gridDim.x - 1) / gridDim.x;
+  const long long u0 = (long long)blockIdx.x * per;
+  const long long u1 = min(total, u0 + per);
+  if (u0 >= u1) return;
+  const int t0 = (int)(u0 / nk), k0 = (int)(u0 % nk);
+  const int t1 = (int)((u1 - 1) / nk), k1 = (int)((u1 - 1) % nk) + 1;
+  double* my_part = s.sk_part + (size_t)blockIdx.x * 32 * NT;
+  int ti, tj;
+  // 1. trailing partial tile: slabs [0, k1) of t1, handed to the next CTA
+  if (k1 < nk) {
+    tile_of(s, mode, t1, ti, tj);
+    syrk_piece(s, mode, syrk_sm, ti, tj, 0, k1, nullptr, my_part);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(s.sk_flag + blockIdx.x), "r"(1u)
+                   : "memory");
+    }
+  }
+  // 2. whole tiles
+  const int full_lo = k0 == 0 ? t0 : t0 + 1;
+  const int full_hi = k1 == nk ? t1 : t1 - 1;
+  for (int t = full_lo; t <= full_hi; ++t) {
+    tile_of(s, mode, t, ti, tj);
+    syrk_piece(s, mode, syrk_sm, ti, tj, 0, nk, nullptr, nullptr);
+  }
+  // 3. leading partial tile: slabs [k0, nk) of t0, continuing CTA blockIdx-1's chains
+  if (k0 > 0) {
+    if (threadIdx.x == 0) {
+      unsigned v = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(s.sk_flag + blockIdx.x - 1)
+                     : "memory");
+      } while (v == 0);
+    }
+    __syncthreads();
+    tile_of(s, mode, t0, ti, tj);
+    syrk_piece(s, mode, syrk_sm, ti, tj, k0, nk, s.sk_part + (size_t)(blockIdx.x - 1) * 32 * NT,
+               nullptr);
+  }
+}
 // q_b = h(j_b) / D_b with h = -(A^T b) (nnls.hpp:79, :133-134); atb = A^T b.
 __global__ void q_from_atb_kernel(const double* atb, const int* pos, const double* scale, int n,
                                   double* q, double* hvec) {
@@ -437,6 +514,16 @@ cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+int syrk_streamk_ctas(const SetupArgs& s, int mode, int sm_count) {
+  const int nt = (s.n + BM - 1) / BM;
+  const long long tiles = mode == 2 ? (long long)nt * ((s.nrhs + BM - 1) / BM) : (long long)nt * (nt + 1) / 2;
+  const long long nk = (s.d + BK - 1) / BK;
+  // stream-K only pays when the tile grid leaves a ragged last wave, and needs
+  // every share to span >= 2 tiles (one partial tile at each end at most)
+  if (tiles < 2LL * sm_count || tiles % sm_count == 0 || nk < 2) return 0;
+  return sm_count;
+}
+
 cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream) {
   const int nt = (s.n + BM - 1) / BM;
   const int tiles = mode == 2 ? nt * ((s.nrhs + BM - 1) / BM) : nt * (nt + 1) / 2;
@@ -445,8 +532,20 @@ cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream) {
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(syrk_exact_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(syrk_streamk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kSyrkSmem);
     if (e != cudaSuccess) return e;
     attr = true;
+  }
+  if (s.sk_part && s.sk_flag && s.sk_ctas > 0) {
+    cudaError_t e = cudaMemsetAsync(s.sk_flag, 0, sizeof(int) * s.sk_ctas, stream);
+    if (e != cudaSuccess) return e;
+    SetupArgs sa = s;
+    int md = mode, tl = tiles;
+    void* args[] = {&sa, &md, &tl};
+    return cudaLaunchCooperativeKernel((const void*)syrk_streamk_kernel, dim3(s.sk_ctas), dim3(NT),
+                                       args, kSyrkSmem, stream);
   }
   syrk_exact_kernel<<<tiles, NT, kSyrkSmem, stream>>>(s, mode);
   return cudaGetLastError();
