@@ -212,6 +212,40 @@ int alnnls_solve_nnls_batched_device(alnnls_ctx* ctx, uint64_t d, uint64_t n,
                                      const alnnls_config* cfg, double* dX,
                                      alnnls_column_result* cols, alnnls_summary* out);
 
+/* ---- multi-GPU exact setup by row blocks -----------
+ * A is split into row blocks A_0, A_1, ... (ranks). Every sum of the
+ * reference setup is one ascending chain over the rows (gram linalg.hpp:168,
+ * transpose_matvec :215, residual_norm_sq nnls.hpp:119-122), so a block can
+ * continue the chain states left by the blocks before it: feeding the blocks
+ * in row order reproduces the single-GPU results bit for bit.
+ * Gram states are kept per upper-triangular 128 x 128 output tile
+ * (ALNNLS_GRAM_TILE_DOUBLES doubles per tile, an opaque layout); all buffers
+ * are device pointers, and the calls return after their work is complete. */
+#define ALNNLS_GRAM_TILE_DOUBLES 16384
+uint64_t alnnls_gram_tiles(uint64_t n);
+/* Tiles [tile_lo, tile_hi) over the block (rows x n, ld lda): from dpin
+ * (states after the earlier blocks, tile t at (t - tile_lo) * TILE_DOUBLES;
+ * NULL = first block) to dpout (same layout), or, when dpout is NULL, the
+ * finished Gram entries of those tiles into dH (n x n, column-major). */
+int alnnls_gram_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const double* dA,
+                                uint64_t lda, uint64_t tile_lo, uint64_t tile_hi,
+                                const double* dpin, double* dpout, double* dH);
+/* A^T b chains over the block: dout[j] = dpin[j] (or 0) + sum over the block rows
+ * in order (transpose_matvec, before the negation of nnls.hpp:133-134). */
+int alnnls_atb_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const double* dA,
+                               uint64_t lda, const double* db, const double* dpin, double* dout);
+/* solve_nnls from the finished Gram dH (n x n) and A^T b chains dAtb: rescale,
+ * solve_nqp, unscale (nnls.hpp:133-141). The residual needs A and b and is
+ * formed by the ranks with alnnls_residual_rowblock_device; out->residual_sq is 0. */
+int alnnls_solve_nnls_gram_device(alnnls_ctx* ctx, uint64_t n, const double* dH,
+                                  const double* dAtb, const alnnls_config* cfg,
+                                  alnnls_summary* out);
+/* residual_norm_sq over the block's rows, continuing the ordered chain from s_in
+ * (0 for the first block): *s_out = ((s_in + r_0^2) + r_1^2) + ..., r = A_blk x - b_blk. */
+int alnnls_residual_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const double* dA,
+                                    uint64_t lda, const double* db, const double* dx, double s_in,
+                                    double* s_out);
+
 #ifdef __cplusplus
 }
 #endif

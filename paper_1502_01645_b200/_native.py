@@ -21,6 +21,8 @@ EXPORTS = [
     "alnnls_rescale", "alnnls_gram", "alnnls_transpose_matvec", "alnnls_matvec",
     "alnnls_masked_matvec", "alnnls_solve_nnls_batched", "alnnls_solve_nnls_batched_device",
     "alnnls_timer_start", "alnnls_timer_stop", "alnnls_launch_count",
+    "alnnls_gram_tiles", "alnnls_gram_rowblock_device", "alnnls_atb_rowblock_device",
+    "alnnls_solve_nnls_gram_device", "alnnls_residual_rowblock_device",
 ]
 
 _lib = None
@@ -78,6 +80,13 @@ def load():
                                        C.POINTER(abi.Summary)], i32),
         "alnnls_solve_nnls_batched_device": ([vp, u64, u64, vp, u64, vp, C.POINTER(abi.Config),
                                               vp, vp, C.POINTER(abi.Summary)], i32),
+        "alnnls_gram_tiles": ([u64], u64),
+        "alnnls_gram_rowblock_device": ([vp, u64, u64, vp, u64, u64, u64, vp, vp, vp], i32),
+        "alnnls_atb_rowblock_device": ([vp, u64, u64, vp, u64, vp, vp, vp], i32),
+        "alnnls_solve_nnls_gram_device": ([vp, u64, vp, vp, C.POINTER(abi.Config),
+                                           C.POINTER(abi.Summary)], i32),
+        "alnnls_residual_rowblock_device": ([vp, u64, u64, vp, u64, vp, vp, C.c_double,
+                                             C.POINTER(C.c_double)], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

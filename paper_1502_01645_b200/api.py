@@ -241,6 +241,44 @@ class Solver:
                           timings={"setup_s": s.t_setup_s, "loop_s": s.t_loop_s,
                                    "finish_s": s.t_finish_s, "total_s": s.t_total_s})
 
+    # ---- multi-GPU exact setup by row blocks (include/alnnls.h) ----
+    GRAM_TILE_DOUBLES = 16384
+
+    def gram_tiles(self, n):
+        return int(self.lib.alnnls_gram_tiles(n))
+
+    def gram_rowblock_device(self, rows, n, A_ptr, lda, tile_lo, tile_hi, pin_ptr=0, pout_ptr=0,
+                             H_ptr=0):
+        """Continues the Gram tiles [tile_lo, tile_hi) over a row block (device pointers)."""
+        self._check(self.lib.alnnls_gram_rowblock_device(
+            self.ctx, rows, n, C.c_void_p(A_ptr), lda, tile_lo, tile_hi,
+            C.c_void_p(pin_ptr) if pin_ptr else None, C.c_void_p(pout_ptr) if pout_ptr else None,
+            C.c_void_p(H_ptr) if H_ptr else None))
+
+    def atb_rowblock_device(self, rows, n, A_ptr, lda, b_ptr, pin_ptr, out_ptr):
+        self._check(self.lib.alnnls_atb_rowblock_device(
+            self.ctx, rows, n, C.c_void_p(A_ptr), lda, C.c_void_p(b_ptr),
+            C.c_void_p(pin_ptr) if pin_ptr else None, C.c_void_p(out_ptr)))
+
+    def solve_nnls_gram_device(self, n, H_ptr, atb_ptr, config: SolverConfig = SolverConfig(),
+                               fetch=True):
+        """rescale + solve_nqp + unscale from a finished Gram and A^T b chains."""
+        self._summary = abi.Summary()
+        cfg = config.to_abi()
+        st = self.lib.alnnls_solve_nnls_gram_device(self.ctx, n, C.c_void_p(H_ptr),
+                                                    C.c_void_p(atb_ptr), C.byref(cfg),
+                                                    C.byref(self._summary))
+        if st != abi.OK:
+            self._raise(st)
+        return self._nnls_result() if fetch else self._summary
+
+    def residual_rowblock_device(self, rows, n, A_ptr, lda, b_ptr, x_ptr, s_in=0.0):
+        out = C.c_double(0.0)
+        self._check(self.lib.alnnls_residual_rowblock_device(
+            self.ctx, rows, n, C.c_void_p(A_ptr), lda, C.c_void_p(b_ptr), C.c_void_p(x_ptr),
+            float(s_in), C.byref(out)))
+        return out.value
+
     def solve_nnls_batched(self, A, B, config: SolverConfig = SolverConfig()):
         """solve_nnls(A, B[:, j], config) for every column j (bitwise, exact profile).
         Returns (X (n x nrhs), [per-column dict], summary timings)."""

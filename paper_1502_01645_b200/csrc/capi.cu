@@ -1066,4 +1066,150 @@ int alnnls_solve_nnls_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const dou
   return copy_out(ctx, X, dX, sizeof(double) * n * nrhs);
 }
 
+// ---- multi-GPU exact setup by row blocks ----------------------------------------------
+
+uint64_t alnnls_gram_tiles(uint64_t n) { return gram_tiles(n); }
+
+int alnnls_gram_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const double* dA,
+                                uint64_t lda, uint64_t tile_lo, uint64_t tile_hi,
+                                const double* dpin, double* dpout, double* dH) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!dA || rows < 1 || n < 1 || lda < rows || tile_hi < tile_lo || tile_hi > gram_tiles(n) ||
+      (!dpout && !dH))
+    return set_err(ctx, ALNNLS_EINVAL, "gram_rowblock: bad argument");
+  SetupArgs sa{};
+  sa.A = dA;
+  sa.lda = lda;
+  sa.d = (int)rows;
+  sa.n = (int)n;
+  sa.H = dH;
+  CK(launch_syrk_rowblock(sa, (int)tile_lo, (int)(tile_hi - tile_lo), dpin, dpout, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ALNNLS_OK;
+}
+
+int alnnls_atb_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const double* dA,
+                               uint64_t lda, const double* db, const double* dpin, double* dout) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!dA || !db || !dout || rows < 1 || n < 1 || lda < rows)
+    return set_err(ctx, ALNNLS_EINVAL, "atb_rowblock: bad argument");
+  CK(launch_coldot(dA, lda, (int)rows, (int)n, db, dout, ctx->stream, dpin));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ALNNLS_OK;
+}
+
+int alnnls_solve_nnls_gram_device(alnnls_ctx* ctx, uint64_t n, const double* dH,
+                                  const double* dAtb, const alnnls_config* cfg,
+                                  alnnls_summary* out) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!dH || !dAtb || !cfg || n < 1) return set_err(ctx, ALNNLS_EINVAL, "solve_nnls_gram: bad argument");
+  int st__ = ALNNLS_OK;
+  cudaStream_t s = ctx->stream;
+  alnnls_summary sum{};
+  CK(cudaEventRecord(ctx->ev[0], s));
+  // rescale (nnls.hpp:41-83) from H and h = -A^T b
+  SetupArgs sa{};
+  sa.n = (int)n;
+  sa.diag = ENSURE(double, diag, n);
+  sa.pos = ENSURE(int, pos, n);
+  sa.scale = ENSURE(double, scale, n);
+  sa.retained = ENSURE(uint32_t, retained, n);
+  sa.m_out = ENSURE(int, mscalar, 4);
+  double* h = ENSURE(double, hvec, n);
+  CK(launch_diag(dH, (int)n, sa.diag, s));
+  CK(launch_negate(dAtb, (int)n, h, s));
+  CK(launch_retained(sa, s));
+  int hm = 0;
+  CK(cudaMemcpyAsync(&hm, sa.m_out, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint64_t m = (uint64_t)hm;
+  const uint64_t mm = m > 0 ? m : 1;
+  ctx->qR = (uint64_t)nqp_rows_per_cta((int)mm, ctx->sm_count);
+  double* Q = ENSURE(double, Q, blocked_size(mm, ctx->qR));
+  double* q = ENSURE(double, q, vec_pad(m));
+  if (m > 0)
+    CK(launch_rescale_from_h(dH, h, (int)n, sa.pos, sa.scale, Q, (int)m, (int)ctx->qR, q, s));
+  ctx->have_setup = true;
+  CK(cudaEventRecord(ctx->ev[1], s));
+  ctx->last_nnls = true;
+  ctx->last_n = n;
+  ctx->last_m = m;
+  double* y = ENSURE(double, y_out, mm);
+  if (m > 0) {
+    Resolved r;
+    if ((rc = resolve(ctx, cfg, m, &r))) return rc;
+    rc = run_nqp(ctx, m, r, cfg, nullptr, &sum);
+    if (rc) {
+      if (out) *out = sum;
+      ctx->last = sum;
+      return rc;
+    }
+    CK(cudaMemcpyAsync(y, ctx->g_parity ? ctx->x_alt.p : ctx->x.p, sizeof(double) * m,
+                       cudaMemcpyDeviceToDevice, s));
+  } else {
+    alnnls_iter_record rec{};
+    alnnls_iter_record* tr = ENSURE(alnnls_iter_record, trace, 2);
+    CK(cudaMemcpyAsync(tr, &rec, sizeof(rec), cudaMemcpyHostToDevice, s));
+    sum.termination = ALNNLS_EMPTY_PASSIVE_SET;
+    sum.trace_len = 1;
+    CK(cudaEventRecord(ctx->ev[2], s));
+    CK(cudaEventRecord(ctx->ev[3], s));
+  }
+  double* xn = ENSURE(double, X, n);
+  CK(launch_unscale(y, sa.scale, sa.retained, (int)m, xn, (int)n, s));
+  CK(cudaEventRecord(ctx->ev[4], s));
+  CK(cudaStreamSynchronize(s));
+  float t01 = 0, t23 = 0, t34 = 0, t04 = 0;
+  cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
+  cudaEventElapsedTime(&t34, ctx->ev[3], ctx->ev[4]);
+  cudaEventElapsedTime(&t04, ctx->ev[0], ctx->ev[4]);
+  sum.t_setup_s = t01 * 1e-3;
+  sum.t_loop_s = t23 * 1e-3;
+  sum.t_finish_s = t34 * 1e-3;
+  sum.t_total_s = t04 * 1e-3;
+  sum.n = n;
+  sum.m = m;
+  sum.n_dropped = n - m;
+  ctx->last = sum;
+  if (out) *out = sum;
+  return ALNNLS_OK;
+}
+
+int alnnls_residual_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const double* dA,
+                                    uint64_t lda, const double* db, const double* dx, double s_in,
+                                    double* s_out) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!dA || !db || !dx || !s_out || rows < 1 || n < 1 || lda < rows)
+    return set_err(ctx, ALNNLS_EINVAL, "residual_rowblock: bad argument");
+  int st__ = ALNNLS_OK;
+  cudaStream_t s = ctx->stream;
+  // matvec over the support of x (zero x_j terms are exact no-ops), then the chain
+  uint32_t* list = ENSURE(uint32_t, list, n);
+  double* vals = ENSURE(double, vals, n + 8);
+  int* len = ENSURE(int, mscalar, 4);
+  CK(launch_support(dx, (int)n, list, vals, len, s));
+  int hlen = 0;
+  CK(cudaMemcpyAsync(&hlen, len, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  double* ax = ENSURE(double, ax, rows);
+  double* pr = ENSURE(double, bcols, rows + 8);
+  double* res = ENSURE(double, resid, 2);
+  const double* A = dA;
+  uint64_t ld = lda;
+  if ((lda & 1) || (reinterpret_cast<uintptr_t>(dA) & 15)) {  // the bulk-copy GEMV's alignment
+    double* dst = ENSURE(double, A, round_up(rows, 4) * n);
+    CK(launch_copy_pad(dA, lda, dst, round_up(rows, 4), rows, n, s));
+    A = dst;
+    ld = round_up(rows, 4);
+  }
+  CK(launch_masked_gemv(A, ld, (int)rows, list, vals, hlen, ax, ctx->sm_count, s));
+  CK(launch_residual(ax, db, (int)rows, pr, res, s, s_in));
+  return copy_out(ctx, s_out, res, sizeof(double));
+}
+
 }  // extern "C"

@@ -155,8 +155,12 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* scratch, int* to
 
 // Sequential sum s = ((0 + p0) + p1) + ... in index order, products already
 // rounded. One thread; loads are batched ahead of the dependent DADD chain.
+__device__ __forceinline__ double chain_sum_from(double s, const double* __restrict__ p, int len);
 __device__ __forceinline__ double chain_sum(const double* __restrict__ p, int len) {
-  double s = 0.0;
+  return chain_sum_from(0.0, p, len);
+}
+// s = ((s0 + p0) + p1) + ... : continues a chain left by earlier row blocks.
+__device__ __forceinline__ double chain_sum_from(double s, const double* __restrict__ p, int len) {
   constexpr int B = 16;
   int t = 0;
   double buf[B];

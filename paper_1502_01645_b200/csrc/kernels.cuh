@@ -147,13 +147,21 @@ cudaError_t launch_unscale(const double* y, const double* scale, const uint32_t*
                            double* x, int n, cudaStream_t stream);
 // residual_norm_sq (nnls.hpp:115-123): r_i = (A x)_i - b_i, s = sum r_i^2 in order.
 cudaError_t launch_residual(const double* ax, const double* b, int d, double* prod, double* out,
-                            cudaStream_t stream);
+                            cudaStream_t stream, double s0 = 0.0);
 // Compaction of the support of x (x_j != 0, ascending) for matvec(A, x).
 cudaError_t launch_support(const double* x, int n, uint32_t* list, double* vals, int* len,
                            cudaStream_t stream);
 // transpose_matvec: y_j = sum_i M[i,j] v_i (linalg.hpp:209-219)
 cudaError_t launch_coldot(const double* M, uint64_t ld, int rows, int cols, const double* v,
-                          double* y, cudaStream_t stream);
+                          double* y, cudaStream_t stream, const double* y0 = nullptr);
+// Multi-GPU exact Gram by row blocks (setup.cu syrk_rowblock_kernel): tile count,
+// and continuation of tiles [tile_lo, tile_lo + ntiles) over the rows of s.A
+// from chain states pin to pout ([ntiles][32][512]; pout == nullptr writes s.H).
+uint64_t gram_tiles(uint64_t n);
+cudaError_t launch_syrk_rowblock(const SetupArgs& s, int tile_lo, int ntiles, const double* pin,
+                                 double* pout, cudaStream_t stream);
+cudaError_t launch_diag(const double* H, int n, double* diag, cudaStream_t stream);
+cudaError_t launch_negate(const double* x, int n, double* y, cudaStream_t stream);
 // g = y + q (warm start, nqp.hpp:232-233)
 cudaError_t launch_add(const double* y, const double* q, double* g, int m, cudaStream_t stream);
 // any non-finite entry among `count` doubles (strided columns) -> *flag = 1

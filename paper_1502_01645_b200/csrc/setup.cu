@@ -377,13 +377,13 @@ __global__ void unscale_kernel(const double* y, const double* scale, const uint3
 
 // r_i = ax_i - b_i; prod_i = r_i*r_i in parallel; then one ordered chain.
 __global__ void residual_kernel(const double* ax, const double* b, int d, double* prod,
-                                double* out) {
+                                double* out, double s0) {
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const double r = xsub(ax[i], b[i]);
     prod[i] = xmul(r, r);
   }
   __syncthreads();
-  if (threadIdx.x == 0) *out = chain_sum(prod, d);
+  if (threadIdx.x == 0) *out = chain_sum_from(s0, prod, d);
 }
 
 __global__ void support_kernel(const double* x, int n, uint32_t* list, double* vals, int* len) {
@@ -407,11 +407,11 @@ __global__ void support_kernel(const double* x, int n, uint32_t* list, double* v
 
 // y_j = sum_i M[i, j] v_i, one ascending chain per column (linalg.hpp:209-219).
 __global__ void coldot_kernel(const double* M, uint64_t ld, int rows, int cols, const double* v,
-                              double* y) {
+                              double* y, const double* y0) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   const double* p = M + (size_t)c * ld;
-  double acc = 0.0;
+  double acc = y0 ? y0[c] : 0.0;  // y0: chain states after earlier row blocks
   int k = 0;
   constexpr int B = 8;
   for (; k + B <= rows; k += B) {
@@ -514,6 +514,32 @@ cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// Row-block continuation (multi-GPU exact Gram): tiles
+// [tile_lo, tile_lo + gridDim.x) over the block's rows s.A[0, s.d), starting
+// from the chain states `pin` the previous row blocks left (nullptr: start of
+// the chains) and ending in `pout` (nullptr: finish, write H). The states of a
+// tile are the kernel's thread layout [32][NT]; feeding the row blocks in order
+// is the reference's single ascending-k chain per entry.
+__global__ void __launch_bounds__(NT, 1) syrk_rowblock_kernel(SetupArgs s, int tile_lo,
+                                                              const double* pin, double* pout) {
+  extern __shared__ __align__(16) double syrk_sm[];
+  int ti, tj;
+  tile_of(s, 0, tile_lo + (int)blockIdx.x, ti, tj);
+  const size_t off = (size_t)blockIdx.x * 32 * NT;
+  syrk_piece(s, 0, syrk_sm, ti, tj, 0, (s.d + BK - 1) / BK, pin ? pin + off : nullptr,
+             pout ? pout + off : nullptr);
+}
+
+__global__ void diag_kernel(const double* H, int n, double* diag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) diag[i] = H[(size_t)i * n + i];
+}
+
+__global__ void negate_kernel(const double* x, int n, double* y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = -x[i];
+}
+
 int syrk_streamk_ctas(const SetupArgs& s, int mode, int sm_count) {
   const int nt = (s.n + BM - 1) / BM;
   const long long tiles = mode == 2 ? (long long)nt * ((s.nrhs + BM - 1) / BM) : (long long)nt * (nt + 1) / 2;
@@ -569,8 +595,8 @@ cudaError_t launch_unscale(const double* y, const double* scale, const uint32_t*
 }
 
 cudaError_t launch_residual(const double* ax, const double* b, int d, double* prod, double* out,
-                            cudaStream_t stream) {
-  residual_kernel<<<1, 1024, 0, stream>>>(ax, b, d, prod, out);
+                            cudaStream_t stream, double s0) {
+  residual_kernel<<<1, 1024, 0, stream>>>(ax, b, d, prod, out, s0);
   return cudaGetLastError();
 }
 
@@ -581,9 +607,9 @@ cudaError_t launch_support(const double* x, int n, uint32_t* list, double* vals,
 }
 
 cudaError_t launch_coldot(const double* M, uint64_t ld, int rows, int cols, const double* v,
-                          double* y, cudaStream_t stream) {
+                          double* y, cudaStream_t stream, const double* y0) {
   if (cols <= 0) return cudaSuccess;
-  coldot_kernel<<<(cols + 127) / 128, 128, 0, stream>>>(M, ld, rows, cols, v, y);
+  coldot_kernel<<<(cols + 127) / 128, 128, 0, stream>>>(M, ld, rows, cols, v, y, y0);
   return cudaGetLastError();
 }
 
@@ -611,4 +637,34 @@ cudaError_t launch_copy_pad(const double* src, uint64_t ld_src, double* dst, uin
   return cudaGetLastError();
 }
 
+}  // namespace alnnls
+
+namespace alnnls {
+uint64_t gram_tiles(uint64_t n) {
+  const uint64_t nt = (n + BM - 1) / BM;
+  return nt * (nt + 1) / 2;
+}
+cudaError_t launch_syrk_rowblock(const SetupArgs& s, int tile_lo, int ntiles, const double* pin,
+                                 double* pout, cudaStream_t stream) {
+  if (ntiles <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(syrk_rowblock_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  syrk_rowblock_kernel<<<ntiles, NT, kSyrkSmem, stream>>>(s, tile_lo, pin, pout);
+  return cudaGetLastError();
+}
+cudaError_t launch_diag(const double* H, int n, double* diag, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  diag_kernel<<<(n + 255) / 256, 256, 0, stream>>>(H, n, diag);
+  return cudaGetLastError();
+}
+cudaError_t launch_negate(const double* x, int n, double* y, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  negate_kernel<<<(n + 255) / 256, 256, 0, stream>>>(x, n, y);
+  return cudaGetLastError();
+}
 }  // namespace alnnls

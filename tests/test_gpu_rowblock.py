@@ -1,0 +1,73 @@
+"""Exact multi-GPU setup by row blocks (c5) on ONE GPU: the row
+blocks are fed one after another through the same C-ABI entries the ranks call,
+and the results must be bitwise the single-call reference functions (gram,
+transpose_matvec, solve_nnls, residual_norm_sq)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_1502_01645_b200.api import SolverConfig
+from paper_1502_01645_b200.rowblock import row_split
+from tests.parity import same_bits
+
+pytestmark = pytest.mark.gpu
+TD = 16384
+
+
+def run_blocks(solver, A, b, blocks, batches):
+    d, n = A.shape
+    dA = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()  # column-major A, ld = d
+    db = torch.from_numpy(b).cuda()
+    T = solver.gram_tiles(n)
+    H = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    states = None
+    for p, (r0, r1) in enumerate(blocks):
+        last = p == len(blocks) - 1
+        out = None if last else torch.empty(T * TD, dtype=torch.float64, device="cuda")
+        for t0, t1 in batches(T):
+            pin = states[t0 * TD:] if states is not None else None
+            pout = out[t0 * TD:] if out is not None else None
+            solver.gram_rowblock_device(r1 - r0, n, dA.data_ptr() + 8 * r0, d, t0, t1,
+                                        pin.data_ptr() if pin is not None else 0,
+                                        pout.data_ptr() if pout is not None else 0,
+                                        0 if pout is not None else H.data_ptr())
+        states = out
+    atb = None
+    for (r0, r1) in blocks:
+        nxt = torch.empty(n, dtype=torch.float64, device="cuda")
+        solver.atb_rowblock_device(r1 - r0, n, dA.data_ptr() + 8 * r0, d, db.data_ptr() + 8 * r0,
+                                   atb.data_ptr() if atb is not None else 0, nxt.data_ptr())
+        atb = nxt
+    return dA, db, H, atb
+
+
+@pytest.mark.parametrize("d,n,nblk", [(700, 300, 3), (257, 129, 2), (1000, 520, 4)])
+def test_rowblock_gram_and_atb_bitwise(solver, oracle, d, n, nblk):
+    rng = np.random.default_rng(d + n)
+    A = np.asfortranarray(rng.standard_normal((d, n)))
+    b = rng.standard_normal(d)
+    _, _, H, atb = run_blocks(solver, A, b, row_split(d, nblk),
+                              lambda T: [(t, min(T, t + 2)) for t in range(0, T, 2)])
+    Href = oracle.gram(A)
+    assert same_bits(H.cpu().numpy().reshape(-1, order="F"), Href.reshape(-1, order="F"))
+    assert same_bits(atb.cpu().numpy(), oracle.transpose_matvec(A, b))
+
+
+def test_rowblock_solve_and_residual_bitwise(solver):
+    from paper_1502_01645_b200 import instances
+    inst = instances.make_config("c5", d=1200, n=600)
+    A, b = inst["A"], inst["b"]
+    cfg = SolverConfig(epsilon=inst["epsilon"], stall_window=10**9)
+    ref = solver.solve_nnls(A, b, cfg)
+    blocks = row_split(A.shape[0], 3)
+    dA, db, H, atb = run_blocks(solver, A, b, blocks, lambda T: [(0, T)])
+    got = solver.solve_nnls_gram_device(A.shape[1], H.data_ptr(), atb.data_ptr(), cfg)
+    assert same_bits(got.x, ref.x)
+    assert got.inner.iterations() == ref.inner.iterations()
+    assert same_bits([r.f for r in got.inner.trace], [r.f for r in ref.inner.trace])
+    dx = torch.from_numpy(got.x).cuda()
+    s = 0.0
+    for (r0, r1) in blocks:
+        s = solver.residual_rowblock_device(r1 - r0, A.shape[1], dA.data_ptr() + 8 * r0, A.shape[0],
+                                            db.data_ptr() + 8 * r0, dx.data_ptr(), s)
+    assert same_bits([s], [ref.residual_sq])
