@@ -17,6 +17,12 @@ the timed region. Timing: CUDA events on the library's stream, max over ranks.
 N > 1 runs one independent replica per GPU ("replicas only": one solve's
 iteration loop does not shard).
 
+--workload c5 with N > 1 (configs[4]): A's rows are split across the ranks and
+the exact setup runs as a row-block pipeline (rowblock.py): every rank
+continues the Gram tile chains of the ranks before it and passes them on over
+NCCL, the last rank rescales and iterates, the residual chain is relayed back
+through the ranks. Bitwise equal to the single-GPU solve; "scaling": "strong".
+
 --workload c4 (configs[3]): a step is the whole batched solve of B (20000 x
 65536) against the shared Q; the 65536 right-hand sides are split by column
 across the N ranks with no data-path collective ("scaling": "strong"), and
@@ -118,7 +124,7 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
-    if ws > 1:
+    if ws > 1 or os.environ.get("ALNNLS_FORCE_ROWBLOCK"):
         import torch.distributed as dist  # noqa
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         backend = "nccl" if args.impl == "ours" else "gloo"
@@ -361,7 +367,8 @@ def run_ours(args, ws, rank, local, dist):
         "data": "synthetic (seeded SplitMix64, BASELINE.json configs)",
         "config": {"workload": f"{args.workload}: d={d}, n={n}", "eps": inst["epsilon"],
                    "stall_window": "off", "profile": "exact (bitwise reference trajectory)",
-                   "l2": "inputs larger than L2 (A 268 MB, Q 134 MB at c2)",
+                   "l2": (f"inputs larger than L2 (A {8 * d * n / 1e6:.0f} MB, "
+                          f"Q {8 * n * n / 1e6:.0f} MB)"),
                    "parallelism": f"replicas x{ws}"},
         "iterations": iters, "time_to_tol_ms": t_max / args.steps * 1e3,
         "iters_per_s": iters / per_loop if per_loop > 0 else None,
@@ -380,6 +387,95 @@ def run_ours(args, ws, rank, local, dist):
                        "transpose_matvec, rescale, solve_nqp, unscale, residual on the full "
                        "problem (H from the bit-identical GPU gram); single thread"),
             "breakdown": detail}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- c5 at N > 1: exact row-block setup pipeline ------------------------------------------
+def run_ours_rowblock(args, ws, rank, local, dist):
+    import torch
+    from paper_1502_01645_b200.api import Solver
+    from paper_1502_01645_b200.rowblock import chain_relay, pipelined_gram, row_split
+    torch.cuda.set_device(local)
+    inst = instances.make_config(args.workload)
+    A, b = inst["A"], inst["b"]
+    d, n = A.shape
+    r0, r1 = row_split(d, ws)[rank]
+    rows = r1 - r0
+    cfg = solver_config(inst)
+    s = Solver(local)
+    dA = torch.from_numpy(np.ascontiguousarray(A[r0:r1, :].T)).cuda()  # block, column-major, ld rows
+    db = torch.from_numpy(np.ascontiguousarray(b[r0:r1])).cuda()
+    del A
+    T = s.gram_tiles(n)
+    TD = s.GRAM_TILE_DOUBLES
+    batch = 2 * 148
+    last = rank == ws - 1
+    H = torch.empty((n, n), dtype=torch.float64, device="cuda") if last else None
+    sync = torch.cuda.synchronize
+
+    def step():
+        def gram_batch(t0, t1, pin, pout):
+            s.gram_rowblock_device(rows, n, dA.data_ptr(), rows, t0, t1,
+                                   pin.data_ptr() if pin is not None else 0,
+                                   pout.data_ptr() if pout is not None else 0,
+                                   H.data_ptr() if pout is None else 0)
+        pipelined_gram(dist, rank, ws, T, batch, TD, gram_batch, "cuda", sync=sync)
+
+        def atb(pin):
+            out = torch.empty(n, dtype=torch.float64, device="cuda")
+            s.atb_rowblock_device(rows, n, dA.data_ptr(), rows, db.data_ptr(),
+                                  pin.data_ptr() if pin is not None else 0, out.data_ptr())
+            return out
+        h = chain_relay(dist, rank, ws, torch.empty(n, dtype=torch.float64, device="cuda"), atb,
+                        sync=sync)
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        iters = 0
+        if last:
+            summ = s.solve_nnls_gram_device(n, H.data_ptr(), h.data_ptr(), cfg, fetch=False)
+            iters = int(summ.iterations)
+            x.copy_(torch.from_numpy(s._vec(s.lib.alnnls_get_x, n)).cuda())
+        dist.broadcast(x, src=ws - 1)
+        sync()
+
+        def resid(pin):
+            v = s.residual_rowblock_device(rows, n, dA.data_ptr(), rows, db.data_ptr(), x.data_ptr(),
+                                           float(pin[0]) if pin is not None else 0.0)
+            return torch.tensor([v], dtype=torch.float64, device="cuda")
+        r = chain_relay(dist, rank, ws, torch.empty(1, dtype=torch.float64, device="cuda"), resid,
+                        sync=sync)
+        return iters, (float(r[0]) if r is not None else None)
+
+    for _ in range(args.warmup):
+        iters, _ = step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            iters, res = step()
+        ev1.record()
+        torch.cuda.synchronize()
+    t = ev0.elapsed_time(ev1) * 1e-3
+    tt = torch.tensor([t, float(iters)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max, iters = float(tt[0]), int(tt[1])
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": args.steps / t_max, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64, BASELINE.json configs[4])",
+        "config": {"workload": f"{args.workload}: d={d}, n={n}", "eps": inst["epsilon"],
+                   "stall_window": "off", "profile": "exact (bitwise reference trajectory)",
+                   "parallelism": f"row blocks x{ws}: k-chain Gram pipeline (NCCL send/recv), "
+                                  "iterations on the last rank",
+                   "l2": "inputs larger than L2"},
+        "iterations": iters, "gpu_launches": None, "clocks": clk.summary(),
+        "e2e": None,
+    }
     print(json.dumps(line), flush=True)
     return 0
 
@@ -579,6 +675,8 @@ def main():
             return run_reference(args, ws, rank)
         if args.workload == "c4":
             return run_ours_batched(args, ws, rank, local, dist)
+        if args.workload == "c5" and (ws > 1 or os.environ.get("ALNNLS_FORCE_ROWBLOCK")):
+            return run_ours_rowblock(args, ws, rank, local, dist)
         return run_ours(args, ws, rank, local, dist)
     finally:
         if dist is not None:
