@@ -352,19 +352,26 @@ __device__ void row_apply(const LoopArgs& a, RowShared& S, int blk, int row0, in
     gn[i] = xadd(gc[i], a.gd[i]);
     xn[i] = xc[i];
   }
-  if (threadIdx.x == 0) {  // own range of the ascending changed list
-    int lo = 0, hi = cl;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((int)__ldcg(a.chg + mid) < row0) lo = mid + 1; else hi = mid;
+  // own range [t_lo, t_hi) of the ascending changed list: a two-round
+  // blockDim-ary search (two L2 round trips instead of a 2 log2(cl)-deep chain)
+  {
+    const int nt = blockDim.x;
+    const int step = (cl + nt - 1) / nt;  // round 1 samples chg[0], chg[step], ...
+    const int i = threadIdx.x * step;
+    const int v = i < cl ? (int)__ldcg(a.chg + i) : 0x7fffffff;
+    const int c_lo = __syncthreads_count(v < row0);          // samples below row0
+    const int c_hi = __syncthreads_count(v < row0 + nrows);
+    // the boundary lies in (sample c-1, sample c]: scan that bucket
+    const int b_lo = max(0, c_lo - 1) * step, b_hi = max(0, c_hi - 1) * step;
+    const int j = threadIdx.x;
+    const int w1 = j < step && b_lo + j < cl ? (int)__ldcg(a.chg + b_lo + j) : 0x7fffffff;
+    const int w2 = j < step && b_hi + j < cl ? (int)__ldcg(a.chg + b_hi + j) : 0x7fffffff;
+    const int n_lo = __syncthreads_count(j < step && b_lo + j < cl && w1 < row0);
+    const int n_hi = __syncthreads_count(j < step && b_hi + j < cl && w2 < row0 + nrows);
+    if (threadIdx.x == 0) {
+      S.t_lo = c_lo == 0 ? 0 : b_lo + n_lo;
+      S.t_hi = c_hi == 0 ? 0 : b_hi + n_hi;
     }
-    int lo2 = lo, hi2 = cl;
-    while (lo2 < hi2) {
-      const int mid = (lo2 + hi2) >> 1;
-      if ((int)__ldcg(a.chg + mid) < row0 + nrows) lo2 = mid + 1; else hi2 = mid;
-    }
-    S.t_lo = lo;
-    S.t_hi = lo2;
   }
   __syncthreads();
   for (int t = S.t_lo + threadIdx.x; t < S.t_hi; t += blockDim.x) {
