@@ -390,10 +390,13 @@ __device__ int row_lists(const LoopArgs& a, RowShared& S, int blk, int nblk, int
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (warp == 0) {
     int before = 0, all = 0;
-    for (int b = lane; b < nblk; b += 32) {
-      const int c = __ldcg(a.cnt + b);
-      all += c;
-      if (b < blk) before += c;
+    int cv[6];  // nblk <= 192: all loads in flight together
+#pragma unroll
+    for (int r = 0; r < 6; ++r) cv[r] = lane + 32 * r < nblk ? __ldcg(a.cnt + lane + 32 * r) : 0;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      all += cv[r];
+      if (lane + 32 * r < blk) before += cv[r];
     }
     for (int o = 16; o > 0; o >>= 1) {
       before += __shfl_xor_sync(0xffffffffu, before, o);
@@ -565,10 +568,20 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
       if (threadIdx.x < 32) {  // gather the row CTAs' partials of the current state
         int c = 0, bd = 0;
         double mn = __longlong_as_double(0x7ff0000000000000LL);
-        for (int b = threadIdx.x; b < nblk; b += 32) {
-          c += __ldcg(a.cnt + b);
-          bd |= __ldcg(a.badv + b);
-          mn = fmin(mn, __ldcg(a.minx + b));
+        int cv[6], bv[6];
+        double mv[6];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {  // nblk <= 192: all loads in flight together
+          const int b = threadIdx.x + 32 * r;
+          cv[r] = b < nblk ? __ldcg(a.cnt + b) : 0;
+          bv[r] = b < nblk ? __ldcg(a.badv + b) : 0;
+          mv[r] = b < nblk ? __ldcg(a.minx + b) : __longlong_as_double(0x7ff0000000000000LL);
+        }
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+          c += cv[r];
+          bd |= bv[r];
+          mn = fmin(mn, mv[r]);
         }
         for (int o = 16; o > 0; o >>= 1) {
           c += __shfl_xor_sync(0xffffffffu, c, o);
