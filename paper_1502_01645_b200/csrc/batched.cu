@@ -67,7 +67,7 @@ struct BatchSmem {
 };
 
 __host__ __device__ constexpr int batch_ld(int nb) { return nb + 2; }
-__host__ __device__ constexpr int round8(int m) { return (m + 7) & ~7; }
+__host__ __device__ constexpr int round8(int m) { return (m + 15) & ~15; }  // (16: GEMM blocks of up to 16 rows)
 size_t batch_smem_bytes(int m, int nb) {
   const size_t mp = (size_t)round8(m);
   return (mp * batch_ld(nb) + 5 * mp * nb) * sizeof(double);
@@ -356,190 +356,170 @@ __device__ void refill(const BatchArgs& a, ColState& S, const BatchSmem& sm, int
   }
 }
 
+// One exact chain GEMM pass for a group of CG columns starting at column
+// grp * CG: U[:, col] = Q V[:, col], rows i = trow + r * ROWT (ascending j per
+// output). Off-mask entries of V are 0 and their +-0 products are exact no-ops
+// (idle slots, pad rows j >= m with their zero Q operands too).
+template <int RPT, int CG, int ROWT, int LD, int JB = 8>
+__device__ __forceinline__ void gemm_pass(const BatchArgs& a, const BatchSmem& sm, int grp, int trow) {
+  const int m = sm.m, mp = sm.mp;
+  double acc[RPT * CG];
+#pragma unroll
+  for (int t = 0; t < RPT * CG; ++t) acc[t] = 0.0;
+  // JB: Q columns per block; two blocks in registers (ping-pong)
+  auto load_q = [&](int j0, double (&qv)[RPT][JB]) {
+#pragma unroll
+    for (int u = 0; u < JB; ++u) {
+      const double* qc = a.Q + (size_t)(j0 + u) * m;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = trow + r * ROWT;
+        qv[r][u] = (j0 + u < m && i < m) ? __ldg(qc + i) : 0.0;
+      }
+    }
+  };
+  auto block = [&](int j0, const double (&qv)[RPT][JB]) {
+#pragma unroll
+    for (int u = 0; u < JB; ++u) {
+      const double* vrow = sm.V + (size_t)(j0 + u) * LD + grp * CG;
+      double vb[CG];
+#pragma unroll
+      for (int b = 0; b < CG; b += 2) {
+        const double2 t = *reinterpret_cast<const double2*>(vrow + b);
+        vb[b] = t.x;
+        vb[b + 1] = t.y;
+      }
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+#pragma unroll
+        for (int b = 0; b < CG; ++b) acc[r * CG + b] = xmac(acc[r * CG + b], qv[r][u], vb[b]);
+    }
+  };
+  double qa[RPT][JB], qb[RPT][JB];
+  load_q(0, qa);
+  for (int j0 = 0; j0 < mp; j0 += 2 * JB) {  // mp is a multiple of JB; V rows >= m are zero
+    const bool two = j0 + JB < mp;
+    if (two) load_q(j0 + JB, qb);
+    block(j0, qa);
+    if (j0 + 2 * JB < mp) load_q(j0 + 2 * JB, qa);
+    if (two) block(j0 + JB, qb);
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = trow + r * ROWT;
+    if (i < m) {
+#pragma unroll
+      for (int b = 0; b < CG; ++b) sm.U[(size_t)(grp * CG + b) * mp + i] = acc[r * CG + b];
+    }
+  }
+}
+
+// Column b's state machine after its GEMM pass (nqp.hpp:276-318): P1 result ->
+// den, alpha, candidate step; P2 result -> df, accept (next mask / stop tests)
+// or halve and retry. One warp; V of the column is ready for its next pass.
+__device__ void column_step(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b) {
+  const int lane = threadIdx.x & 31;
+  const int m = sm.m;
+  const int ph = S.phase[b];
+  if (ph == kIdle) return;
+  if (ph == kNeedP1) {
+    const double den = den_chain(sm, b);  // exact_step, nqp.hpp:166-172
+    if (!(den > 0.0)) {
+      finish_col(a, S, sm, b, ALNNLS_ZERO_CURVATURE, 0);
+      refill(a, S, sm, b);
+      return;
+    }
+    if (lane == 0) {
+      S.alpha[b] = xdiv(S.gbs[b], den);
+      S.tries[b] = 0;
+      S.mults[b] += (unsigned long long)m * (unsigned long long)S.ml[b];
+    }
+    __syncwarp();
+  } else {  // kNeedP2: gd = Q delta in U
+    const double df = df_chain(sm, b);
+    const bool accept = df <= 0.0 || S.tries[b] >= 60;
+    if (accept) {  // x[C] = cand, grad += gd (nqp.hpp:309-313)
+      double* xb = sm.x(b);
+      double* gw = sm.g(b);
+      const double* cb = sm.c(b);
+      const double* ub = sm.u(b);
+      for (int i = lane; i < m; i += 32) {
+        xb[i] = cb[i];
+        gw[i] = xadd(gw[i], ub[i]);
+      }
+      if (lane == 0) ++S.k[b];
+      __syncwarp();
+      if (mask_phase(a, S, sm, b)) refill(a, S, sm, b);
+      return;
+    }
+    if (lane == 0) {
+      S.alpha[b] = xmul(S.alpha[b], 0.5);  // nqp.hpp:317
+      ++S.tries[b];
+    }
+    __syncwarp();
+  }
+  // candidate step with the current alpha
+  const int cl = cand_phase(a, S, sm, b);
+  if (cl == 0) {  // nothing moved (nqp.hpp:304): next iteration on the same state
+    if (lane == 0) ++S.k[b];
+    __syncwarp();
+    if (mask_phase(a, S, sm, b)) refill(a, S, sm, b);
+    return;
+  }
+  if (lane == 0) {
+    S.mults[b] += (unsigned long long)m * (unsigned long long)cl;
+    S.phase[b] = kNeedP2;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ BatchSmem carve(double* bsm, int m, int nb) {
+  BatchSmem sm;
+  const int mp = round8(m);
+  sm.ld = batch_ld(nb);
+  sm.m = m;
+  sm.mp = mp;
+  sm.V = bsm;
+  sm.U = bsm + (size_t)mp * sm.ld;
+  sm.C = sm.U + (size_t)mp * nb;
+  sm.X = sm.C + (size_t)mp * nb;
+  sm.G = sm.X + (size_t)mp * nb;
+  sm.q = sm.G + (size_t)mp * nb;
+  const int total = mp * sm.ld + 5 * mp * nb;  // zero once: pads must read as +0
+  for (int e = threadIdx.x; e < total; e += blockDim.x) bsm[e] = 0.0;
+  return sm;
+}
+
+// Every pass, all threads run the GEMM for all NB columns, then one warp per
+// column runs its state machine. (A warp-specialised variant -- 8 warps on the
+// GEMM of one half of the columns while 8 run the other half's state machines --
+// measured slower at c4: 1.71-1.86 s vs 1.65 s; with 2 warps per scheduler the
+// GEMM cannot hide the L2 latency of Q.)
 template <int NB>
 __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
   extern __shared__ __align__(16) double bsm[];
   __shared__ ColState S;
-  const int m = a.m;
-  const int mp = round8(m);
   constexpr int LD = batch_ld(NB);
-  BatchSmem sm;
-  sm.ld = LD;
-  sm.m = m;
-  sm.mp = mp;
-  sm.V = bsm;
-  sm.U = bsm + (size_t)mp * LD;
-  sm.C = sm.U + (size_t)mp * NB;
-  sm.X = sm.C + (size_t)mp * NB;
-  sm.G = sm.X + (size_t)mp * NB;
-  sm.q = sm.G + (size_t)mp * NB;
-  {  // zero everything once: pads (rows >= m, panel tails) must read as +0
-    const int total = mp * LD + 5 * mp * NB;
-    for (int e = threadIdx.x; e < total; e += kBT) bsm[e] = 0.0;
-  }
+  const BatchSmem sm = carve(bsm, a.m, NB);
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   constexpr int nwarps = kBT / 32;
   for (int b = warp; b < NB; b += nwarps) refill(a, S, sm, b);
   __syncthreads();
-  // GEMM thread mapping: GROUPS groups of CG columns; rows i = trow + r * ROWT
   constexpr int CG = NB < 8 ? NB : 8;
   constexpr int GROUPS = NB / CG;
   constexpr int ROWT = kBT / GROUPS;
   constexpr int RPT = (4096 / NB + ROWT - 1) / ROWT;  // rows per thread at the largest m (4096/NB)
   const int grp = threadIdx.x / ROWT, trow = threadIdx.x % ROWT;
-#ifdef ALNNLS_BATCH_PROFILE
-  long long t_gemm = 0, t_cols = 0, npass = 0;
-  long long pt[4] = {0, 0, 0, 0}, pn[4] = {0, 0, 0, 0};
-  long long pc0 = 0;
-#define PROF_T0 pc0 = clock64()
-#define PROF_T1(k) (pt[k] += clock64() - pc0, ++pn[k])
-#else
-#define PROF_T0
-#define PROF_T1(k)
-#endif
   for (;;) {
-#ifdef ALNNLS_BATCH_PROFILE
-    const long long c0 = clock64();
-#endif
-    // any active column?
     int active = 0;
     for (int b = 0; b < NB; ++b) active |= S.phase[b] != kIdle;
     if (!active) break;
-    // ---- one exact chain GEMM pass: U = Q V (ascending j per output). Off-mask
-    // entries of V are 0 and their +-0 products are exact no-ops (idle slots,
-    // pad rows j >= m with their zero Q operands too).
-    double acc[RPT * CG];
-#pragma unroll
-    for (int t = 0; t < RPT * CG; ++t) acc[t] = 0.0;
-    constexpr int JB = 8;  // Q columns per block; two blocks in registers (ping-pong)
-    auto load_q = [&](int j0, double (&qv)[RPT][JB]) {
-#pragma unroll
-      for (int u = 0; u < JB; ++u) {
-        const double* qc = a.Q + (size_t)(j0 + u) * m;
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const int i = trow + r * ROWT;
-          qv[r][u] = (j0 + u < m && i < m) ? __ldg(qc + i) : 0.0;
-        }
-      }
-    };
-    auto block = [&](int j0, const double (&qv)[RPT][JB]) {
-#pragma unroll
-      for (int u = 0; u < JB; ++u) {
-        const double* vrow = sm.V + (size_t)(j0 + u) * LD + grp * CG;
-        double vb[CG];
-#pragma unroll
-        for (int b = 0; b < CG; b += 2) {
-          const double2 t = *reinterpret_cast<const double2*>(vrow + b);
-          vb[b] = t.x;
-          vb[b + 1] = t.y;
-        }
-#pragma unroll
-        for (int r = 0; r < RPT; ++r)
-#pragma unroll
-          for (int b = 0; b < CG; ++b) acc[r * CG + b] = xmac(acc[r * CG + b], qv[r][u], vb[b]);
-      }
-    };
-    double qa[RPT][JB], qb[RPT][JB];
-    load_q(0, qa);
-    for (int j0 = 0; j0 < mp; j0 += 2 * JB) {  // mp is a multiple of JB; V rows >= m are zero
-      const bool two = j0 + JB < mp;
-      if (two) load_q(j0 + JB, qb);
-      block(j0, qa);
-      if (j0 + 2 * JB < mp) load_q(j0 + 2 * JB, qa);
-      if (two) block(j0 + JB, qb);
-    }
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      const int i = trow + r * ROWT;
-      if (i < m) {
-#pragma unroll
-        for (int b = 0; b < CG; ++b) sm.U[(size_t)(grp * CG + b) * mp + i] = acc[r * CG + b];
-      }
-    }
+    gemm_pass<RPT, CG, ROWT, LD>(a, sm, grp, trow);
     __syncthreads();
-#ifdef ALNNLS_BATCH_PROFILE
-    const long long c1 = clock64();
-    t_gemm += c1 - c0;
-    ++npass;
-#endif
-    // ---- per-column state machines ----
-    for (int b = warp; b < NB; b += nwarps) {
-      const int ph = S.phase[b];
-      if (ph == kIdle) continue;
-      if (ph == kNeedP1) {
-        PROF_T0;
-        const double den = den_chain(sm, b);
-        PROF_T1(0);
-        if (!(den > 0.0)) {
-          finish_col(a, S, sm, b, ALNNLS_ZERO_CURVATURE, 0);
-          refill(a, S, sm, b);
-          continue;
-        }
-        if (lane == 0) {
-          S.alpha[b] = xdiv(S.gbs[b], den);
-          S.tries[b] = 0;
-          S.mults[b] += (unsigned long long)m * (unsigned long long)S.ml[b];
-        }
-        __syncwarp();
-      } else {  // kNeedP2: gd = Q delta in U
-        PROF_T0;
-        const double df = df_chain(sm, b);
-        PROF_T1(1);
-        const bool accept = df <= 0.0 || S.tries[b] >= 60;
-        if (accept) {  // x[C] = cand, grad += gd (nqp.hpp:309-313)
-          double* xb = sm.x(b);
-          double* gw = sm.g(b);
-          const double* cb = sm.c(b);
-          const double* ub = sm.u(b);
-          for (int i = lane; i < m; i += 32) {
-            xb[i] = cb[i];
-            gw[i] = xadd(gw[i], ub[i]);
-          }
-          if (lane == 0) ++S.k[b];
-          __syncwarp();
-          PROF_T0;
-          if (mask_phase(a, S, sm, b)) refill(a, S, sm, b);
-          PROF_T1(2);
-          continue;
-        }
-        if (lane == 0) {
-          S.alpha[b] = xmul(S.alpha[b], 0.5);  // nqp.hpp:317
-          ++S.tries[b];
-        }
-        __syncwarp();
-      }
-      // candidate step with the current alpha
-      PROF_T0;
-      const int cl = cand_phase(a, S, sm, b);
-      PROF_T1(3);
-      if (cl == 0) {  // nothing moved (nqp.hpp:304): next iteration on the same state
-        if (lane == 0) ++S.k[b];
-        __syncwarp();
-        if (mask_phase(a, S, sm, b)) refill(a, S, sm, b);
-        continue;
-      }
-      if (lane == 0) {
-        S.mults[b] += (unsigned long long)m * (unsigned long long)cl;
-        S.phase[b] = kNeedP2;
-      }
-      __syncwarp();
-    }
+    for (int b = warp; b < NB; b += nwarps) column_step(a, S, sm, b);
     __syncthreads();
-#ifdef ALNNLS_BATCH_PROFILE
-    t_cols += clock64() - c1;
-#endif
   }
-#ifdef ALNNLS_BATCH_PROFILE
-  if (threadIdx.x == 0 && blockIdx.x < 2)
-    printf("batch prof cta %d: passes %lld gemm %lld cyc/pass, cols %lld cyc/pass\n", blockIdx.x, npass,
-           t_gemm / (npass ? npass : 1), t_cols / (npass ? npass : 1));
-  if (threadIdx.x == 0 && blockIdx.x < 2)
-    printf("  warp0: den %lld (n %lld) df %lld (n %lld) mask %lld (n %lld) cand %lld (n %lld)\n",
-           pt[0] / (pn[0] ? pn[0] : 1), pn[0], pt[1] / (pn[1] ? pn[1] : 1), pn[1],
-           pt[2] / (pn[2] ? pn[2] : 1), pn[2], pt[3] / (pn[3] ? pn[3] : 1), pn[3]);
-#endif
 }
 
 // x[retained[a], j] = Y[a, j] / D_a; dropped columns 0 (nnls.hpp:87-96).
