@@ -10,7 +10,10 @@ import pytest
 from paper_1502_01645_b200 import abi, instances
 from tests.parity import same_bits
 
-GOLD = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+GOLD = sorted(p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))
+              if not os.path.basename(p).startswith("full_"))
+# full-size BASELINE configs (tests/golden/make_golden_full.py): GPU-only checks
+FULL = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "full_*.npz")))
 
 
 def load(path):
@@ -109,3 +112,38 @@ def test_gpu_matches_reference_golden(path, solver):
         assert same_bits(r.x, g["x"]) and same_bits(r.final_grad, g["final_grad"])
         assert np.array_equal(r.multiplies_per_iter, g["mults"])
         check_trace(r.trace, g)
+
+
+def _trace_sha(tr):
+    import hashlib
+    h = hashlib.sha256()
+    for r in tr:
+        al = np.nan if r.alpha is None else r.alpha
+        h.update(np.array([r.iter, r.passive_count], np.uint64).tobytes())
+        h.update(np.array([r.f, r.grad_bar_sq, al], np.float64).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", FULL, ids=[os.path.basename(p)[:-4] for p in FULL])
+def test_gpu_full_size_config_matches_reference(path, solver):
+    """BASELINE.json c2 / c3 at full size, bit for bit against the reference's own
+    run (x, inner x, final gradient, residual, iterations, termination, every
+    trace record through a sha256)."""
+    from paper_1502_01645_b200.api import SolverConfig
+    g = load(path)
+    name = os.path.basename(path)[5:-4]
+    inst = instances.make_config(name)
+    A, b = inst["A"], inst["b"]
+    if instances.sha256(np.asfortranarray(A), b) != str(g["input_sha256"]):
+        pytest.skip("generated inputs differ from the fixture's (host libm / LAPACK)")
+    kw = dict(eval(str(g["cfg"])))
+    r = solver.solve_nnls(A, b, SolverConfig(epsilon=kw["epsilon"], max_iters=kw["max_iters"],
+                                             stall_window=kw["stall_window"]))
+    assert r.inner.iterations() == int(g["iterations"])
+    assert r.inner.termination == str(g["termination"])
+    assert same_bits(r.x, g["x"]) and same_bits(r.inner.x, g["inner_x"])
+    assert same_bits(r.inner.final_grad, g["final_grad"])
+    assert same_bits([r.residual_sq], [g["residual_sq"]])
+    assert len(r.inner.trace) == int(g["trace_len"])
+    assert _trace_sha(r.inner.trace) == str(g["trace_sha256"])

@@ -77,3 +77,25 @@ def test_batched_matches_single_solves(solver):
         assert same_bits(X[:, j], r.x)
         assert cols[j]["iterations"] == r.inner.iterations()
         assert same_bits([cols[j]["residual_sq"]], [r.residual_sq])
+
+
+def test_batched_c4_full_shape_sampled_columns(solver):
+    """c4 at its full shape (A 20000 x 256) over 2048 right-hand sides; every
+    64th column is checked bit for bit against the reference pipeline (SURVEY
+    §8d: "bitwise on every oracle-sampled column")."""
+    from oracle.oracle import Oracle, available
+    if not available("ref"):
+        pytest.skip("oracle/_ref not built")
+    inst = instances.make_batched(nrhs=2048)
+    cfg = SolverConfig(epsilon=inst["epsilon"], stall_window=10**9)
+    X, cols, _ = solver.solve_nnls_batched(inst["A"], inst["B"], cfg)
+    sample = list(range(0, 2048, 64))
+    Bs = np.asfortranarray(inst["B"][:, sample])
+    import os
+    Xr, cr = Oracle("ref").solve_nnls_columns(inst["A"], Bs, cfg.to_abi(record_multiplies=False),
+                                              threads=os.cpu_count() or 1)
+    for k, j in enumerate(sample):
+        assert same_bits(X[:, j], Xr[:, k]), j
+        assert cols[j]["iterations"] == cr[k].iterations
+        assert same_bits([cols[j]["residual_sq"]], [cr[k].residual_sq])
+    assert np.max(np.abs(X - inst["H_true"])) < 1e-3
