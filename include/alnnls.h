@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define ALNNLS_ABI_VERSION 1
+#define ALNNLS_ABI_VERSION 2
 
 typedef enum alnnls_status {
   ALNNLS_OK = 0,
@@ -76,6 +76,7 @@ typedef struct alnnls_config {
   uint64_t trace_every;  /* reference default 1; 0 is treated as 1 (nqp.hpp:222) */
   int32_t profile;       /* alnnls_profile */
   int32_t record_multiplies; /* fill SolveStats::multiplies_per_iter */
+  int32_t nesterov_restart;  /* SolverConfig::nesterov_restart (accelerated solver only) */
 } alnnls_config;
 
 /* antilop::IterRecord (nqp.hpp:103-110). has_alpha = 0 on the final record. */

@@ -122,6 +122,7 @@ inline alnnls_config to_abi(const SolverConfig& c) {
   a.time_cap_s = c.time_cap ? c.time_cap->count() : 0.0;
   a.stall_window = c.stall_window;
   a.trace_every = c.trace_every;
+  a.nesterov_restart = c.nesterov_restart ? 1 : 0;
   return a;
 }
 

@@ -401,9 +401,155 @@ static double residual_norm_sq(uint64_t d, uint64_t n, const double* A, const do
   return s;
 }
 
+typedef int (*inner_solver)(uint64_t m, const double* Q, const double* q, const double* start,
+                            const alnnls_config* cfg, oracle_out* out);
+
+/* linalg.hpp:222-226: one ascending chain over the column-major data */
+double oracle_frobenius_norm(uint64_t rows, uint64_t cols, const double* M) {
+  double s = 0.0;
+  for (uint64_t e = 0; e < rows * cols; ++e) s += M[e] * M[e];
+  return sqrt(s);
+}
+
+/* accelerated.hpp:21-113 (solve_accelerated): Nesterov momentum projected
+ * gradient with the fixed step 1/||Q||_F; start must be NULL (the reference
+ * has no warm start here). */
+int oracle_solve_accelerated(uint64_t n, const double* Q, const double* q, const double* start,
+                             const alnnls_config* cfg, oracle_out* out) {
+  (void)start;
+  double eps;
+  if (cfg->has_epsilon) {
+    if (!(cfg->epsilon > 0.0)) return fail(out, ALNNLS_EINVAL, "SolverConfig: epsilon must be > 0");
+    eps = cfg->epsilon;
+  } else {
+    eps = 1e-10 * (double)n;
+  }
+  uint64_t max_iters;
+  if (cfg->has_max_iters) {
+    if (cfg->max_iters < 1) return fail(out, ALNNLS_EINVAL, "SolverConfig: max_iters must be >= 1");
+    max_iters = cfg->max_iters;
+  } else {
+    max_iters = 5 * n;
+  }
+  const uint64_t trace_every = cfg->trace_every > 0 ? cfg->trace_every : 1;
+  const double m_norm = oracle_frobenius_norm(n, n, Q);
+  const size_t nb = sizeof(double) * (n ? n : 1);
+  double* x = (double*)calloc(1, nb);
+  double* y = (double*)calloc(1, nb);
+  double* xn = (double*)calloc(1, nb);
+  double* grad = (double*)malloc(nb);
+  double* gy = (double*)malloc(nb);
+  double t = 1.0, f_prev = INFINITY, min_iterate = 0.0;
+  double best_gbs = INFINITY;
+  uint64_t since_best = 0, trace_len = 0;
+  int status = ALNNLS_OK, termination = ALNNLS_MAX_ITERS;
+  double last_f = 0.0, last_gbs = 0.0;
+  const double t0 = now_s();
+  for (uint64_t k = 0;; ++k) {
+    oracle_matvec(n, n, Q, x, grad); /* :45-46 */
+    for (uint64_t i = 0; i < n; ++i) grad[i] += q[i];
+    uint64_t ml = 0;
+    double gbs = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+      if (x[i] > 0.0 || grad[i] < 0.0) {
+        ++ml;
+        gbs += grad[i] * grad[i];
+      }
+    }
+    const double f = 0.5 * (dot(n, x, grad) + dot(n, q, x));
+    const double elapsed = now_s() - t0;
+    if (!isfinite(f) || !isfinite(gbs)) {
+      status = fail(out, ALNNLS_ENUMERIC, "solve_accelerated: non-finite objective or gradient");
+      if (out) out->summary.numeric_failure = 1;
+      break;
+    }
+    int stop = -1; /* :60-75 */
+    if (ml == 0) {
+      stop = ALNNLS_EMPTY_PASSIVE_SET;
+    } else if (gbs < eps) {
+      stop = ALNNLS_GRADIENT_BELOW_EPSILON;
+    } else if (k >= max_iters) {
+      stop = ALNNLS_MAX_ITERS;
+    } else if (cfg->has_time_cap && elapsed >= cfg->time_cap_s) {
+      stop = ALNNLS_TIME_CAP;
+    } else if (m_norm == 0.0) {
+      stop = ALNNLS_ZERO_CURVATURE;
+    } else if (gbs < best_gbs) {
+      best_gbs = gbs;
+      since_best = 0;
+    } else if (++since_best >= cfg->stall_window) {
+      stop = ALNNLS_STALLED;
+    }
+    if (stop >= 0) {
+      push_record(out, &trace_len, k, f, gbs, ml, elapsed, 0.0, 0);
+      termination = stop;
+      last_f = f;
+      last_gbs = gbs;
+      if (out) out->summary.iterations = k;
+      break;
+    }
+    const double alpha = 1.0 / m_norm; /* :83-86 */
+    if (k % trace_every == 0) push_record(out, &trace_len, k, f, gbs, ml, elapsed, alpha, 1);
+    oracle_matvec(n, n, Q, y, gy); /* :89-94 */
+    for (uint64_t i = 0; i < n; ++i) gy[i] += q[i];
+    for (uint64_t i = 0; i < n; ++i) {
+      const double v = y[i] - alpha * gy[i];
+      xn[i] = 0.0 < v ? v : 0.0; /* std::max(0.0, v) */
+    }
+    const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t)); /* :96-100 */
+    const double momentum = (t - 1.0) / t_next;
+    for (uint64_t i = 0; i < n; ++i) y[i] = xn[i] + momentum * (xn[i] - x[i]);
+    if (cfg->nesterov_restart && f > f_prev) { /* :102-107 */
+      t = 1.0;
+      memcpy(y, xn, sizeof(double) * n);
+    } else {
+      t = t_next;
+    }
+    f_prev = f;
+    memcpy(x, xn, sizeof(double) * n);
+    double mn = 0.0; /* :110-112 */
+    for (uint64_t i = 0; i < n; ++i) mn = x[i] < mn ? x[i] : mn;
+    min_iterate = mn < min_iterate ? mn : min_iterate;
+  }
+  if (out) {
+    out->summary.termination = termination;
+    out->summary.trace_len = trace_len;
+    out->summary.min_iterate = min_iterate;
+    out->summary.f_final = last_f;
+    out->summary.gbs_final = last_gbs;
+    out->summary.m = n;
+    out->summary.t_loop_s = now_s() - t0;
+    if (status == ALNNLS_OK) {
+      if (out->x) memcpy(out->x, x, sizeof(double) * n);
+      if (out->final_grad) memcpy(out->final_grad, grad, sizeof(double) * n); /* :115-117 */
+    }
+  }
+  free(x);
+  free(y);
+  free(xn);
+  free(grad);
+  free(gy);
+  return status;
+}
+
+static int nnls_pipeline(uint64_t d, uint64_t n, const double* A, const double* b,
+                         const alnnls_config* cfg, oracle_out* out, inner_solver solve);
+
 /* nnls.hpp:129-144 */
 int oracle_solve_nnls(uint64_t d, uint64_t n, const double* A, const double* b,
                       const alnnls_config* cfg, oracle_out* out) {
+  return nnls_pipeline(d, n, A, b, cfg, out, oracle_solve_nqp);
+}
+
+/* accelerated.hpp:121-139 (solve_anti_accelerated): the same rescale / unscale /
+ * residual pipeline around solve_accelerated. */
+int oracle_solve_anti_accelerated(uint64_t d, uint64_t n, const double* A, const double* b,
+                                  const alnnls_config* cfg, oracle_out* out) {
+  return nnls_pipeline(d, n, A, b, cfg, out, oracle_solve_accelerated);
+}
+
+static int nnls_pipeline(uint64_t d, uint64_t n, const double* A, const double* b,
+                         const alnnls_config* cfg, oracle_out* out, inner_solver solve) {
   const double t0 = now_s();
   double* H = (double*)malloc(sizeof(double) * (n * n ? n * n : 1));
   double* h = (double*)malloc(sizeof(double) * (n ? n : 1));
@@ -439,7 +585,7 @@ int oracle_solve_nnls(uint64_t d, uint64_t n, const double* A, const double* b,
     inner.x_cap = m;
     inner.final_grad = out ? out->final_grad : NULL;
     memset(&inner.summary, 0, sizeof(inner.summary));
-    st = oracle_solve_nqp(m, Q, q, NULL, cfg, &inner);
+    st = solve(m, Q, q, NULL, cfg, &inner);
     if (out) {
       out->summary = inner.summary;
       memcpy(out->error, inner.error, sizeof(out->error));

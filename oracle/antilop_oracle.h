@@ -62,6 +62,13 @@ int oracle_solve_nqp(uint64_t m, const double* Q, const double* q, const double*
 /* nnls.hpp:129-144 */
 int oracle_solve_nnls(uint64_t d, uint64_t n, const double* A, const double* b,
                       const alnnls_config* cfg, oracle_out* out);
+/* accelerated.hpp:21-117 and :121-139 (the Anti+Acc baseline) */
+int oracle_solve_accelerated(uint64_t m, const double* Q, const double* q, const double* start,
+                             const alnnls_config* cfg, oracle_out* out);
+int oracle_solve_anti_accelerated(uint64_t d, uint64_t n, const double* A, const double* b,
+                                  const alnnls_config* cfg, oracle_out* out);
+/* linalg.hpp:222-226 */
+double oracle_frobenius_norm(uint64_t rows, uint64_t cols, const double* M);
 /* nqp.hpp:183-186 and :190-207 */
 double oracle_objective(uint64_t m, const double* Q, const double* q, const double* x);
 double oracle_kkt_error(uint64_t m, const double* Q, const double* q, const double* x);
@@ -78,6 +85,11 @@ int ref_rescale(uint64_t n, const double* H, const double* h, double* Q, double*
                 oracle_out* out);
 int ref_solve_nqp(uint64_t m, const double* Q, const double* q, const double* start,
                   const alnnls_config* cfg, oracle_out* out);
+int ref_solve_accelerated(uint64_t m, const double* Q, const double* q, const double* start,
+                          const alnnls_config* cfg, oracle_out* out);
+int ref_solve_anti_accelerated(uint64_t d, uint64_t n, const double* A, const double* b,
+                               const alnnls_config* cfg, oracle_out* out);
+double ref_frobenius_norm(uint64_t rows, uint64_t cols, const double* M);
 int ref_solve_nnls(uint64_t d, uint64_t n, const double* A, const double* b,
                    const alnnls_config* cfg, oracle_out* out);
 double ref_objective(uint64_t m, const double* Q, const double* q, const double* x);

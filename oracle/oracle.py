@@ -83,6 +83,10 @@ class Oracle:
                           C.POINTER(OracleOut)],
             "solve_nnls": [C.c_uint64, C.c_uint64, _dp, _dp, C.POINTER(abi.Config),
                            C.POINTER(OracleOut)],
+            "solve_accelerated": [C.c_uint64, _dp, _dp, C.c_void_p, C.POINTER(abi.Config),
+                                  C.POINTER(OracleOut)],
+            "solve_anti_accelerated": [C.c_uint64, C.c_uint64, _dp, _dp, C.POINTER(abi.Config),
+                                       C.POINTER(OracleOut)],
         }.items():
             f = getattr(L, p + name)
             f.argtypes = args
@@ -91,6 +95,9 @@ class Oracle:
             f = getattr(L, p + name)
             f.argtypes = [C.c_uint64, _dp, _dp, _dp]
             f.restype = C.c_double
+        f = getattr(L, p + "frobenius_norm")
+        f.argtypes = [C.c_uint64, C.c_uint64, _dp]
+        f.restype = C.c_double
         if kind == "ref":
             f = L.ref_solve_nnls_columns
             f.argtypes = [C.c_uint64, C.c_uint64, _dp, C.c_uint64, _dp, C.POINTER(abi.Config),
@@ -225,11 +232,32 @@ class Oracle:
             raise OracleError(st, out.error.decode(), res)
         return self._result(out, keep, False)
 
-    def solve_nnls(self, A, b, cfg):
+    def frobenius_norm(self, M):
+        M = np.asfortranarray(M, dtype=np.float64)
+        return self._fn("frobenius_norm")(M.shape[0], M.shape[1], M.reshape(-1, order="F"))
+
+    def solve_accelerated(self, Q, q, cfg):
+        """accelerated.hpp:21-117 (Nesterov baseline on an NQP)."""
+        Q = np.asfortranarray(Q, dtype=np.float64)
+        m = Q.shape[0]
+        out, keep = self._alloc(cfg, m, m)
+        st = self._fn("solve_accelerated")(m, Q.reshape(-1, order="F"),
+                                           np.ascontiguousarray(q, np.float64), None,
+                                           C.byref(cfg), C.byref(out))
+        if st != abi.OK:
+            res = self._result(out, keep, False) if st == abi.ENUMERIC else None
+            raise OracleError(st, out.error.decode(), res)
+        return self._result(out, keep, False)
+
+    def solve_anti_accelerated(self, A, b, cfg):
+        """accelerated.hpp:121-139 (Anti+Acc: rescale, then the Nesterov baseline)."""
+        return self.solve_nnls(A, b, cfg, fn="solve_anti_accelerated")
+
+    def solve_nnls(self, A, b, cfg, fn="solve_nnls"):
         A = np.asfortranarray(A, dtype=np.float64)
         d, n = A.shape
         out, keep = self._alloc(cfg, n, n)
-        st = self._fn("solve_nnls")(d, n, A.reshape(-1, order="F"),
+        st = self._fn(fn)(d, n, A.reshape(-1, order="F"),
                                     np.ascontiguousarray(b, np.float64), C.byref(cfg), C.byref(out))
         if st != abi.OK:
             res = self._result(out, keep, True) if st == abi.ENUMERIC else None

@@ -13,6 +13,7 @@
 #include <thread>
 #include <vector>
 
+#include "antilop/accelerated.hpp"
 #include "antilop/nnls.hpp"
 
 #include "antilop_oracle.h"
@@ -36,6 +37,7 @@ R::SolverConfig to_cfg(const alnnls_config* c) {
   if (c->has_time_cap) s.time_cap = std::chrono::duration<double>(c->time_cap_s);
   s.stall_window = static_cast<std::size_t>(c->stall_window);
   s.trace_every = static_cast<std::size_t>(c->trace_every);
+  s.nesterov_restart = c->nesterov_restart != 0;
   return s;
 }
 
@@ -204,6 +206,50 @@ int ref_solve_nnls(uint64_t d, uint64_t n, const double* A, const double* b,
     }
     return 0;
   });
+}
+
+int ref_solve_accelerated(uint64_t m, const double* Q, const double* q, const double* start,
+                          const alnnls_config* cfg, oracle_out* out) {
+  (void)start;
+  return guarded(out, [&] {
+    R::NqpProblem p(make_matrix(m, m, Q), make_vector(m, q));
+    const auto res = R::solve_accelerated(p, to_cfg(cfg));
+    if (out) {
+      R::SolveStats none;
+      fill_result(res, none, out);
+      out->summary.m = m;
+      out->summary.n = m;
+      if (out->x) std::memcpy(out->x, res.x.data().data(), sizeof(double) * m);
+    }
+    return 0;
+  });
+}
+
+int ref_solve_anti_accelerated(uint64_t d, uint64_t n, const double* A, const double* b,
+                               const alnnls_config* cfg, oracle_out* out) {
+  return guarded(out, [&] {
+    const auto a = make_matrix(d, n, A);
+    const auto bv = make_vector(d, b);
+    const auto res = R::solve_anti_accelerated(a, bv, to_cfg(cfg));
+    if (out) {
+      R::SolveStats none;
+      fill_result(res.inner, none, out);
+      out->summary.n = n;
+      out->summary.n_dropped = res.dropped_columns.size();
+      out->summary.m = n - res.dropped_columns.size();
+      out->summary.residual_sq = res.residual_sq;
+      if (out->x) std::memcpy(out->x, res.x.data().data(), sizeof(double) * n);
+      if (out->inner_x)
+        std::copy(res.inner.x.begin(), res.inner.x.end(), out->inner_x);
+      if (out->dropped)
+        std::copy(res.dropped_columns.begin(), res.dropped_columns.end(), out->dropped);
+    }
+    return 0;
+  });
+}
+
+double ref_frobenius_norm(uint64_t rows, uint64_t cols, const double* M) {
+  return R::frobenius_norm(make_matrix(rows, cols, M));
 }
 
 double ref_objective(uint64_t m, const double* Q, const double* q, const double* x) {

@@ -28,6 +28,7 @@ class Config(C.Structure):
         ("trace_every", C.c_uint64),
         ("profile", C.c_int32),
         ("record_multiplies", C.c_int32),
+        ("nesterov_restart", C.c_int32),
     ]
 
 
@@ -78,7 +79,7 @@ class ColumnResult(C.Structure):
 
 
 def make_config(epsilon=None, max_iters=None, time_cap=None, stall_window=50, trace_every=1,
-                profile=PROFILE_EXACT, record_multiplies=True):
+                profile=PROFILE_EXACT, record_multiplies=True, nesterov_restart=False):
     """SolverConfig (nqp.hpp:71-99) as the POD the ABI takes; None = unset optional."""
     c = Config()
     c.has_epsilon = 0 if epsilon is None else 1
@@ -91,6 +92,7 @@ def make_config(epsilon=None, max_iters=None, time_cap=None, stall_window=50, tr
     c.trace_every = int(trace_every)
     c.profile = int(profile)
     c.record_multiplies = 1 if record_multiplies else 0
+    c.nesterov_restart = 1 if nesterov_restart else 0
     return c
 
 

@@ -46,7 +46,8 @@ class SolverConfig:
 
     def to_abi(self, record_multiplies=True):
         return abi.make_config(self.epsilon, self.max_iters, self.time_cap, self.stall_window,
-                               self.trace_every, self.profile, record_multiplies)
+                               self.trace_every, self.profile, record_multiplies,
+                               self.nesterov_restart)
 
     def resolve_epsilon(self, n):
         if self.epsilon is not None:

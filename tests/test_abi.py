@@ -64,7 +64,7 @@ def test_config_defaults_match_reference():
     # SolverConfig{} (nqp.hpp:71-99): unset epsilon/max_iters/time_cap, stall 50, trace 1
     assert (c.has_epsilon, c.has_max_iters, c.has_time_cap) == (0, 0, 0)
     assert (c.stall_window, c.trace_every, c.profile) == (50, 1, abi.PROFILE_EXACT)
-    assert lib.alnnls_abi_version() == 1
+    assert lib.alnnls_abi_version() == 2
 
 
 def test_no_cpu_fallback():

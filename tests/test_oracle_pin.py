@@ -140,3 +140,30 @@ def test_invalid_inputs(oracle, ref):
         with pytest.raises(OracleError) as ei:
             o.masked_matvec(np.eye(2), np.ones(2), [2])
         assert ei.value.status == abi.ERANGE
+
+
+# ---- Anti+Acc baseline (accelerated.hpp) --------------------
+
+@pytest.mark.parametrize("name,d,n,restart,kw", [
+    ("c1", 200, 80, False, dict(epsilon=1e-8, max_iters=3000, stall_window=10**9)),
+    ("c1", 200, 80, True, dict(epsilon=1e-8, max_iters=3000, stall_window=10**9)),
+    ("c2", 300, 150, False, dict(epsilon=1e-8, stall_window=10**9)),
+    ("c5", 240, 120, True, dict()),  # defaults: eps 1e-10 m, 5m iterations, stall 50
+    ("c3", 160, 160, False, dict(epsilon=1e-10, max_iters=400, trace_every=7)),
+])
+def test_anti_accelerated_matches_reference(name, d, n, restart, kw):
+    from oracle.oracle import Oracle, available
+    if not available("ref"):
+        pytest.skip("oracle/_ref not built")
+    inst = instances.make_config(name, d=d, n=n)
+    cfg = abi.make_config(nesterov_restart=restart, **kw)
+    e = Oracle("oracle").solve_anti_accelerated(inst["A"], inst["b"], cfg)
+    r = Oracle("ref").solve_anti_accelerated(inst["A"], inst["b"], cfg)
+    assert e["iterations"] == r["iterations"] and e["termination"] == r["termination"]
+    assert np.array_equal(e["x"].view(np.uint64), r["x"].view(np.uint64))
+    assert np.array_equal(e["final_grad"].view(np.uint64), r["final_grad"].view(np.uint64))
+    assert e["residual_sq"] == r["residual_sq"]
+    assert len(e["trace"]) == len(r["trace"])
+    for a, b in zip(e["trace"], r["trace"]):
+        assert a["iter"] == b["iter"] and a["passive_count"] == b["passive_count"]
+        assert a["f"] == b["f"] and a["grad_bar_sq"] == b["grad_bar_sq"] and a["alpha"] == b["alpha"]
