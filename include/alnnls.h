@@ -213,6 +213,23 @@ int alnnls_solve_nnls_batched_device(alnnls_ctx* ctx, uint64_t d, uint64_t n,
                                      const alnnls_config* cfg, double* dX,
                                      alnnls_column_result* cols, alnnls_summary* out);
 
+/* ---- Anti+Acc baseline: accelerated.hpp ---------------------
+ * solve_accelerated (accelerated.hpp:21-117): Nesterov projected gradient with
+ * the fixed step 1/||Q||_F (||Q||_F one ascending chain, linalg.hpp:222-226);
+ * config.nesterov_restart enables the restart. solve_anti_accelerated
+ * (:121-139): rescale, solve_accelerated, unscale, residual. Bitwise the
+ * reference under EXACT; results through the same alnnls_get_* accessors. */
+int alnnls_solve_accelerated(alnnls_ctx* ctx, uint64_t m, const double* Q, const double* q,
+                             const alnnls_config* cfg, alnnls_summary* out);
+int alnnls_solve_accelerated_device(alnnls_ctx* ctx, uint64_t m, const double* dQ, uint64_t ldq,
+                                    const double* dq, const alnnls_config* cfg,
+                                    alnnls_summary* out);
+int alnnls_solve_anti_accelerated(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A,
+                                  const double* b, const alnnls_config* cfg, alnnls_summary* out);
+int alnnls_solve_anti_accelerated_device(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA,
+                                         uint64_t lda, const double* db, const alnnls_config* cfg,
+                                         alnnls_summary* out);
+
 /* ---- multi-GPU exact setup by row blocks -----------
  * A is split into row blocks A_0, A_1, ... (ranks). Every sum of the
  * reference setup is one ascending chain over the rows (gram linalg.hpp:168,

@@ -23,6 +23,8 @@ EXPORTS = [
     "alnnls_timer_start", "alnnls_timer_stop", "alnnls_launch_count",
     "alnnls_gram_tiles", "alnnls_gram_rowblock_device", "alnnls_atb_rowblock_device",
     "alnnls_solve_nnls_gram_device", "alnnls_residual_rowblock_device",
+    "alnnls_solve_accelerated", "alnnls_solve_accelerated_device", "alnnls_solve_anti_accelerated",
+    "alnnls_solve_anti_accelerated_device",
 ]
 
 _lib = None
@@ -81,6 +83,14 @@ def load():
         "alnnls_solve_nnls_batched_device": ([vp, u64, u64, vp, u64, vp, C.POINTER(abi.Config),
                                               vp, vp, C.POINTER(abi.Summary)], i32),
         "alnnls_gram_tiles": ([u64], u64),
+        "alnnls_solve_accelerated": ([vp, u64, vp, vp, C.POINTER(abi.Config),
+                                      C.POINTER(abi.Summary)], i32),
+        "alnnls_solve_accelerated_device": ([vp, u64, vp, u64, vp, C.POINTER(abi.Config),
+                                             C.POINTER(abi.Summary)], i32),
+        "alnnls_solve_anti_accelerated": ([vp, u64, u64, vp, vp, C.POINTER(abi.Config),
+                                           C.POINTER(abi.Summary)], i32),
+        "alnnls_solve_anti_accelerated_device": ([vp, u64, u64, vp, u64, vp, C.POINTER(abi.Config),
+                                                  C.POINTER(abi.Summary)], i32),
         "alnnls_gram_rowblock_device": ([vp, u64, u64, vp, u64, u64, u64, vp, vp, vp], i32),
         "alnnls_atb_rowblock_device": ([vp, u64, u64, vp, u64, vp, vp, vp], i32),
         "alnnls_solve_nnls_gram_device": ([vp, u64, vp, vp, C.POINTER(abi.Config),

@@ -348,6 +348,49 @@ class Solver:
             self._raise(st)
         return self._solve_result(False)
 
+    # ---- Anti+Acc baseline (accelerated.hpp) -------------------------------
+    def solve_anti_accelerated(self, A, b, config: SolverConfig = SolverConfig()):
+        """solve_anti_accelerated (accelerated.hpp:121-139): rescale, Nesterov, unscale."""
+        A = _fortran(A)
+        b = np.ascontiguousarray(_f64(b, "b")).reshape(-1)
+        if A.shape[0] != b.shape[0]:
+            raise ValueError("solve_anti_accelerated: A and b dimension mismatch")
+        d, n = A.shape
+        self._summary = abi.Summary()
+        cfg = config.to_abi(record_multiplies=False)
+        st = self.lib.alnnls_solve_anti_accelerated(self.ctx, d, n, _ptr(A), _ptr(b), C.byref(cfg),
+                                                    C.byref(self._summary))
+        if st != abi.OK:
+            self._raise(st)
+        return self._nnls_result()
+
+    def solve_anti_accelerated_device(self, A_ptr, lda, d, n, b_ptr,
+                                      config: SolverConfig = SolverConfig(), fetch=True):
+        self._summary = abi.Summary()
+        cfg = config.to_abi(record_multiplies=False)
+        st = self.lib.alnnls_solve_anti_accelerated_device(self.ctx, d, n, C.c_void_p(A_ptr), lda,
+                                                           C.c_void_p(b_ptr), C.byref(cfg),
+                                                           C.byref(self._summary))
+        if st != abi.OK:
+            self._raise(st)
+        return self._nnls_result() if fetch else self._summary
+
+    def solve_accelerated(self, Q, q, config: SolverConfig = SolverConfig()):
+        """solve_accelerated (accelerated.hpp:21-117) on an NQP."""
+        Q = _fortran(Q)
+        q = np.ascontiguousarray(_f64(q, "q")).reshape(-1)
+        if Q.shape[0] != Q.shape[1]:
+            raise ValueError("NqpProblem: Q must be square")
+        if Q.shape[0] != q.shape[0]:
+            raise ValueError("NqpProblem: Q and q dimension mismatch")
+        self._summary = abi.Summary()
+        cfg = config.to_abi(record_multiplies=False)
+        st = self.lib.alnnls_solve_accelerated(self.ctx, q.shape[0], _ptr(Q), _ptr(q), C.byref(cfg),
+                                               C.byref(self._summary))
+        if st != abi.OK:
+            self._raise(st)
+        return self._solve_result(False)
+
     # ---- setup and dense kernels ---------------------------------------------------------
     def setup(self, A, b):
         """rescale(gram(A), -A^T b) on device -> dict(Q, q, scale, retained, dropped)."""

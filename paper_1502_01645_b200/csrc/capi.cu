@@ -38,7 +38,8 @@ struct alnnls_ctx {
 
   DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
   DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
-      hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb, uP, gdC, skp, skf;
+      hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb, uP, gdC, skp, skf,
+      ay, axn, aw, avy, apc;
 
   // last solve
   bool last_nnls = false;
@@ -48,6 +49,7 @@ struct alnnls_ctx {
   std::vector<uint64_t> dropped_h;
   bool have_setup = false;
   int g_parity = 0;
+  int solver = 0;  // 0: solve_nqp loop; 1: accelerated baseline (set by the *_accelerated entries)
   unsigned long long phase_ns[8] = {};
   uint64_t launches = 0;
   cudaEvent_t timer[2] = {};
@@ -144,8 +146,9 @@ int check_ctx(alnnls_ctx* ctx) {
 
 // ---- the device-resident NQP solve on ctx->Q / ctx->q (already uploaded) ------
 // x0: nullptr -> start at 0 (g = q); otherwise device start vector (validated).
+// solver 0: solve_nqp (nqp.hpp:215-339); 1: solve_accelerated (accelerated.hpp:21-117).
 int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config* cfg,
-            const double* dstart, alnnls_summary* out) {
+            const double* dstart, alnnls_summary* out, int solver = 0) {
   int st__ = ALNNLS_OK;
   const double* Q = static_cast<const double*>(ctx->Q.p);
   const double* q = static_cast<const double*>(ctx->q.p);
@@ -250,8 +253,28 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   if (a.rows_per_cta > 352)
     return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: dimension too large for one GPU row split");
   const int nctas = 1 + (int)((m + a.rows_per_cta - 1) / a.rows_per_cta);
+  if (solver == 1) {
+    if (m > 46340) return set_err(ctx, ALNNLS_EINVAL, "solve_accelerated: m too large");
+    a.y = ENSURE(double, ay, mp);
+    a.xn = ENSURE(double, axn, mp);
+    a.w = ENSURE(double, aw, mp);
+    a.vy = ENSURE(double, avy, mp);
+    a.pcnt = ENSURE(int, apc, 160);
+    a.restart = cfg->nesterov_restart != 0;
+    CK(cudaMemsetAsync(a.y, 0, sizeof(double) * m, s));
+    double* nrm = ENSURE(double, resid, 2);
+    CK(launch_frobenius(Q, (int)m, (int)ctx->qR, nrm, s));  // M = ||Q||_F (accelerated.hpp:27)
+    double hn = 0.0;
+    CK(cudaMemcpyAsync(&hn, nrm, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    a.alpha = 1.0 / hn;  // :83 (host IEEE division, same rounding)
+  }
   CK(cudaEventRecord(ctx->ev[2], s));
-  CK(launch_nqp_loop(a, nctas, s));
+  if (solver == 1) {
+    CK(launch_acc_loop(a, nctas, s));
+  } else {
+    CK(launch_nqp_loop(a, nctas, s));
+  }
   CK(cudaEventRecord(ctx->ev[3], s));
   LoopCtrl hc;
   CK(cudaMemcpyAsync(&hc, ctrl, sizeof(LoopCtrl), cudaMemcpyDeviceToHost, s));
@@ -338,7 +361,7 @@ int run_setup(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_
 
 // nnls.hpp:129-144 on device-resident A (lda, 16B-aligned, lda even) and b.
 int run_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t lda,
-             const double* db, const alnnls_config* cfg, alnnls_summary* out) {
+             const double* db, const alnnls_config* cfg, alnnls_summary* out, int solver = 0) {
   int st__ = ALNNLS_OK;
   cudaStream_t s = ctx->stream;
   alnnls_summary sum{};
@@ -355,7 +378,7 @@ int run_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t
     Resolved r;
     rc = resolve(ctx, cfg, m, &r);  // solve_nqp validates its config (nqp.hpp:220-221)
     if (rc) return rc;
-    rc = run_nqp(ctx, m, r, cfg, nullptr, &sum);
+    rc = run_nqp(ctx, m, r, cfg, nullptr, &sum, solver | ctx->solver);
     if (rc) {
       if (out) *out = sum;
       ctx->last = sum;
@@ -511,7 +534,8 @@ void alnnls_destroy(alnnls_ctx* ctx) {
                     &ctx->resid,  &ctx->flag,  &ctx->H,       &ctx->hvec,  &ctx->start, &ctx->bcols,
                     &ctx->X,      &ctx->x_alt, &ctx->mask2,   &ctx->gP2,   &ctx->xP2,  &ctx->qP2,
                     &ctx->part,   &ctx->resb,  &ctx->yb,      &ctx->qb,   &ctx->uP,   &ctx->gdC,
-                    &ctx->skp,    &ctx->skf};
+                    &ctx->skp,    &ctx->skf,   &ctx->ay,      &ctx->axn,   &ctx->aw,
+                    &ctx->avy,    &ctx->apc};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
@@ -594,7 +618,7 @@ int alnnls_solve_nqp_device(alnnls_ctx* ctx, uint64_t m, const double* dQ, uint6
   ctx->last_n = m;
   ctx->last_m = m;
   alnnls_summary sum{};
-  rc = run_nqp(ctx, m, r, cfg, dstart, &sum);
+  rc = run_nqp(ctx, m, r, cfg, dstart, &sum, ctx->solver);
   sum.n = m;
   ctx->last = sum;
   if (out) *out = sum;
@@ -640,7 +664,7 @@ int alnnls_solve_nqp(alnnls_ctx* ctx, uint64_t m, const double* Q, const double*
   ctx->last_n = m;
   ctx->last_m = m;
   alnnls_summary sum{};
-  rc = run_nqp(ctx, m, r, cfg, ds, &sum);
+  rc = run_nqp(ctx, m, r, cfg, ds, &sum, ctx->solver);
   sum.n = m;
   sum.t_total_s = sum.t_loop_s;
   ctx->last = sum;
@@ -1210,6 +1234,41 @@ int alnnls_residual_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, 
   CK(launch_masked_gemv(A, ld, (int)rows, list, vals, hlen, ax, ctx->sm_count, s));
   CK(launch_residual(ax, db, (int)rows, pr, res, s, s_in));
   return copy_out(ctx, s_out, res, sizeof(double));
+}
+
+// ---- Anti+Acc baseline (accelerated.hpp) -------------------------------------------------
+namespace {
+struct SolverScope {  // routes the wrapped entry to the accelerated loop
+  alnnls_ctx* c;
+  SolverScope(alnnls_ctx* ctx) : c(ctx) { if (c) c->solver = 1; }
+  ~SolverScope() { if (c) c->solver = 0; }
+};
+}  // namespace
+
+int alnnls_solve_accelerated(alnnls_ctx* ctx, uint64_t m, const double* Q, const double* q,
+                             const alnnls_config* cfg, alnnls_summary* out) {
+  SolverScope sc(ctx);
+  return alnnls_solve_nqp(ctx, m, Q, q, nullptr, cfg, out);
+}
+
+int alnnls_solve_accelerated_device(alnnls_ctx* ctx, uint64_t m, const double* dQ, uint64_t ldq,
+                                    const double* dq, const alnnls_config* cfg,
+                                    alnnls_summary* out) {
+  SolverScope sc(ctx);
+  return alnnls_solve_nqp_device(ctx, m, dQ, ldq, dq, nullptr, cfg, out);
+}
+
+int alnnls_solve_anti_accelerated(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A,
+                                  const double* b, const alnnls_config* cfg, alnnls_summary* out) {
+  SolverScope sc(ctx);
+  return alnnls_solve_nnls(ctx, d, n, A, b, cfg, out);
+}
+
+int alnnls_solve_anti_accelerated_device(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA,
+                                         uint64_t lda, const double* db, const alnnls_config* cfg,
+                                         alnnls_summary* out) {
+  SolverScope sc(ctx);
+  return alnnls_solve_nnls_device(ctx, d, n, dA, lda, db, cfg, out);
 }
 
 }  // extern "C"

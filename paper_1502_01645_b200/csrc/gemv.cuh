@@ -33,7 +33,7 @@ struct RowRing {
   uint64_t* full;
   uint64_t* empty;
   double* data;   // [S][G][seg]
-  double* vals;   // [S][G]
+  double* vals;   // [S][2][G] (the second half: a second right-hand side)
   int S;
   int G;          // columns per stage
   int seg;        // doubles per column slot
@@ -44,7 +44,7 @@ struct RowRing {
 
 __host__ __device__ inline int ring_seg(int nrows) { return (nrows + 1) & ~1; }
 __host__ __device__ inline size_t ring_stage_bytes(int seg, int G) {
-  return (size_t)G * seg * 8 + (size_t)G * 8;
+  return (size_t)G * seg * 8 + (size_t)2 * G * 8;
 }
 
 // Carves the ring out of `smem` (16B aligned, `bytes` long). seg = doubles per
@@ -90,7 +90,9 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
                                  const uint32_t* __restrict__ list,
                                  const double* __restrict__ vals, int len,
                                  double* __restrict__ out, const int* opos = nullptr,
-                                 double* __restrict__ out_c = nullptr) {
+                                 double* __restrict__ out_c = nullptr,
+                                 const double* __restrict__ vals2 = nullptr,
+                                 double* __restrict__ out2 = nullptr) {
   const int G = r.G;
   const int nst = (len + G - 1) / G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -107,7 +109,8 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
       const int cnt = min(G, len - sbase);
       if (lane == 0) {
         mbar_wait(&r.empty[st], ph ^ 1u);
-        const uint32_t bytes = (uint32_t)(cnt * seg * 8 + ((cnt + 1) & ~1) * 8);
+        const uint32_t bytes =
+            (uint32_t)(cnt * seg * 8 + (vals2 ? 2 : 1) * ((cnt + 1) & ~1) * 8);
         mbar_arrive_expect_tx(&r.full[st], bytes);
       }
       __syncwarp();
@@ -135,13 +138,16 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
         }
       }
       if (lane == 0)
-        bulk_g2s(r.vals + (size_t)st * G, vals + sbase, (uint32_t)(((cnt + 1) & ~1) * 8),
+        bulk_g2s(r.vals + (size_t)st * 2 * G, vals + sbase, (uint32_t)(((cnt + 1) & ~1) * 8),
                  &r.full[st]);
+      if (lane == 1 && vals2)
+        bulk_g2s(r.vals + (size_t)st * 2 * G + G, vals2 + sbase,
+                 (uint32_t)(((cnt + 1) & ~1) * 8), &r.full[st]);
     }
   } else if (warp < r.P + r.cons_warps) {
     const int t = (warp - r.P) * 32 + lane;
     const int tt = t < nrows ? t : 0;
-    double acc = 0.0;
+    double acc = 0.0, acc2 = 0.0;
     for (int s = 0; s < nst; ++s) {
       const uint32_t p = r.pos + s;
       const int st = (int)(p % r.S);
@@ -149,7 +155,27 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
       const int cnt = min(G, len - s * G);
       mbar_wait(&r.full[st], ph);
       const double* col = r.data + (size_t)st * G * seg;
-      const double* v = r.vals + (size_t)st * G;
+      const double* v = r.vals + (size_t)st * 2 * G;
+      if (vals2) {  // two right-hand sides: two independent chains per row
+        const double* v2 = v + G;
+        for (int l0 = 0; l0 < cnt; l0 += 16) {
+          double p1[16], p2[16];
+#pragma unroll
+          for (int l = 0; l < 16; ++l) {
+            const double c = l0 + l < cnt ? col[(l0 + l) * seg + tt] : 0.0;
+            p1[l] = xmul(c, v[l0 + l < cnt ? l0 + l : 0]);
+            p2[l] = xmul(c, v2[l0 + l < cnt ? l0 + l : 0]);
+          }
+#pragma unroll
+          for (int l = 0; l < 16; ++l) {  // past cnt: 0 * v = +-0, an exact no-op
+            acc = xadd(acc, p1[l]);
+            acc2 = xadd(acc2, p2[l]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&r.empty[st]);
+        continue;
+      }
       // All rounded products of a full stage are formed first (independent
       // LDS + DMUL, in registers), then one dependent DADD chain runs over
       // them: ptxas cannot interleave the chain ahead of the loads, so the
@@ -176,6 +202,7 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
     if (t < nrows) {
       out[row0 + t] = acc;
       if (opos && opos[t] >= 0) out_c[opos[t]] = acc;
+      if (out2) out2[row0 + t] = acc2;
     }
   }
   r.pos += nst;

@@ -73,11 +73,24 @@ struct LoopArgs {
   LoopCtrl* ctrl;
   unsigned int* bar;  // grid barrier words {count, generation}, zeroed before launch
   int rows_per_cta;
+  // accelerated (Nesterov) solver only (accelerated.hpp:21-117)
+  double* y;        // extrapolated point (m)
+  double* xn;       // projected step from y (m)
+  double* w;        // Q y (m)
+  double* vy;       // y on the union list (mask holds the list, gP the x values)
+  int* pcnt;        // per row-CTA passive counts of (x, grad)
+  double alpha;     // 1 / ||Q||_F
+  int restart;      // SolverConfig::nesterov_restart
 };
 
 // Exact device-resident solve_nqp loop (nqp.hpp:249-334). One cooperative
 // launch for the whole solve; returns the launch status.
 cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream);
+// Accelerated (Nesterov) baseline loop (accelerated.hpp:21-117), same CTA layout.
+cudaError_t launch_acc_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream);
+// frobenius_norm of the blocked m x m Q (linalg.hpp:222-226): one ascending chain
+// over the column-major entries, then sqrt, into *out (one CTA).
+cudaError_t launch_frobenius(const double* Qb, int m, int R, double* out, cudaStream_t stream);
 int nqp_rows_per_cta(int m, int sm_count);
 size_t nqp_loop_smem_bytes();
 

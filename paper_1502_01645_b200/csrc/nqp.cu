@@ -766,6 +766,236 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
   }
 }
 
+// ==== Accelerated (Nesterov) baseline: accelerated.hpp:21-117 =========================
+// Per iteration k (reference order): grad = Q x + q; the stop tests on (x, grad);
+// grad_y = Q y + q; x' = max(0, y - alpha grad_y) with alpha = 1/||Q||_F;
+// t' = (1 + sqrt(1 + 4t^2))/2; y' = x' + ((t-1)/t') (x' - x) (or x' after a
+// restart); x = x'. Both products run in ONE pass over Q: the union of the
+// supports of x and y is streamed once and every row carries two chains (a zero
+// x_j or y_j adds +-0, an exact no-op, so each chain equals the reference's
+// matvec over all columns). Vector CTA: the gbs / x.g / q.x chains (over all m
+// positions, skipped terms added as -0), stop tests and trace. Row CTAs: the
+// pass, the elementwise updates and the next union list.
+
+// Row phase after the pass: grad = u + q and grad_y = w + q (linalg.hpp:185 then
+// accelerated.hpp:46, :90), x' = max(0, y - alpha grad_y); passive counts.
+__device__ void acc_rows_after_pass(const LoopArgs& a, RowShared& S, int blk, int row0, int nrows) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int c = 0, bad = 0;
+  for (int t = threadIdx.x; t < nrows; t += blockDim.x) {
+    const int i = row0 + t;
+    const double gi = xadd(a.u[i], a.q[i]);
+    const double gyi = xadd(a.w[i], a.q[i]);
+    a.g[i] = gi;
+    const double v = xsub(a.y[i], xmul(a.alpha, gyi));
+    a.xn[i] = 0.0 < v ? v : 0.0;  // std::max(0.0, v)
+    c += (a.x[i] > 0.0 || gi < 0.0) ? 1 : 0;
+    if (!isfinite(gi)) bad = 1;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) S.wc[warp] = c;
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < kWarps; ++w) tot += S.wc[w];
+    a.pcnt[blk] = tot;
+    a.badv[blk] = bad;
+  }
+}
+
+// Row phase after the stop test: y' and x = x' (accelerated.hpp:96-108); count the
+// union flags (x_i != 0 or y_i != 0) for the next pass.
+__device__ void acc_rows_update(const LoopArgs& a, RowShared& S, int blk, int row0, int nrows,
+                                double momentum, int restart) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int c = 0;
+  for (int t = threadIdx.x; t < nrows; t += blockDim.x) {
+    const int i = row0 + t;
+    const double xn = a.xn[i];
+    const double yi = restart ? xn : xadd(xn, xmul(momentum, xsub(xn, a.x[i])));
+    a.y[i] = yi;
+    a.x[i] = xn;
+    c += (xn != 0.0 || yi != 0.0) ? 1 : 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) S.wc[warp] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < kWarps; ++w) tot += S.wc[w];
+    a.cnt[blk] = tot;
+  }
+}
+
+// Union list of own rows at the global offset sum(cnt[0..blk)), values x and y.
+__device__ int acc_rows_list(const LoopArgs& a, RowShared& S, int blk, int nblk, int row0,
+                             int nrows) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    int before = 0, all = 0;
+    int cv[6];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) cv[r] = lane + 32 * r < nblk ? __ldcg(a.cnt + lane + 32 * r) : 0;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      all += cv[r];
+      if (lane + 32 * r < blk) before += cv[r];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      before += __shfl_xor_sync(0xffffffffu, before, o);
+      all += __shfl_xor_sync(0xffffffffu, all, o);
+    }
+    if (lane == 0) {
+      S.base = before;
+      S.total = all;
+    }
+  }
+  const int t = threadIdx.x;  // one round: nrows <= blockDim.x
+  double xi = 0.0, yi = 0.0;
+  bool f = false;
+  if (t < nrows) {
+    xi = a.x[row0 + t];
+    yi = a.y[row0 + t];
+    f = xi != 0.0 || yi != 0.0;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, f);
+  if (lane == 0) S.wc[warp] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = S.base;
+    for (int w = 0; w < kWarps; ++w) {
+      const int c = S.wc[w];
+      S.wc[w] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (f) {
+    const int pos = S.wc[warp] + __popc(bal & ((1u << lane) - 1u));
+    a.mask[pos] = (uint32_t)(row0 + t);
+    a.gP[pos] = xi;
+    a.vy[pos] = yi;
+  }
+  return S.total;
+}
+
+__global__ void __launch_bounds__(kLoopThreads, 1) acc_loop_kernel(LoopArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ LeaderState L;
+  __shared__ RowShared RS;
+  const bool leader = blockIdx.x == 0;
+  const int R = a.rows_per_cta;
+  const int nblk = (int)gridDim.x - 1;
+  const int blk = (int)blockIdx.x - 1;
+  const int row0 = leader ? 0 : blk * R;
+  const int nrows = leader ? 0 : max(0, min(a.m - row0, R));
+  const double* qblk = a.Q + (size_t)(leader ? 0 : blk) * R * a.m;
+  RowRing ring;
+  if (!leader) ring_setup(ring, smem, kRingSmemBytes, nrows, R, kWarps);
+  double* sbuf = reinterpret_cast<double*>(smem);
+  volatile LoopCtrl* vc = a.ctrl;
+  const uint64_t t0 = globaltimer_ns();
+  if (leader && threadIdx.x == 0) {
+    a.ctrl->trace_len = 0;
+    a.ctrl->mult_len = 0;
+    a.ctrl->mult_total = 0;
+    a.ctrl->numeric_failure = 0;
+    a.ctrl->g_parity = 0;
+    a.ctrl->min_iterate = 0.0;  // result.min_iterate = 0 (:32); x' >= 0 keeps it there
+    L.best_gbs = __longlong_as_double(0x7ff0000000000000LL);
+    L.since_best = 0;
+    L.f = __longlong_as_double(0x7ff0000000000000LL);  // f_prev = +inf
+  }
+  int len = 0;       // union list length (x = y = 0 at the start: empty)
+  double t = 1.0;    // every thread carries the same momentum sequence
+  for (unsigned long long k = 0;; ++k) {
+    // ===== pass: u = Q x, w = Q y over the union list; then grad, grad_y, x' =====
+    if (!leader)
+      gemv_rows(ring, qblk, R, true, row0, nrows, a.mask, a.gP, len, a.u, nullptr, nullptr,
+                a.vy, a.w);
+    __syncthreads();  // own rows of u, w written by the consumer warps
+    if (!leader) acc_rows_after_pass(a, RS, blk, row0, nrows);
+    grid.sync();
+    // ===== vector CTA: chains and the ordered stop tests (accelerated.hpp:45-81) =====
+    if (leader) {
+      const double *x = a.x, *g = a.g, *q = a.q;
+      const int m = a.m;
+      const int lens[3] = {m, m, m};
+      leader_chains_var<3>(sbuf, kRingSmemBytes, L, lens, [&](int c, int i) {
+        const double xi = __ldcg(x + i), gi = __ldcg(g + i);
+        if (c == 0) return (xi > 0.0 || gi < 0.0) ? xmul(gi, gi) : -0.0;  // gbs over the mask
+        if (c == 1) return xi != 0.0 ? xmul(xi, gi) : -0.0;               // dot(x, grad)
+        return xi != 0.0 ? xmul(__ldcg(q + i), xi) : -0.0;                // dot(q, x)
+      });
+      if (threadIdx.x == 0) {
+        int ml = 0, bad = 0;
+        for (int b = 0; b < nblk; ++b) {
+          ml += __ldcg(a.pcnt + b);
+          bad |= __ldcg(a.badv + b);
+        }
+        const double gbs = L.res[0];
+        const double f = xmul(0.5, xadd(L.res[1], L.res[2]));
+        const double el = (double)(globaltimer_ns() - t0) * 1e-9;
+        int stop = -1;
+        if (bad || !isfinite(f) || !isfinite(gbs)) stop = 100;  // NumericFailure (:55-58)
+        else if (ml == 0) stop = ALNNLS_EMPTY_PASSIVE_SET;
+        else if (gbs < a.eps) stop = ALNNLS_GRADIENT_BELOW_EPSILON;
+        else if (k >= a.max_iters) stop = ALNNLS_MAX_ITERS;
+        else if (a.has_time_cap && el >= a.time_cap_s) stop = ALNNLS_TIME_CAP;
+        else if (a.alpha == __longlong_as_double(0x7ff0000000000000LL))  // m_norm == 0
+          stop = ALNNLS_ZERO_CURVATURE;
+        else if (gbs < L.best_gbs) {
+          L.best_gbs = gbs;
+          L.since_best = 0;
+        } else if (++L.since_best >= a.stall_window) {
+          stop = ALNNLS_STALLED;
+        }
+        int act = kActCont;
+        if (stop == 100) {
+          a.ctrl->numeric_failure = 1;
+          act = kActStop;
+        } else if (stop >= 0) {
+          stop_final(a, k, f, gbs, ml, el, stop);
+          act = kActStop;
+        } else {
+          if (k % a.trace_every == 0) write_record(a, k, f, gbs, ml, el, a.alpha, 1);
+          if (a.restart && f > L.f) act = kActRollback;  // restart (:102-105)
+        }
+        L.f = f;  // f_prev
+        a.ctrl->act = act;
+        __threadfence();
+      }
+    }
+    grid.sync();
+    const int act = vc->act;
+    if (act == kActStop) break;
+    // ===== y', x = x' (accelerated.hpp:96-108), next union list =====
+    const double t_next = xmul(0.5, xadd(1.0, __dsqrt_rn(xadd(1.0, xmul(xmul(4.0, t), t)))));
+    const double momentum = xdiv(xsub(t, 1.0), t_next);
+    const int rs = act == kActRollback;
+    if (!leader) acc_rows_update(a, RS, blk, row0, nrows, momentum, rs);
+    t = rs ? 1.0 : t_next;
+    grid.sync();
+    if (!leader) len = acc_rows_list(a, RS, blk, nblk, row0, nrows);
+    grid.sync();
+  }
+}
+
+__global__ void __launch_bounds__(kLoopThreads, 1) frobenius_kernel(const double* Qb, int m, int R,
+                                                                    double* out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ LeaderState L;
+  double* sbuf = reinterpret_cast<double*>(smem);
+  // column-major order: entry e = j*m + i (m*m < 2^31, checked on the host)
+  leader_chains<1>(sbuf, kRingSmemBytes, L, m * m, [&](int, int e) {
+    const int j = e / m, i = e - j * m;
+    const double v = __ldg(Qb + blk_index(i, j, m, R));
+    return xmul(v, v);
+  });
+  if (threadIdx.x == 0) *out = __dsqrt_rn(L.res[0]);
+}
+
 }  // namespace
 
 size_t nqp_loop_smem_bytes() { return kRingSmemBytes; }
@@ -850,4 +1080,32 @@ cudaError_t launch_masked_gemv_blocked(const double* Qb, int m, int R, const uin
   return gemv_launch(Qb, 0, m, R, 1, list, vals, len, y, stream);
 }
 
+}  // namespace alnnls
+
+namespace alnnls {
+cudaError_t launch_acc_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(acc_loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)nqp_loop_smem_bytes());
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  LoopArgs args = a;
+  void* params[] = {&args};
+  return cudaLaunchCooperativeKernel((void*)acc_loop_kernel, dim3(num_ctas), dim3(kLoopThreads),
+                                     params, nqp_loop_smem_bytes(), stream);
+}
+
+cudaError_t launch_frobenius(const double* Qb, int m, int R, double* out, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(frobenius_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)nqp_loop_smem_bytes());
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  frobenius_kernel<<<1, kLoopThreads, nqp_loop_smem_bytes(), stream>>>(Qb, m, R, out);
+  return cudaGetLastError();
+}
 }  // namespace alnnls
