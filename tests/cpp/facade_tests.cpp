@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "antilop/accelerated.hpp"
 #include "antilop/nnls.hpp"
 
 using namespace antilop;
@@ -201,6 +202,49 @@ int main() {
     const std::string js = result_summary_json(solve_nnls(DenseMatrix::identity(2), Vector{3.0, -1.0}));
     REQUIRE(js.find("\"termination\":\"GradientBelowEpsilon\"") != std::string::npos);
     REQUIRE(js.find("\"dropped_columns\":[]") != std::string::npos);
+  });
+  // ---- accelerated baseline (test_baselines.cpp:162-245, restated) ----
+  auto tight = [] {
+    SolverConfig c;
+    c.epsilon = 1e-16;
+    c.max_iters = 200000;
+    c.stall_window = 1000000;
+    return c;
+  };
+  run("accelerated: origin optimal", [] {
+    const auto res = solve_accelerated(NqpProblem(DenseMatrix::identity(2), Vector{3.0, 4.0}));
+    REQUIRE(res.termination == Termination::EmptyPassiveSet && res.iterations() == 0);
+    REQUIRE(res.x[0] == 0.0 && res.x[1] == 0.0);
+  });
+  run("accelerated: identity within 200 iterations", [] {
+    SolverConfig c;
+    c.epsilon = 1e-16;
+    c.max_iters = 200;
+    c.stall_window = 1000000;
+    const auto res = solve_accelerated(NqpProblem(DenseMatrix::identity(2), Vector{-1.0, -2.0}), c);
+    REQUIRE(res.termination == Termination::GradientBelowEpsilon && res.iterations() <= 200);
+    REQUIRE(near(res.x[0], 1.0, 1e-8) && near(res.x[1], 2.0, 1e-8));
+  });
+  run("accelerated: coupled 2x2 (plain and restart)", [&] {
+    for (bool restart : {false, true}) {
+      SolverConfig c = tight();
+      c.nesterov_restart = restart;
+      const auto res = solve_accelerated(
+          NqpProblem(DenseMatrix(2, 2, {1.0, 1.0 / 30.0, 1.0 / 30.0, 1.0}), Vector{-4.0, -5.0 / 3.0}), c);
+      REQUIRE(res.termination == Termination::GradientBelowEpsilon);
+      REQUIRE(near(res.x[0], 3550.0 / 899.0, 1e-6) && near(res.x[1], 1380.0 / 899.0, 1e-6));
+    }
+  });
+  run("accelerated: zero curvature", [] {
+    const auto res = solve_accelerated(NqpProblem(DenseMatrix(2, 2, 0.0), Vector{-1.0, -1.0}));
+    REQUIRE(res.termination == Termination::ZeroCurvature);
+  });
+  run("anti+acc: identity and zero matrix", [&] {
+    const auto r = solve_anti_accelerated(DenseMatrix::identity(2), Vector{3.0, -1.0}, tight());
+    REQUIRE(near(r.x[0], 3.0, 1e-8) && r.x[1] == 0.0 && near(r.residual_sq, 1.0, 1e-8));
+    const auto z = solve_anti_accelerated(DenseMatrix(3, 2, 0.0), Vector{1.0, 1.0, 1.0});
+    REQUIRE(z.x[0] == 0.0 && z.x[1] == 0.0 && z.inner.termination == Termination::EmptyPassiveSet);
+    REQUIRE(z.dropped_columns == (std::vector<std::size_t>{0, 1}));
   });
   std::printf("facade_tests: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
