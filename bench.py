@@ -289,8 +289,11 @@ def run_ours(args, ws, rank, local, dist):
         if dist is not None:
             dist.barrier()
 
+    anti = args.solver == "anti_acc"
+    solve_dev = s.solve_anti_accelerated_device if anti else s.solve_nnls_device
+    solve_host = s.solve_anti_accelerated if anti else s.solve_nnls
     for _ in range(args.warmup):
-        s.solve_nnls_device(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
+        solve_dev(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
     summ = s.last_summary()
     iters = int(summ.iterations)
     mults = int(summ.multiplies_total)
@@ -302,7 +305,7 @@ def run_ours(args, ws, rank, local, dist):
         s.timer_start()
         t_setup = t_loop = 0.0
         for _ in range(args.steps):
-            s.solve_nnls_device(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
+            solve_dev(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
             sm = s.last_summary()
             t_setup += sm.t_setup_s
             t_loop += sm.t_loop_s
@@ -324,11 +327,11 @@ def run_ours(args, ws, rank, local, dist):
     pb.copy_(torch.from_numpy(b))
     hA = pA.numpy().T  # Fortran-ordered (d, n) view of pinned memory
     hb = pb.numpy()
-    res = s.solve_nnls(hA, hb, cfg)  # warm
+    res = solve_host(hA, hb, cfg)  # warm
     barrier()
     s.timer_start()
     for _ in range(args.steps):
-        res = s.solve_nnls(hA, hb, cfg)
+        res = solve_host(hA, hb, cfg)
     te = s.timer_stop()
     if dist is not None:
         tt = torch.tensor([te], device="cuda", dtype=torch.float64)
@@ -366,6 +369,8 @@ def run_ours(args, ws, rank, local, dist):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64, BASELINE.json configs)",
         "config": {"workload": f"{args.workload}: d={d}, n={n}", "eps": inst["epsilon"],
+                   "solver": ("solve_anti_accelerated (accelerated.hpp)" if anti
+                              else "solve_nnls (nnls.hpp)"),
                    "stall_window": "off", "profile": "exact (bitwise reference trajectory)",
                    "l2": (f"inputs larger than L2 (A {8 * d * n / 1e6:.0f} MB, "
                           f"Q {8 * n * n / 1e6:.0f} MB)"),
@@ -376,7 +381,7 @@ def run_ours(args, ws, rank, local, dist):
         "roofline": dominant, "roofline_other": roof_setup if dominant is roof_loop else roof_loop,
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
     }
-    if ws == 1 and not args.no_cpu_baseline:
+    if ws == 1 and not args.no_cpu_baseline and not anti:
         ora, kind = ref_oracle()
         H = s.gram(A)  # bitwise equal to the reference gram (tests/test_gpu_parity.py)
         rows = sample_rows_for(inst)
@@ -667,6 +672,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--nrhs", type=int, default=0, help="c4: override the column count")
+    ap.add_argument("--solver", default="nnls", choices=["nnls", "anti_acc"],
+                    help="anti_acc: the Anti+Acc baseline (accelerated.hpp) on the same workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     ws, rank, local, dist = dist_setup(args)
