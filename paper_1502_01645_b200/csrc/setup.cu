@@ -22,7 +22,10 @@ namespace alnnls {
 namespace {
 
 constexpr int BM = 128;   // output tile (square)
-constexpr int BK = 16;    // k slab
+#ifndef ALNNLS_SYRK_BK
+#define ALNNLS_SYRK_BK 16
+#endif
+constexpr int BK = ALNNLS_SYRK_BK;  // k slab
 constexpr int NT = 512;   // 16 warps: 4 per scheduler to hide the 8-cycle DMUL->DADD latency
 constexpr int LDS = BM + 2;  // padded smem row (doubles): 16B-aligned rows, <=2-way store conflicts
 // thread tile 8 rows x 4 cols: rows 2tx+(r&1)+32(r>>1), cols 2ty+(c&1)+64(c>>1)
@@ -77,13 +80,14 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
   const uint64_t ldb = mode == 2 ? s.ldb : s.lda;
   const int nb = mode == 2 ? s.nrhs : s.n;
 
-  // loader: element e = tid + r*NT (r < 4) of a BK x BM slab: column e/BK, row k0 + e%BK.
+  // loader: element e = tid + r*NT (r < LPT) of a BK x BM slab: column e/BK, row k0 + e%BK.
   // Out-of-range elements are zero-filled (src-size 0): adding +0 to a chain is exact
   // (s + (+0) == s, and s is never -0).
-  const double* pa[4];
-  const double* pb[4];
+  constexpr int LPT = BK * BM / NT;
+  const double* pa[LPT];
+  const double* pb[LPT];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
+  for (int r = 0; r < LPT; ++r) {
     const int e = threadIdx.x + r * NT;
     const int ca = i0 + e / BK, cb = j0 + e / BK;
     pa[r] = ca < s.n ? s.A + (size_t)ca * s.lda : nullptr;
@@ -93,7 +97,7 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
     const int buf = (kb - kb0) % kStages;
     const int k0 = kb * BK;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < LPT; ++r) {
       const int e = threadIdx.x + r * NT;
       const int kk = e % BK, k = k0 + kk;
       const bool va = pa[r] && k < s.d, vb = pb[r] && k < s.d;
