@@ -190,9 +190,9 @@ __global__ void __launch_bounds__(384, 1) k(const double* Qb, int m, int R, cons
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1); float ms;
-  const int m = 4096; const double dens = 0.71;
+  const int m = 4096; const double dens = argc > 1 ? atof(argv[1]) : 0.71;
   int R = (m + 146) / 147; R = (R + 3) & ~3; const int nb = (m + R - 1) / R;
   double *Q, *vals, *y; uint32_t* list;
   CK(cudaMalloc(&Q, (size_t)nb * R * m * 8)); CK(cudaMemset(Q, 0, (size_t)nb * R * m * 8));
@@ -212,11 +212,11 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     printf("%-22s G=%2d P=%d: %6.1f us/pass (|P|=%d, chain floor %.1f us)\n", name, G, P, ms * 1e3 / 20, L, L * 8 / 1.9e3);
   };
-  for (int G : {64}) for (int P : {4}) {
+  for (int G : {64}) for (int P : {1, 2, 3, 4}) {
     run(k<5>, "stage in regs", G, P);
-    run(k<1>, "no MACs", G, P);
+    run(k<8>, "consumer only (regs)", G, P);
   }
-  run(k<8>, "consumer only (regs)", 64, 4);
+  run(k<1>, "no MACs", 64, 4);
   run(k<10>, "consumer only (pinned)", 64, 4);
   run(k<9>, "full pinned", 64, 4);
   return 0;
