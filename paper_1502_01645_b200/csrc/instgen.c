@@ -134,6 +134,127 @@ int alnnls_gen_matrix(double* A, uint64_t d, uint64_t n, uint64_t seed, int law,
   return 0;
 }
 
+/* ---- c3: A = U diag(s) V^T with U, V Haar-random orthogonal -----------------------
+ * Deterministic on any host and thread count (no BLAS/LAPACK): Stewart's
+ * construction Q = H_0 H_1 ... H_{n-2} S, each H_k a Householder reflection built
+ * from an independent seeded Gaussian vector of length n - k (column k of a
+ * seeded N(0,1) matrix, rows k..n-1), S the sign fix that makes the implied
+ * triangular factor positive. Every sum runs in a fixed order and every row is
+ * owned by one thread. */
+typedef struct {
+  double* Qr;          /* n x n row-major */
+  const double* u;     /* reflector, length L (rows k..n-1 of the row space) */
+  uint64_t n, k, r0, r1;
+  double beta;
+} refl_job;
+
+static void* refl_rows(void* arg) {
+  refl_job* jb = (refl_job*)arg;
+  const uint64_t L = jb->n - jb->k;
+  for (uint64_t i = jb->r0; i < jb->r1; ++i) {
+    double* row = jb->Qr + i * jb->n + jb->k;
+    double w = 0.0;
+    for (uint64_t j = 0; j < L; ++j) w += row[j] * jb->u[j];
+    const double c = jb->beta * w;
+    for (uint64_t j = 0; j < L; ++j) row[j] -= c * jb->u[j];
+  }
+  return NULL;
+}
+
+static void haar(double* Q /* n x n column-major out */, uint64_t n, uint64_t seed, int threads) {
+  double* G = (double*)malloc(sizeof(double) * n * n);
+  double* Qr = (double*)calloc(n * n, sizeof(double));
+  double* u = (double*)malloc(sizeof(double) * (n ? n : 1));
+  double* sgn = (double*)malloc(sizeof(double) * (n ? n : 1));
+  fill_matrix(G, n, n, seed, LAW_NORMAL, NULL, 1.0, threads);
+  for (uint64_t i = 0; i < n; ++i) Qr[i * n + i] = 1.0;
+  if (threads < 1) threads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+  refl_job* jobs = (refl_job*)malloc(sizeof(refl_job) * threads);
+  for (uint64_t k = 0; k + 1 < n; ++k) {
+    const uint64_t L = n - k;
+    const double* v = G + k * n + k;
+    double nrm2 = 0.0;
+    for (uint64_t j = 0; j < L; ++j) nrm2 += v[j] * v[j];
+    const double nrm = sqrt(nrm2);
+    const double s0 = v[0] >= 0.0 ? 1.0 : -1.0;
+    for (uint64_t j = 0; j < L; ++j) u[j] = v[j];
+    u[0] += s0 * nrm; /* H v = -s0 ||v|| e_0 */
+    double uu = 0.0;
+    for (uint64_t j = 0; j < L; ++j) uu += u[j] * u[j];
+    sgn[k] = -s0;
+    if (uu == 0.0) continue;
+    const double beta = 2.0 / uu;
+    for (int t = 0; t < threads; ++t) {
+      refl_job jb = {Qr, u, n, k, n * t / threads, n * (t + 1) / threads, beta};
+      jobs[t] = jb;
+      pthread_create(&th[t], NULL, refl_rows, &jobs[t]);
+    }
+    for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+  }
+  if (n) sgn[n - 1] = G[(n - 1) * n + (n - 1)] >= 0.0 ? 1.0 : -1.0;
+  for (uint64_t i = 0; i < n; ++i) /* column-major out, columns scaled by the sign fix */
+    for (uint64_t j = 0; j < n; ++j) Q[j * n + i] = Qr[i * n + j] * sgn[j];
+  free(G);
+  free(Qr);
+  free(u);
+  free(sgn);
+  free(th);
+  free(jobs);
+}
+
+typedef struct {
+  double* A;
+  const double* U;
+  const double* W; /* W[j*k + t] = s_t * V[j, t] */
+  uint64_t d, k, j0, j1;
+} prod_job;
+
+static void* prod_cols(void* arg) {
+  prod_job* jb = (prod_job*)arg;
+  for (uint64_t j = jb->j0; j < jb->j1; ++j) {
+    double* a = jb->A + j * jb->d;
+    for (uint64_t i = 0; i < jb->d; ++i) a[i] = 0.0;
+    for (uint64_t t = 0; t < jb->k; ++t) {
+      const double c = jb->W[j * jb->k + t];
+      const double* ut = jb->U + t * jb->d;
+      for (uint64_t i = 0; i < jb->d; ++i) a[i] += ut[i] * c;
+    }
+  }
+  return NULL;
+}
+
+/* A (d x n, column-major) = U[:, :k] diag(s) V[:, :k]^T, s_t = 10^(-6 t / (k-1)). */
+int alnnls_gen_c3_matrix(double* A, uint64_t d, uint64_t n, uint64_t seed, int threads) {
+  const uint64_t k = d < n ? d : n;
+  double* U = (double*)malloc(sizeof(double) * d * d);
+  double* V = (double*)malloc(sizeof(double) * n * n);
+  double* W = (double*)malloc(sizeof(double) * n * (k ? k : 1));
+  haar(U, d, seed * 1000 + 11, threads);
+  haar(V, n, seed * 1000 + 13, threads);
+  for (uint64_t j = 0; j < n; ++j)
+    for (uint64_t t = 0; t < k; ++t) {
+      const double st = pow(10.0, -6.0 * (double)t / (double)(k > 1 ? k - 1 : 1));
+      W[j * k + t] = st * V[t * n + j];
+    }
+  if (threads < 1) threads = 1;
+  if ((uint64_t)threads > n) threads = (int)(n ? n : 1);
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+  prod_job* jobs = (prod_job*)malloc(sizeof(prod_job) * threads);
+  for (int t = 0; t < threads; ++t) {
+    prod_job jb = {A, U, W, d, k, n * t / threads, n * (t + 1) / threads};
+    jobs[t] = jb;
+    pthread_create(&th[t], NULL, prod_cols, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+  free(U);
+  free(V);
+  free(W);
+  free(th);
+  free(jobs);
+  return 0;
+}
+
 /*
  * BASELINE.json configs (kind 1..5). A is d x n column-major, b has d entries,
  * x_true n. kind 3 (Haar product) is assembled by the Python harness from

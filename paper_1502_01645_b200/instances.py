@@ -38,6 +38,7 @@ def _gen():
         L.alnnls_gen_config.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, dp, dp, dp,
                                         C.c_int]
         L.alnnls_gen_htrue.argtypes = [dp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64]
+        L.alnnls_gen_c3_matrix.argtypes = [dp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int]
         _lib = L
     return _lib
 
@@ -75,12 +76,8 @@ def make_config(name, d=None, n=None, seed=None):
     b = np.empty(d)
     x = np.empty(n)
     if kind == 3:
-        U = _haar(d, seed * 1000 + 11)
-        V = _haar(n, seed * 1000 + 13)
-        k = min(d, n)
-        s = 10.0 ** (-6.0 * np.arange(k) / max(1, k - 1))
-        Af = (U[:, :k] * s[None, :]) @ V[:, :k].T
-        A[:] = np.asfortranarray(Af).reshape(-1, order="F")
+        # U diag(s) V^T with Haar U, V, assembled in C (deterministic on any host)
+        _gen().alnnls_gen_c3_matrix(A, d, n, seed, _threads())
     _gen().alnnls_gen_config(kind, d, n, seed, A, b, x, _threads())
     return {
         "A": A.reshape(d, n, order="F"),
