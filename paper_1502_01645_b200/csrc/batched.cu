@@ -24,6 +24,9 @@ namespace alnnls {
 
 namespace {
 
+#ifndef ALNNLS_GEMM_JB
+#define ALNNLS_GEMM_JB 8  // Q columns per register block of the batched GEMM (prefetch distance)
+#endif
 constexpr int kBT = 512;          // threads per batched CTA (one warp per column at NB = 16)
 constexpr int kMaxCols = 16;      // NB upper bound (columns per CTA)
 
@@ -515,7 +518,7 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
     int active = 0;
     for (int b = 0; b < NB; ++b) active |= S.phase[b] != kIdle;
     if (!active) break;
-    gemm_pass<RPT, CG, ROWT, LD>(a, sm, grp, trow);
+    gemm_pass<RPT, CG, ROWT, LD, ALNNLS_GEMM_JB>(a, sm, grp, trow);
     __syncthreads();
     for (int b = warp; b < NB; b += nwarps) column_step(a, S, sm, b);
     __syncthreads();
