@@ -33,13 +33,15 @@ struct alnnls_ctx {
   int sm_count = 0;
   int cc_major = 0, cc_minor = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // H2D of the host-buffer entries (overlapped uploads)
   cudaEvent_t ev[6] = {};
+  cudaEvent_t up[8] = {};             // row-block upload events
   std::string err;
 
   DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
   DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
       hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb, uP, gdC, skp, skf,
-      ay, axn, aw, avy, apc;
+      ay, axn, aw, avy, apc, tst;
 
   // last solve
   bool last_nnls = false;
@@ -485,6 +487,148 @@ int device_check_finite(alnnls_ctx* ctx, std::initializer_list<FiniteArg> args) 
   return ALNNLS_OK;
 }
 
+// Host-buffer solve_nnls with the upload of A overlapped with the Gram: A is
+// copied in row blocks on the copy stream, and each block's Gram contribution
+// is computed as soon as it lands by continuing every tile's chain states over
+// its rows (setup.cu syrk_rowblock_kernel; A^T b chains likewise), so the
+// result is bitwise the one-shot Gram. The finiteness check runs after the last
+// block (results are discarded on failure, as if validated first).
+constexpr int kUpBlocks = 4;
+int run_nnls_overlapped(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, const double* b,
+                        const alnnls_config* cfg, alnnls_summary* out) {
+  int st__ = ALNNLS_OK;
+  cudaStream_t s = ctx->stream, cs = ctx->copy_stream;
+  const uint64_t lda = round_up(d, 4);
+  double* dA = ENSURE(double, A, lda * n);
+  double* db = ENSURE(double, b, d);
+  const uint64_t T = gram_tiles(n);
+  const uint64_t TD = 32 * 512;
+  double* H = ENSURE(double, H, n * n);
+  double* st_buf = ENSURE(double, tst, 2 * T * TD);  // ping-pong tile chain states
+  double* hb = ENSURE(double, hvec, 2 * n + 8);       // ping-pong A^T b chain states
+  CK(cudaEventRecord(ctx->ev[0], s));
+  CK(cudaStreamWaitEvent(cs, ctx->ev[0], 0));
+  CK(cudaMemcpyAsync(db, b, sizeof(double) * d, cudaMemcpyHostToDevice, cs));
+  const double* pin = nullptr;
+  const double* hin = nullptr;
+  for (int k = 0; k < kUpBlocks; ++k) {
+    const uint64_t r0 = d * k / kUpBlocks, r1 = d * (k + 1) / kUpBlocks;
+    if (r1 > r0)
+      CK(cudaMemcpy2DAsync(dA + r0, lda * sizeof(double), A + r0, d * sizeof(double),
+                           (r1 - r0) * sizeof(double), n, cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(ctx->up[k], cs));
+    CK(cudaStreamWaitEvent(s, ctx->up[k], 0));
+    if (r1 == r0) continue;
+    const bool last = r1 == d;
+    SetupArgs sa{};
+    sa.A = dA + r0;
+    sa.lda = lda;
+    sa.d = (int)(r1 - r0);
+    sa.n = (int)n;
+    sa.H = H;
+    double* pout = last ? nullptr : st_buf + (size_t)(k & 1) * T * TD;
+    sa.tpin = pin;
+    sa.tpout = pout;
+    if (int rc = streamk_buffers(ctx, sa, 0)) return rc;
+    if (sa.sk_ctas > 0) {
+      CK(launch_syrk(sa, 0, s));  // stream-K over all tiles, chains continued
+    } else {
+      CK(launch_syrk_rowblock(sa, 0, (int)T, pin, pout, s));
+    }
+    double* hout = hb + (size_t)(k & 1) * (n + 4);
+    CK(launch_coldot(dA + r0, lda, (int)(r1 - r0), (int)n, db + r0, hout, s, hin));
+    pin = pout;
+    hin = hout;
+  }
+  if (int rc = device_check_finite(ctx, {{dA, d, n, lda, "DenseMatrix: non-finite entry"},
+                                         {db, d, 1, d, "Vector: non-finite entry"}}))
+    return rc;
+  // rescale from the finished H and A^T b, loop, unscale, residual
+  alnnls_summary sum{};
+  {
+    const double* atb = hin;
+    SetupArgs sa{};
+    sa.n = (int)n;
+    sa.diag = ENSURE(double, diag, n);
+    sa.pos = ENSURE(int, pos, n);
+    sa.scale = ENSURE(double, scale, n);
+    sa.retained = ENSURE(uint32_t, retained, n);
+    sa.m_out = ENSURE(int, mscalar, 4);
+    double* h = ENSURE(double, bcols, n + 8);
+    CK(launch_diag(H, (int)n, sa.diag, s));
+    CK(launch_negate(atb, (int)n, h, s));
+    CK(launch_retained(sa, s));
+    int hm = 0;
+    CK(cudaMemcpyAsync(&hm, sa.m_out, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint64_t m = (uint64_t)hm;
+    const uint64_t mm = m > 0 ? m : 1;
+    ctx->qR = (uint64_t)nqp_rows_per_cta((int)mm, ctx->sm_count);
+    double* Q = ENSURE(double, Q, blocked_size(mm, ctx->qR));
+    double* q = ENSURE(double, q, vec_pad(m));
+    if (m > 0) CK(launch_rescale_from_h(H, h, (int)n, sa.pos, sa.scale, Q, (int)m, (int)ctx->qR, q, s));
+    ctx->have_setup = true;
+    CK(cudaEventRecord(ctx->ev[1], s));
+    ctx->last_nnls = true;
+    ctx->last_n = n;
+    ctx->last_m = m;
+    double* y = ENSURE(double, y_out, mm);
+    if (m > 0) {
+      Resolved r;
+      if (int rc = resolve(ctx, cfg, m, &r)) return rc;
+      if (int rc = run_nqp(ctx, m, r, cfg, nullptr, &sum, ctx->solver)) {
+        if (out) *out = sum;
+        ctx->last = sum;
+        return rc;
+      }
+      CK(cudaMemcpyAsync(y, ctx->g_parity ? ctx->x_alt.p : ctx->x.p, sizeof(double) * m,
+                         cudaMemcpyDeviceToDevice, s));
+    } else {
+      alnnls_iter_record rec{};
+      alnnls_iter_record* tr = ENSURE(alnnls_iter_record, trace, 2);
+      CK(cudaMemcpyAsync(tr, &rec, sizeof(rec), cudaMemcpyHostToDevice, s));
+      sum.termination = ALNNLS_EMPTY_PASSIVE_SET;
+      sum.trace_len = 1;
+      CK(cudaEventRecord(ctx->ev[2], s));
+      CK(cudaEventRecord(ctx->ev[3], s));
+    }
+    double* xn = ENSURE(double, X, n);
+    CK(launch_unscale(y, sa.scale, sa.retained, (int)m, xn, (int)n, s));
+    uint32_t* list = ENSURE(uint32_t, list, n);
+    double* vals = ENSURE(double, vals, n + 8);
+    int* len = ENSURE(int, mscalar, 4);
+    CK(launch_support(xn, (int)n, list, vals, len, s));
+    int hlen = 0;
+    CK(cudaMemcpyAsync(&hlen, len, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double* ax = ENSURE(double, ax, d);
+    double* pr = ENSURE(double, resid, d + 8);
+    double* res = ENSURE(double, flag, 8);  // doubles in the flag buffer (ints there are done)
+    CK(launch_masked_gemv(dA, lda, (int)d, list, vals, hlen, ax, ctx->sm_count, s));
+    CK(launch_residual(ax, db, (int)d, pr, res, s));
+    CK(cudaEventRecord(ctx->ev[4], s));
+    double hres = 0.0;
+    CK(cudaMemcpyAsync(&hres, res, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float t01 = 0, t23 = 0, t34 = 0, t04 = 0;
+    cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&t34, ctx->ev[3], ctx->ev[4]);
+    cudaEventElapsedTime(&t04, ctx->ev[0], ctx->ev[4]);
+    sum.t_setup_s = t01 * 1e-3;  // includes the overlapped upload
+    sum.t_loop_s = t23 * 1e-3;
+    sum.t_finish_s = t34 * 1e-3;
+    sum.t_total_s = t04 * 1e-3;
+    sum.residual_sq = hres;
+    sum.n = n;
+    sum.m = m;
+    sum.n_dropped = n - m;
+  }
+  ctx->last = sum;
+  if (out) *out = sum;
+  return ALNNLS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -519,6 +663,8 @@ int alnnls_create(alnnls_ctx** out, int device) {
     return ALNNLS_ENODEV;
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
+  for (auto& e : c->up) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
   *out = c;
   return ALNNLS_OK;
 }
@@ -535,11 +681,14 @@ void alnnls_destroy(alnnls_ctx* ctx) {
                     &ctx->X,      &ctx->x_alt, &ctx->mask2,   &ctx->gP2,   &ctx->xP2,  &ctx->qP2,
                     &ctx->part,   &ctx->resb,  &ctx->yb,      &ctx->qb,   &ctx->uP,   &ctx->gdC,
                     &ctx->skp,    &ctx->skf,   &ctx->ay,      &ctx->axn,   &ctx->aw,
-                    &ctx->avy,    &ctx->apc};
+                    &ctx->avy,    &ctx->apc,   &ctx->tst};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->up)
+    if (e) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -587,6 +736,10 @@ int alnnls_solve_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, 
   if (rc) return rc;
   if (!cfg || !A || !b) return set_err(ctx, ALNNLS_EINVAL, "solve_nnls: null argument");
   if (d < 1 || n < 1) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  // large exact problems: overlap the upload of A with the Gram (row blocks)
+  if (cfg->profile == ALNNLS_PROFILE_EXACT && d >= 4096 && n >= 1024 && n <= 46340 &&
+      d * n >= (uint64_t)1 << 24)
+    return run_nnls_overlapped(ctx, d, n, A, b, cfg, out);
   int st__ = ALNNLS_OK;
   uint64_t lda = 0;
   if ((rc = upload_matrix(ctx, ctx->A, d, n, A, &lda))) return rc;

@@ -128,6 +128,10 @@ struct SetupArgs {
   double* sk_part;
   int* sk_flag;
   int sk_ctas;
+  // mode 0 row-block continuation through the stream-K kernel: every tile's chain
+  // starts from tpin[t] and ends in tpout[t] ([tiles][32][512]) instead of 0 / H
+  const double* tpin;
+  double* tpout;
 };
 // CTAs for the stream-K exact SYRK of this shape (0: use one CTA per tile).
 int syrk_streamk_ctas(const SetupArgs& s, int mode, int sm_count);

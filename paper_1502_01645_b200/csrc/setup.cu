@@ -220,10 +220,14 @@ __global__ void __launch_bounds__(NT, 1) syrk_streamk_kernel(SetupArgs s, int mo
   const int t1 = (int)((u1 - 1) / nk), k1 = (int)((u1 - 1) % nk) + 1;
   double* my_part = s.sk_part + (size_t)blockIdx.x * 32 * NT;
   int ti, tj;
+  // tile chain states carried in from earlier row blocks / out to later ones
+  // (row-block continuation, s.tpin / s.tpout, [tiles][32][NT]; nullptr: none)
+  auto tin = [&](int t) { return s.tpin ? s.tpin + (size_t)t * 32 * NT : nullptr; };
+  auto tout = [&](int t) { return s.tpout ? s.tpout + (size_t)t * 32 * NT : nullptr; };
   // 1. trailing partial tile: slabs [0, k1) of t1, handed to the next CTA
   if (k1 < nk) {
     tile_of(s, mode, t1, ti, tj);
-    syrk_piece(s, mode, syrk_sm, ti, tj, 0, k1, nullptr, my_part);
+    syrk_piece(s, mode, syrk_sm, ti, tj, 0, k1, tin(t1), my_part);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(NT, 1) syrk_streamk_kernel(SetupArgs s, int mo
   const int full_hi = k1 == nk ? t1 : t1 - 1;
   for (int t = full_lo; t <= full_hi; ++t) {
     tile_of(s, mode, t, ti, tj);
-    syrk_piece(s, mode, syrk_sm, ti, tj, 0, nk, nullptr, nullptr);
+    syrk_piece(s, mode, syrk_sm, ti, tj, 0, nk, tin(t), tout(t));
   }
   // 3. leading partial tile: slabs [k0, nk) of t0, continuing CTA blockIdx-1's chains
   if (k0 > 0) {
@@ -250,7 +254,7 @@ __global__ void __launch_bounds__(NT, 1) syrk_streamk_kernel(SetupArgs s, int mo
     __syncthreads();
     tile_of(s, mode, t0, ti, tj);
     syrk_piece(s, mode, syrk_sm, ti, tj, k0, nk, s.sk_part + (size_t)(blockIdx.x - 1) * 32 * NT,
-               nullptr);
+               tout(t0));
   }
 }
 // q_b = h(j_b) / D_b with h = -(A^T b) (nnls.hpp:79, :133-134); atb = A^T b.
