@@ -509,7 +509,10 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
   constexpr int nwarps = kBT / 32;
   for (int b = warp; b < NB; b += nwarps) refill(a, S, sm, b);
   __syncthreads();
-  constexpr int CG = NB < 8 ? NB : 8;
+#ifndef ALNNLS_GEMM_CG
+#define ALNNLS_GEMM_CG 8
+#endif
+  constexpr int CG = NB < ALNNLS_GEMM_CG ? NB : ALNNLS_GEMM_CG;  // columns per thread
   constexpr int GROUPS = NB / CG;
   constexpr int ROWT = kBT / GROUPS;
   constexpr int RPT = (4096 / NB + ROWT - 1) / ROWT;  // rows per thread at the largest m (4096/NB)
