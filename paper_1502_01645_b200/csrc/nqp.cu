@@ -524,7 +524,6 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
   RowRing ring;
   if (!leader) ring_setup(ring, smem, kRingSmemBytes, nrows, R, kWarps);
   double* sbuf = reinterpret_cast<double*>(smem);
-  volatile LoopCtrl* vc = a.ctrl;
   double* xb[2] = {a.x, a.x_alt};
   double* gb[2] = {a.g, a.g_alt};
   const ListSet ls[2] = {{a.mask, a.gP, a.xP, a.qP}, {a.mask2, a.gP2, a.xP2, a.qP2}};
@@ -661,7 +660,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
       }
     }
     grid.sync();  // B1
-    const int act = vc->act;
+    const int act = __ldcg(&a.ctrl->act);  // after the grid barrier: L2 read, no sys-scope volatile
     if (act == kActStop) break;
     if (act == kActRollback) {  // back to the state before the rejected step
       xp ^= 1;
@@ -740,12 +739,12 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
       }
     }
     grid.sync();  // B_C
-    const int st2 = vc->state2;
+    const int st2 = __ldcg(&a.ctrl->state2);
     if (st2 == kS2Stop) break;
     if (st2 == kS2NoMove) continue;
 
     // ===== P2, speculative update, next passive lists ====================================
-    const int cl = vc->chg_len;
+    const int cl = __ldcg(&a.ctrl->chg_len);
     if (!leader) gemv_rows(ring, qblk, R, true, row0, nrows, a.chg, a.dC, cl, a.gd);
     grid.sync();  // B2
     if (leader && threadIdx.x == 0) phase_mark(L, 4);
@@ -894,7 +893,6 @@ __global__ void __launch_bounds__(kLoopThreads, 1) acc_loop_kernel(LoopArgs a) {
   RowRing ring;
   if (!leader) ring_setup(ring, smem, kRingSmemBytes, nrows, R, kWarps);
   double* sbuf = reinterpret_cast<double*>(smem);
-  volatile LoopCtrl* vc = a.ctrl;
   const uint64_t t0 = globaltimer_ns();
   if (leader && threadIdx.x == 0) {
     a.ctrl->trace_len = 0;
@@ -968,7 +966,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) acc_loop_kernel(LoopArgs a) {
       }
     }
     grid.sync();
-    const int act = vc->act;
+    const int act = __ldcg(&a.ctrl->act);  // after the grid barrier: L2 read, no sys-scope volatile
     if (act == kActStop) break;
     // ===== y', x = x' (accelerated.hpp:96-108), next union list =====
     const double t_next = xmul(0.5, xadd(1.0, __dsqrt_rn(xadd(1.0, xmul(xmul(4.0, t), t)))));
