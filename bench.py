@@ -135,10 +135,16 @@ def dist_setup(args):
     return ws, rank, local, dist
 
 
-def solver_config(inst):
+PROFILE = {"exact": 0, "fast": 1}
+PROFILE_DESC = {"exact": "exact (bitwise reference trajectory)",
+                "fast": "fast (DMMA Gram / Q V passes; not reference-bitwise, DESIGN.md 2a)"}
+
+
+def solver_config(inst, profile="exact"):
     from paper_1502_01645_b200.api import SolverConfig
     # stall off like the reference's own benchmark convention (acceptance.cpp:73-88)
-    return SolverConfig(epsilon=inst["epsilon"], max_iters=inst["max_iters"], stall_window=10**9)
+    return SolverConfig(epsilon=inst["epsilon"], max_iters=inst["max_iters"], stall_window=10**9,
+                        profile=PROFILE[profile])
 
 
 def traffic_from_profiles(workload, kernel):
@@ -278,7 +284,7 @@ def run_ours(args, ws, rank, local, dist):
     inst = instances.make_config(args.workload)
     A, b = inst["A"], inst["b"]
     d, n = A.shape
-    cfg = solver_config(inst)
+    cfg = solver_config(inst, args.profile)
     s = Solver(local)
     # inputs resident in HBM: column-major A == row-major (n, d) tensor
     dA = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
@@ -373,7 +379,7 @@ def run_ours(args, ws, rank, local, dist):
         "config": {"workload": f"{args.workload}: d={d}, n={n}", "eps": inst["epsilon"],
                    "solver": ("solve_anti_accelerated (accelerated.hpp)" if anti
                               else "solve_nnls (nnls.hpp)"),
-                   "stall_window": "off", "profile": "exact (bitwise reference trajectory)",
+                   "stall_window": "off", "profile": PROFILE_DESC[args.profile],
                    "l2": (f"inputs larger than L2 (A {8 * d * n / 1e6:.0f} MB, "
                           f"Q {8 * n * n / 1e6:.0f} MB)"),
                    "parallelism": f"replicas x{ws}"},
@@ -567,7 +573,7 @@ def run_ours_batched(args, ws, rank, local, dist):
     dX = torch.empty((kc, n), dtype=torch.float64, device="cuda")
     del dH
     torch.cuda.synchronize()
-    cfg = SolverConfig(epsilon=spec["epsilon"], stall_window=10**9)
+    cfg = SolverConfig(epsilon=spec["epsilon"], stall_window=10**9, profile=PROFILE[args.profile])
     s = Solver(local)
 
     def barrier():
@@ -645,7 +651,9 @@ def run_ours_batched(args, ws, rank, local, dist):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64, BASELINE.json configs[3]; B = A H_true formed on device)",
         "config": {"workload": f"c4: d={d}, n={n}, nrhs={K}", "eps": spec["epsilon"],
-                   "stall_window": "off", "profile": "exact (bitwise per-column reference trajectory)",
+                   "stall_window": "off",
+                   "profile": ("exact (bitwise per-column reference trajectory)"
+                               if args.profile == "exact" else PROFILE_DESC["fast"]),
                    "l2": "inputs larger than L2 (B 10.5 GB at c4)",
                    "parallelism": f"column shards x{ws}", "columns_rank0": kc},
         "iterations_mean": float(iters.mean()), "iterations_max": int(iters.max()),
@@ -674,6 +682,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--nrhs", type=int, default=0, help="c4: override the column count")
+    ap.add_argument("--profile", default="exact", choices=["exact", "fast"],
+                    help="fast: tensor-core (DMMA) Gram / batched passes, opt-in, not bitwise")
     ap.add_argument("--solver", default="nnls", choices=["nnls", "anti_acc"],
                     help="anti_acc: the Anti+Acc baseline (accelerated.hpp) on the same workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -476,6 +476,64 @@ __device__ void column_step(const BatchArgs& a, ColState& S, const BatchSmem& sm
   __syncwarp();
 }
 
+// FAST profile: the pass U = Q V on the fp64 tensor cores (mma.sync m16n8k8
+// DMMA, the dmma.cu fragment layout), NB = 16 columns, m <= 256: warp w owns
+// rows [16w, 16w + 16) for both 8-column halves. DMMA sums each k8 group with
+// its own ordering, so this is not the reference's chain (FAST is opt-in).
+__device__ __forceinline__ void dmma8(double (&c)[4], double a0, double a1, double a2, double a3,
+                                      double b0, double b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+}
+
+template <int LD>
+__device__ __forceinline__ void dmma_gemm_pass16(const BatchArgs& a, const BatchSmem& sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int m = sm.m, mp = sm.mp;
+  const int r0 = warp * 16;
+  if (r0 >= m) return;
+  const int ra = r0 + g, rb = r0 + g + 8;
+  const bool va = ra < m, vb = rb < m;
+  double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+  constexpr int U = 4;  // k-steps whose Q fragments load together
+  for (int k0 = 0; k0 < mp; k0 += 8 * U) {
+    double q[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k1 = k0 + 8 * u + t, k2 = k1 + 4;
+      const double* c1 = a.Q + (size_t)k1 * m;
+      const double* c2 = a.Q + (size_t)k2 * m;
+      q[u][0] = va && k1 < m ? __ldg(c1 + ra) : 0.0;
+      q[u][1] = vb && k1 < m ? __ldg(c1 + rb) : 0.0;
+      q[u][2] = va && k2 < m ? __ldg(c2 + ra) : 0.0;
+      q[u][3] = vb && k2 < m ? __ldg(c2 + rb) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k1 = k0 + 8 * u + t;
+      if (k0 + 8 * u >= mp) break;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const double b0 = sm.V[(size_t)k1 * LD + 8 * nt + g];
+        const double b1 = sm.V[(size_t)(k1 + 4) * LD + 8 * nt + g];
+        dmma8(acc[nt], q[u][0], q[u][1], q[u][2], q[u][3], b0, b1);
+      }
+    }
+  }
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int row = (c < 2 ? ra : rb);
+      const int col = 8 * nt + 2 * t + (c & 1);
+      if (row < m) sm.U[(size_t)col * mp + row] = acc[nt][c];
+    }
+}
+
 __device__ __forceinline__ BatchSmem carve(double* bsm, int m, int nb) {
   BatchSmem sm;
   const int mp = round8(m);
@@ -521,7 +579,11 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
     int active = 0;
     for (int b = 0; b < NB; ++b) active |= S.phase[b] != kIdle;
     if (!active) break;
-    gemm_pass<RPT, CG, ROWT, LD, ALNNLS_GEMM_JB>(a, sm, grp, trow);
+    if (NB == 16 && a.fast) {
+      dmma_gemm_pass16<LD>(a, sm);
+    } else {
+      gemm_pass<RPT, CG, ROWT, LD, ALNNLS_GEMM_JB>(a, sm, grp, trow);
+    }
     __syncthreads();
     for (int b = warp; b < NB; b += nwarps) column_step(a, S, sm, b);
     __syncthreads();

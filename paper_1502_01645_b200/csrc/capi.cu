@@ -1157,6 +1157,7 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
     ba.max_iters = r.max_iters;
     ba.stall_window = cfg->stall_window;
     ba.next_col = counter;
+    ba.fast = cfg->profile == ALNNLS_PROFILE_FAST;
     CK(cudaEventRecord(ctx->ev[2], s));
     CK(launch_batched(ba, ctx->sm_count, s));
     CK(cudaEventRecord(ctx->ev[3], s));

@@ -19,7 +19,10 @@ dX = torch.empty((nrhs, n), dtype=torch.float64, device="cuda")
 torch.cuda.synchronize()
 print("gen", round(time.time() - t, 2), "s", flush=True)
 s = Solver(0)
-cfg = SolverConfig(epsilon=spec["epsilon"], stall_window=10**9)
+from paper_1502_01645_b200 import abi
+fast = len(sys.argv) > 2 and sys.argv[2] == "fast"
+cfg = SolverConfig(epsilon=spec["epsilon"], stall_window=10**9,
+                   profile=abi.PROFILE_FAST if fast else abi.PROFILE_EXACT)
 for rep in range(2):
     t = time.time()
     cols, tm = s.solve_nnls_batched_device(dA.data_ptr(), dB.data_ptr(), dX.data_ptr(), d, n, nrhs, cfg)
