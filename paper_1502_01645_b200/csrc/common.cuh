@@ -79,48 +79,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       : "memory");
 }
 
-// L1-bypassing load for data written by other CTAs of the same launch.
-__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
-__device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) { return __ldcg(p); }
-
-// ---- grid barrier for a cooperative (co-resident) launch ---------------------------
-// Sense-reversing barrier on two words in global memory ({count, generation}).
-// Waiters back off with __nanosleep so 147 spinning CTAs do not hammer the L2
-// slice the vector CTA also uses. All threads of every CTA must call it.
-struct GridBarrier {
-  unsigned int* count;
-  unsigned int* gen;
-};
-
-__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void grid_barrier(const GridBarrier& b, unsigned int& local_gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int g = local_gen;
-    __threadfence();
-    const unsigned int arrived = atomicAdd(b.count, 1u);
-    if (arrived == gridDim.x - 1) {
-      atomicExch(b.count, 0u);
-      __threadfence();
-      atomicExch(b.gen, g + 1u);
-    } else {
-      unsigned int ns = 32;
-      while (ld_acquire_gpu(b.gen) == g) {
-        __nanosleep(ns);
-        ns = ns < 256 ? ns * 2 : 256;
-      }
-    }
-    local_gen = g + 1u;
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 // ---- block scan (exclusive) of one int per thread -----------------------------
 // Returns the exclusive prefix; *total gets the block sum. Uses `scratch`
 // (>= 33 ints of shared memory). All threads of the block must call it.
@@ -171,58 +129,6 @@ __device__ __forceinline__ double chain_sum_from(double s, const double* __restr
     for (int k = 0; k < B; ++k) s = xadd(s, buf[k]);
   }
   for (; t < len; ++t) s = xadd(s, p[t]);
-  return s;
-}
-
-// Warp-cooperative sequential chain: s = ((0 + p(0)) + p(1)) + ... + p(len-1).
-// Lanes compute the products of a 32-element round in parallel (rounded
-// exactly like the reference, inside `prod`), then every lane runs the same
-// dependent DADD chain over the round via shuffles, so only the adds are
-// serial (8-cycle DADD latency per element on B200). Rounds are prefetched
-// kDepth ahead to hide L2 latency. Must be called by all 32 lanes of a warp;
-// the result is returned in every lane.
-template <int kDepth = 4, class F>
-__device__ __forceinline__ double warp_chain(int len, F prod) {
-  const int lane = threadIdx.x & 31;
-  double p[kDepth];
-#pragma unroll
-  for (int r = 0; r < kDepth; ++r) {
-    const int t = r * 32 + lane;
-    p[r] = t < len ? prod(t) : 0.0;
-  }
-  double s = 0.0;
-  for (int base = 0; base < len; base += 32 * kDepth) {
-#pragma unroll
-    for (int r = 0; r < kDepth; ++r) {
-      const int rb = base + r * 32;
-      const double cur = p[r];
-      const int tn = rb + 32 * kDepth + lane;
-      p[r] = tn < len ? prod(tn) : 0.0;  // refill this slot for the next sweep
-      const int cnt = len - rb;
-      if (cnt >= 32) {
-#pragma unroll
-        for (int k = 0; k < 32; ++k) s = xadd(s, __shfl_sync(0xffffffffu, cur, k));
-      } else if (cnt > 0) {
-        for (int k = 0; k < cnt; ++k) s = xadd(s, __shfl_sync(0xffffffffu, cur, k));
-      }
-    }
-  }
-  return s;
-}
-
-// Same, but loads bypass L1 (products written by other threads/CTAs).
-__device__ __forceinline__ double chain_sum_cg(const double* __restrict__ p, int len) {
-  double s = 0.0;
-  constexpr int B = 16;
-  int t = 0;
-  double buf[B];
-  for (; t + B <= len; t += B) {
-#pragma unroll
-    for (int k = 0; k < B; ++k) buf[k] = __ldcg(p + t + k);
-#pragma unroll
-    for (int k = 0; k < B; ++k) s = xadd(s, buf[k]);
-  }
-  for (; t < len; ++t) s = xadd(s, __ldcg(p + t));
   return s;
 }
 

@@ -6,7 +6,7 @@
 #include <cstdlib>
 #include <vector>
 
-#include "common.cuh"
+#include "probe_util.cuh"
 #include "gemv.cuh"
 
 using namespace alnnls;
