@@ -88,8 +88,8 @@ __global__ void __launch_bounds__(512, 1)
   const int row0 = blockIdx.x * rpc;
   const int nrows = max(0, min(rows - row0, rpc));
   RowRing ring;
-  ring_setup(ring, smem, kRingSmemBytes, nrows);
-  gemv_rows(ring, M, ld, row0, nrows, list, vals, len, y);
+  ring_setup(ring, smem, kRingSmemBytes, nrows, ring_seg(nrows), 12);
+  gemv_rows(ring, M + row0, ld, false, row0, nrows, list, vals, len, y);
 }
 
 // LDG direct: each consumer thread streams its row's entries with deep register prefetch.
