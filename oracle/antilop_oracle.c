@@ -551,13 +551,13 @@ int oracle_solve_anti_accelerated(uint64_t d, uint64_t n, const double* A, const
 static int nnls_pipeline(uint64_t d, uint64_t n, const double* A, const double* b,
                          const alnnls_config* cfg, oracle_out* out, inner_solver solve) {
   const double t0 = now_s();
-  double* H = (double*)malloc(sizeof(double) * (n * n ? n * n : 1));
+  double* H = (double*)malloc(sizeof(double) * (n > 0 ? n * n : 1));
   double* h = (double*)malloc(sizeof(double) * (n ? n : 1));
   oracle_gram(d, n, A, H);
   oracle_transpose_matvec(d, n, A, b, h);
   for (uint64_t i = 0; i < n; ++i) h[i] = -h[i];
 
-  double* Q = (double*)malloc(sizeof(double) * (n * n ? n * n : 1));
+  double* Q = (double*)malloc(sizeof(double) * (n > 0 ? n * n : 1));
   double* q = (double*)malloc(sizeof(double) * (n ? n : 1));
   uint64_t* retained = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
   double* scale = (double*)malloc(sizeof(double) * (n ? n : 1));

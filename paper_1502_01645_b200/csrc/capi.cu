@@ -35,7 +35,7 @@ struct alnnls_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D of the host-buffer entries (overlapped uploads)
   cudaEvent_t ev[6] = {};
-  cudaEvent_t up[8] = {};             // row-block upload events
+  cudaEvent_t up[16] = {};            // row-block upload events (kMaxUpBlocks)
   std::string err;
 
   DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
@@ -312,7 +312,7 @@ int streamk_buffers(alnnls_ctx* ctx, SetupArgs& sa, int mode) {
   sa.sk_part = nullptr;
   sa.sk_flag = nullptr;
   if (sa.sk_ctas > 0) {
-    sa.sk_part = ENSURE(double, skp, (size_t)sa.sk_ctas * 32 * 512);
+    sa.sk_part = ENSURE(double, skp, (size_t)sa.sk_ctas * ALNNLS_GRAM_TILE_DOUBLES);
     sa.sk_flag = ENSURE(int, skf, sa.sk_ctas);
   }
   return ALNNLS_OK;
@@ -490,10 +490,27 @@ int device_check_finite(alnnls_ctx* ctx, std::initializer_list<FiniteArg> args) 
 // Host-buffer solve_nnls with the upload of A overlapped with the Gram: A is
 // copied in row blocks on the copy stream, and each block's Gram contribution
 // is computed as soon as it lands by continuing every tile's chain states over
-// its rows (setup.cu syrk_rowblock_kernel; A^T b chains likewise), so the
-// result is bitwise the one-shot Gram. The finiteness check runs after the last
-// block (results are discarded on failure, as if validated first).
-constexpr int kUpBlocks = 4;
+// its rows (stream-K SYRK with tpin/tpout; A^T b chains likewise), so the
+// result is bitwise the one-shot Gram. Blocks grow geometrically: the first is
+// small (the only upload not hidden), later ones ~1.75x the previous, since a
+// row's Gram work takes ~1.8x its PCIe upload time. The finiteness check runs
+// after the last block (results are discarded on failure, as if validated first).
+constexpr int kMaxUpBlocks = 16;  // ctx->up
+int upload_blocks(uint64_t d, uint64_t* edges) {
+  uint64_t sz = d / 32 < 256 ? 256 : (d / 32 + 15) / 16 * 16;
+  int nb = 0;
+  uint64_t r = 0;
+  edges[0] = 0;
+  while (r < d && nb < kMaxUpBlocks) {
+    uint64_t r1 = r + sz;
+    if (nb == kMaxUpBlocks - 1 || r1 + sz / 2 >= d) r1 = d;  // fold a small remainder in
+    edges[++nb] = r1;
+    r = r1;
+    sz = (sz * 7 / 4 + 15) / 16 * 16;
+  }
+  return nb;
+}
+
 int run_nnls_overlapped(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, const double* b,
                         const alnnls_config* cfg, alnnls_summary* out) {
   int st__ = ALNNLS_OK;
@@ -502,7 +519,7 @@ int run_nnls_overlapped(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A
   double* dA = ENSURE(double, A, lda * n);
   double* db = ENSURE(double, b, d);
   const uint64_t T = gram_tiles(n);
-  const uint64_t TD = 32 * 512;
+  const uint64_t TD = ALNNLS_GRAM_TILE_DOUBLES;
   double* H = ENSURE(double, H, n * n);
   double* st_buf = ENSURE(double, tst, 2 * T * TD);  // ping-pong tile chain states
   double* hb = ENSURE(double, hvec, 2 * n + 8);       // ping-pong A^T b chain states
@@ -511,15 +528,15 @@ int run_nnls_overlapped(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A
   CK(cudaMemcpyAsync(db, b, sizeof(double) * d, cudaMemcpyHostToDevice, cs));
   const double* pin = nullptr;
   const double* hin = nullptr;
-  for (int k = 0; k < kUpBlocks; ++k) {
-    const uint64_t r0 = d * k / kUpBlocks, r1 = d * (k + 1) / kUpBlocks;
-    if (r1 > r0)
-      CK(cudaMemcpy2DAsync(dA + r0, lda * sizeof(double), A + r0, d * sizeof(double),
-                           (r1 - r0) * sizeof(double), n, cudaMemcpyHostToDevice, cs));
+  uint64_t edges[kMaxUpBlocks + 1];
+  const int nblk = upload_blocks(d, edges);
+  for (int k = 0; k < nblk; ++k) {
+    const uint64_t r0 = edges[k], r1 = edges[k + 1];
+    CK(cudaMemcpy2DAsync(dA + r0, lda * sizeof(double), A + r0, d * sizeof(double),
+                         (r1 - r0) * sizeof(double), n, cudaMemcpyHostToDevice, cs));
     CK(cudaEventRecord(ctx->up[k], cs));
     CK(cudaStreamWaitEvent(s, ctx->up[k], 0));
-    if (r1 == r0) continue;
-    const bool last = r1 == d;
+    const bool last = k == nblk - 1;
     SetupArgs sa{};
     sa.A = dA + r0;
     sa.lda = lda;
@@ -536,7 +553,7 @@ int run_nnls_overlapped(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A
       CK(launch_syrk_rowblock(sa, 0, (int)T, pin, pout, s));
     }
     double* hout = hb + (size_t)(k & 1) * (n + 4);
-    CK(launch_coldot(dA + r0, lda, (int)(r1 - r0), (int)n, db + r0, hout, s, hin));
+    CK(launch_atb_chain(dA + r0, lda, (int)(r1 - r0), (int)n, db + r0, hin, hout, s));
     pin = pout;
     hin = hout;
   }
@@ -1048,7 +1065,8 @@ int alnnls_transpose_matvec(alnnls_ctx* ctx, uint64_t rows, uint64_t cols, const
   double* dv = ENSURE(double, b, rows);
   double* dy = ENSURE(double, ax, cols);
   CK(cudaMemcpyAsync(dv, v, sizeof(double) * rows, cudaMemcpyHostToDevice, ctx->stream));
-  CK(launch_coldot(static_cast<double*>(ctx->A.p), ld, (int)rows, (int)cols, dv, dy, ctx->stream));
+  CK(launch_atb_chain(static_cast<double*>(ctx->A.p), ld, (int)rows, (int)cols, dv, nullptr, dy,
+                      ctx->stream));
   return copy_out(ctx, y, dy, sizeof(double) * cols);
 }
 
@@ -1273,7 +1291,7 @@ int alnnls_atb_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const
   if (rc) return rc;
   if (!dA || !db || !dout || rows < 1 || n < 1 || lda < rows)
     return set_err(ctx, ALNNLS_EINVAL, "atb_rowblock: bad argument");
-  CK(launch_coldot(dA, lda, (int)rows, (int)n, db, dout, ctx->stream, dpin));
+  CK(launch_atb_chain(dA, lda, (int)rows, (int)n, db, dpin, dout, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return ALNNLS_OK;
 }

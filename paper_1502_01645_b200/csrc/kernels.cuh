@@ -136,6 +136,10 @@ struct SetupArgs {
 // CTAs for the stream-K exact SYRK of this shape (0: use one CTA per tile).
 int syrk_streamk_ctas(const SetupArgs& s, int mode, int sm_count);
 cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream);
+// A^T b chains over `rows` rows of A, continuing from atb0 (nullptr: +0); also
+// transpose_matvec, y_j = sum_i M[i,j] v_i (linalg.hpp:209-219).
+cudaError_t launch_atb_chain(const double* A, uint64_t lda, int rows, int n, const double* b,
+                             const double* atb0, double* atb, cudaStream_t stream);
 cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream);
 // mode 0: write H (and -A^T b into hvec when b != nullptr); mode 1: fused rescale into Q, q.
 cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream);
@@ -168,12 +172,9 @@ cudaError_t launch_residual(const double* ax, const double* b, int d, double* pr
 // Compaction of the support of x (x_j != 0, ascending) for matvec(A, x).
 cudaError_t launch_support(const double* x, int n, uint32_t* list, double* vals, int* len,
                            cudaStream_t stream);
-// transpose_matvec: y_j = sum_i M[i,j] v_i (linalg.hpp:209-219)
-cudaError_t launch_coldot(const double* M, uint64_t ld, int rows, int cols, const double* v,
-                          double* y, cudaStream_t stream, const double* y0 = nullptr);
 // Multi-GPU exact Gram by row blocks (setup.cu syrk_rowblock_kernel): tile count,
 // and continuation of tiles [tile_lo, tile_lo + ntiles) over the rows of s.A
-// from chain states pin to pout ([ntiles][32][512]; pout == nullptr writes s.H).
+// from chain states pin to pout ([ntiles][ALNNLS_GRAM_TILE_DOUBLES]; pout == nullptr writes s.H).
 uint64_t gram_tiles(uint64_t n);
 cudaError_t launch_syrk_rowblock(const SetupArgs& s, int tile_lo, int ntiles, const double* pin,
                                  double* pout, cudaStream_t stream);

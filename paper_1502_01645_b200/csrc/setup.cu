@@ -9,9 +9,10 @@
 // output (i <= j) is ONE chain over k ascending of rounded products
 // (__dmul_rn then __dadd_rn), exactly the reference's `s += ci[k]*cj[k]`. The
 // b column makes column n of the output A^T b bitwise (products commute,
-// same k order). On B200 the DMUL+DADD pair issues at the DFMA rate
-// (measured: 36 TFLOP/s useful vs 34 DFMA, 37 DMMA), so the exact profile is
-// not capped at half of the fp64 peak. The epilogue writes Q = H/(D_i D_j)
+// same k order). DMUL, DADD and DFMA each issue at 64 lanes/clk/SM on B200,
+// so one DMUL + one DADD per product caps the exact profile at 18.5 TFLOP/s
+// useful, half the 37 TFLOP/s DMMA peak (profiles/r01_fp64_probe.txt). The
+// epilogue writes Q = H/(D_i D_j)
 // (Q_ii = 1) and q = (-h)/D directly: H is never materialised.
 #include "common.cuh"
 #include "gemv.cuh"
@@ -26,9 +27,14 @@ constexpr int BM = 128;   // output tile (square)
 #define ALNNLS_SYRK_BK 16
 #endif
 constexpr int BK = ALNNLS_SYRK_BK;  // k slab
-constexpr int NT = 512;   // 16 warps: 4 per scheduler to hide the 8-cycle DMUL->DADD latency
+#ifndef ALNNLS_SYRK_TC
+#define ALNNLS_SYRK_TC 4
+#endif
+constexpr int TC = ALNNLS_SYRK_TC;       // thread tile 8 rows x TC cols
+constexpr int NT = BM * BM / (8 * TC);  // TC=4: 512 threads (4 warps per scheduler)
+constexpr int TS = BM * BM;             // doubles of one tile's chain states ([8*TC][NT])
 constexpr int LDS = BM + 2;  // padded smem row (doubles): 16B-aligned rows, <=2-way store conflicts
-// thread tile 8 rows x 4 cols: rows 2tx+(r&1)+32(r>>1), cols 2ty+(c&1)+64(c>>1)
+// thread tile 8 rows x TC cols: rows 2tx+(r&1)+32(r>>1), cols 2ty+(c&1)+(256/TC)(c>>1)
 // (each 16B shared load of a row pair is conflict-free across the 16 tx lanes)
 
 // Upper-triangular tile index -> (ti, tj), ti <= tj (tj-major enumeration).
@@ -40,7 +46,10 @@ __device__ __forceinline__ void tri_tile(int t, int& ti, int& tj) {
   ti = t - j * (j + 1) / 2;
 }
 
-constexpr int kStages = 3;
+#ifndef ALNNLS_SYRK_STAGES
+#define ALNNLS_SYRK_STAGES 3
+#endif
+constexpr int kStages = ALNNLS_SYRK_STAGES;  // cp.async slab ring depth
 constexpr size_t kSyrkSmem = (size_t)kStages * 2 * BK * LDS * sizeof(double);
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, uint32_t src_bytes) {
@@ -65,7 +74,7 @@ __device__ __forceinline__ void tile_of(const SetupArgs& s, int mode, int t, int
 }
 
 // k slabs [kb0, kb1) of output tile (ti, tj). The 32 accumulators of each
-// thread start from +0, or from a partial chain state `pin` ([32][NT]) that
+// thread start from +0, or from a partial chain state `pin` ([8*TC][NT]) that
 // another CTA left after slabs [0, kb0); they end in the epilogue, or are
 // stored to `pout` for the CTA that continues the chain. Either way every
 // output is ONE chain over k ascending, bit for bit the same as one CTA doing
@@ -106,11 +115,12 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
     }
   };
 
-  double acc[8][4];
+  double acc[8][TC];
 #pragma unroll
   for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = pin ? __ldcg(pin + (size_t)(r * 4 + c) * NT + threadIdx.x) : 0.0;
+    for (int c = 0; c < TC; ++c)
+      acc[r][c] = pin ? __ldcg(pin + (size_t)(r * TC + c) * NT + threadIdx.x) : 0.0;
 
   __syncthreads();  // the previous piece's last slab buffers are no longer read
 #pragma unroll
@@ -126,7 +136,7 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
     const int buf = (kb - kb0) % kStages;
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      double a[8], b[4];
+      double a[8], b[TC];
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const double2 v = *reinterpret_cast<const double2*>(&As[buf][kk][2 * tx + 32 * h]);
@@ -134,19 +144,19 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
         a[2 * h + 1] = v.y;
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][kk][2 * ty + 64 * h]);
+      for (int h = 0; h < TC / 2; ++h) {
+        const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][kk][2 * ty + (256 / TC) * h]);
         b[2 * h] = v.x;
         b[2 * h + 1] = v.y;
       }
       // each output: one chain over k ascending, rounded product then rounded sum
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        double p[4];
+        double p[TC];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) p[c] = xmul(a[r], b[c]);
+        for (int c = 0; c < TC; ++c) p[c] = xmul(a[r], b[c]);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = xadd(acc[r][c], p[c]);
+        for (int c = 0; c < TC; ++c) acc[r][c] = xadd(acc[r][c], p[c]);
       }
     }
   }
@@ -156,7 +166,7 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) pout[(size_t)(r * 4 + c) * NT + threadIdx.x] = acc[r][c];
+      for (int c = 0; c < TC; ++c) pout[(size_t)(r * TC + c) * NT + threadIdx.x] = acc[r][c];
     return;
   }
   // epilogue: upper triangle only, mirrored (exact symmetry, linalg.hpp:169-170)
@@ -164,8 +174,8 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
   for (int r = 0; r < 8; ++r) {
     const int i = i0 + 2 * tx + (r & 1) + 32 * (r >> 1);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = j0 + 2 * ty + (c & 1) + 64 * (c >> 1);
+    for (int c = 0; c < TC; ++c) {
+      const int j = j0 + 2 * ty + (c & 1) + (256 / TC) * (c >> 1);
       const double v = acc[r][c];
       if (mode == 2) {  // q_b of RHS column j: (-(A^T b_j))_{j_b} / D_b (nnls.hpp:79, :133-134)
         if (i >= s.n || j >= s.nrhs) continue;
@@ -218,12 +228,12 @@ __global__ void __launch_bounds__(NT, 1) syrk_streamk_kernel(SetupArgs s, int mo
   if (u0 >= u1) return;
   const int t0 = (int)(u0 / nk), k0 = (int)(u0 % nk);
   const int t1 = (int)((u1 - 1) / nk), k1 = (int)((u1 - 1) % nk) + 1;
-  double* my_part = s.sk_part + (size_t)blockIdx.x * 32 * NT;
+  double* my_part = s.sk_part + (size_t)blockIdx.x * TS;
   int ti, tj;
   // tile chain states carried in from earlier row blocks / out to later ones
-  // (row-block continuation, s.tpin / s.tpout, [tiles][32][NT]; nullptr: none)
-  auto tin = [&](int t) { return s.tpin ? s.tpin + (size_t)t * 32 * NT : nullptr; };
-  auto tout = [&](int t) { return s.tpout ? s.tpout + (size_t)t * 32 * NT : nullptr; };
+  // (row-block continuation, s.tpin / s.tpout, [tiles][8*TC][NT]; nullptr: none)
+  auto tin = [&](int t) { return s.tpin ? s.tpin + (size_t)t * TS : nullptr; };
+  auto tout = [&](int t) { return s.tpout ? s.tpout + (size_t)t * TS : nullptr; };
   // 1. trailing partial tile: slabs [0, k1) of t1, handed to the next CTA
   if (k1 < nk) {
     tile_of(s, mode, t1, ti, tj);
@@ -253,7 +263,7 @@ __global__ void __launch_bounds__(NT, 1) syrk_streamk_kernel(SetupArgs s, int mo
     }
     __syncthreads();
     tile_of(s, mode, t0, ti, tj);
-    syrk_piece(s, mode, syrk_sm, ti, tj, k0, nk, s.sk_part + (size_t)(blockIdx.x - 1) * 32 * NT,
+    syrk_piece(s, mode, syrk_sm, ti, tj, k0, nk, s.sk_part + (size_t)(blockIdx.x - 1) * TS,
                tout(t0));
   }
 }
@@ -282,7 +292,7 @@ constexpr size_t kColChainSmem = (2 * 32 * kCcLD + 2 * kCcKT) * sizeof(double);
 
 __global__ void __launch_bounds__(256, 1)
     colchain_kernel(const double* A, uint64_t lda, int d, int n, const double* b, double* diag,
-                    double* atb) {
+                    double* atb, const double* atb0) {
   extern __shared__ __align__(16) double cc_sm[];
   double* tile = cc_sm;                    // [2][32][kCcLD]
   double* btile = cc_sm + 2 * 32 * kCcLD;  // [2][kCcKT]
@@ -300,7 +310,8 @@ __global__ void __launch_bounds__(256, 1)
     }
     if (b) btile[buf * kCcKT + kk] = k < d ? __ldg(b + k) : 0.0;
   };
-  double sd = 0.0, sb = 0.0;
+  // atb0: A^T b chain states after earlier row blocks (host-buffer overlap)
+  double sd = 0.0, sb = atb0 && c0 + lane < n ? atb0[c0 + lane] : 0.0;
   if (warp > 0) load(0, 0);
   __syncthreads();
   for (int st = 0; st < nst; ++st) {
@@ -414,28 +425,6 @@ __global__ void support_kernel(const double* x, int n, uint32_t* list, double* v
 }
 
 // y_j = sum_i M[i, j] v_i, one ascending chain per column (linalg.hpp:209-219).
-__global__ void coldot_kernel(const double* M, uint64_t ld, int rows, int cols, const double* v,
-                              double* y, const double* y0) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  const double* p = M + (size_t)c * ld;
-  double acc = y0 ? y0[c] : 0.0;  // y0: chain states after earlier row blocks
-  int k = 0;
-  constexpr int B = 8;
-  for (; k + B <= rows; k += B) {
-    double a[B], w[B];
-#pragma unroll
-    for (int t = 0; t < B; ++t) {
-      a[t] = __ldg(p + k + t);
-      w[t] = __ldg(v + k + t);
-    }
-#pragma unroll
-    for (int t = 0; t < B; ++t) acc = xmac(acc, a[t], w[t]);
-  }
-  for (; k < rows; ++k) acc = xmac(acc, __ldg(p + k), __ldg(v + k));
-  y[c] = acc;
-}
-
 __global__ void add_kernel(const double* y, const double* q, double* g, int m) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m) g[i] = xadd(y[i], q[i]);
@@ -504,7 +493,23 @@ cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream) {
     attr = true;
   }
   colchain_kernel<<<(s.n + 31) / 32, 256, kColChainSmem, stream>>>(
-      s.A, s.lda, s.d, s.n, s.b, s.diag, s.b ? s.hvec_scratch : nullptr);
+      s.A, s.lda, s.d, s.n, s.b, s.diag, s.b ? s.hvec_scratch : nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_atb_chain(const double* A, uint64_t lda, int rows, int n, const double* b,
+                             const double* atb0, double* atb, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(colchain_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kColChainSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  colchain_kernel<<<(n + 31) / 32, 256, kColChainSmem, stream>>>(A, lda, rows, n, b, nullptr, atb,
+                                                                 atb0);
   return cudaGetLastError();
 }
 
@@ -526,14 +531,14 @@ cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream) {
 // [tile_lo, tile_lo + gridDim.x) over the block's rows s.A[0, s.d), starting
 // from the chain states `pin` the previous row blocks left (nullptr: start of
 // the chains) and ending in `pout` (nullptr: finish, write H). The states of a
-// tile are the kernel's thread layout [32][NT]; feeding the row blocks in order
+// tile are the kernel's thread layout [8*TC][NT]; feeding the row blocks in order
 // is the reference's single ascending-k chain per entry.
 __global__ void __launch_bounds__(NT, 1) syrk_rowblock_kernel(SetupArgs s, int tile_lo,
                                                               const double* pin, double* pout) {
   extern __shared__ __align__(16) double syrk_sm[];
   int ti, tj;
   tile_of(s, 0, tile_lo + (int)blockIdx.x, ti, tj);
-  const size_t off = (size_t)blockIdx.x * 32 * NT;
+  const size_t off = (size_t)blockIdx.x * TS;
   syrk_piece(s, 0, syrk_sm, ti, tj, 0, (s.d + BK - 1) / BK, pin ? pin + off : nullptr,
              pout ? pout + off : nullptr);
 }
@@ -614,12 +619,6 @@ cudaError_t launch_support(const double* x, int n, uint32_t* list, double* vals,
   return cudaGetLastError();
 }
 
-cudaError_t launch_coldot(const double* M, uint64_t ld, int rows, int cols, const double* v,
-                          double* y, cudaStream_t stream, const double* y0) {
-  if (cols <= 0) return cudaSuccess;
-  coldot_kernel<<<(cols + 127) / 128, 128, 0, stream>>>(M, ld, rows, cols, v, y, y0);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_add(const double* y, const double* q, double* g, int m, cudaStream_t stream) {
   if (m <= 0) return cudaSuccess;

@@ -224,6 +224,132 @@ __global__ void k_i(double* out, long long* cyc, int seg, int S) {
   if (threadIdx.x == 0) *cyc = c1 - c0;
 }
 
+
+// (k) = (d) with the per-stage wait replaced by a poll of a plain shared-memory
+// flag (what a relay warp that did the mbarrier wait would publish).
+__device__ __forceinline__ uint32_t lds_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_volatile(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+template <int KIND>
+__global__ void k_k(double* out, long long* cyc, int seg, int S) {
+  extern __shared__ double sm[];
+  __shared__ uint32_t flag[12];
+  double* col = sm;
+  double* v = sm + G * SEG;
+  for (int e = threadIdx.x; e < G * SEG + G; e += blockDim.x) sm[e] = 1.0 + e * 1e-9;
+  if (threadIdx.x < 12) flag[threadIdx.x] = 1;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int tt = threadIdx.x % seg;
+  double acc = 0.0;
+  const long long c0 = clock64();
+  constexpr int H = 32;
+  double pa[H], pb[H];
+#pragma unroll
+  for (int l = 0; l < H; ++l) pa[l] = xmul(col[l * seg + tt], v[l]);
+  for (int q = 0; q < 2 * NST - 1; q += 2) {
+#pragma unroll
+    for (int l = 0; l < H; ++l) {
+      pb[l] = xmul(col[(H + l) * seg + tt], v[H + l]);
+      acc = xadd(acc, pa[l]);
+    }
+    const int st = ((q + 2) / 2) % S;
+    if (KIND == 0) { while (lds_acquire(&flag[st % 12]) != 1u) {} }
+    else { while (lds_volatile(&flag[st % 12]) != 1u) {} }
+#pragma unroll
+    for (int l = 0; l < H; ++l) {
+      pa[l] = xmul(col[l * seg + tt], v[l]);
+      acc = xadd(acc, pb[l]);
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < H; ++l) acc = xadd(acc, pa[l]);
+  const long long c1 = clock64();
+  out[threadIdx.x] = acc;
+  if (threadIdx.x == 0) *cyc = c1 - c0;
+}
+
+// (m) dependent latency of one mbarrier phase check on a completed phase
+__global__ void k_m(double* out, long long* cyc, int kind) {
+  __shared__ uint64_t bar[2];
+  if (threadIdx.x == 0) { mbar_init(&bar[0], 1); fence_mbar_init(); }
+  __syncthreads();
+  if (threadIdx.x == 0) mbar_arrive(&bar[0]);
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const long long c0 = clock64();
+  uint32_t par = 0;
+  for (int i = 0; i < 1000; ++i) {
+    if (kind == 0) { par ^= mbar_try_wait(&bar[0], 0) ? 0u : 1u; }
+    else { par ^= mbar_test(&bar[0], par) ? 0u : 1u; }
+  }
+  const long long c1 = clock64();
+  out[threadIdx.x] = par;
+  if (threadIdx.x == 0) *cyc = c1 - c0;
+}
+
+
+// (n) = (d) with the mbarrier waits batched: before every W-th stage the
+// consumer waits for the next W stages at once, then runs them straight-line.
+template <int W>
+__global__ void k_n(double* out, long long* cyc, int seg, int S) {
+  extern __shared__ double sm[];
+  __shared__ uint64_t bar[12];
+  double* col = sm;
+  double* v = sm + G * SEG;
+  for (int e = threadIdx.x; e < G * SEG + G; e += blockDim.x) sm[e] = 1.0 + e * 1e-9;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 12; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 12; ++i) mbar_arrive(&bar[i]);
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int tt = threadIdx.x % seg;
+  double acc = 0.0;
+  const long long c0 = clock64();
+  constexpr int H = 32;
+  double pa[H], pb[H];
+  for (int w = 0; w < W; ++w) mbar_wait(&bar[w % 12], 0);
+#pragma unroll
+  for (int l = 0; l < H; ++l) pa[l] = xmul(col[l * seg + tt], v[l]);
+  for (int s0 = 0; s0 < NST; s0 += W) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const int s = s0 + w;
+      if (w == W - 1 && s + 1 < NST)
+        for (int x = 0; x < W; ++x) mbar_wait(&bar[((s + 1 + x) % S) % 12], 0);
+#pragma unroll
+      for (int l = 0; l < H; ++l) {
+        pb[l] = xmul(col[(H + l) * seg + tt], v[H + l]);
+        acc = xadd(acc, pa[l]);
+      }
+      if (s + 1 < NST) {
+#pragma unroll
+        for (int l = 0; l < H; ++l) {
+          pa[l] = xmul(col[l * seg + tt], v[l]);
+          acc = xadd(acc, pb[l]);
+        }
+      } else {
+#pragma unroll
+        for (int l = 0; l < H; ++l) acc = xadd(acc, pb[l]);
+      }
+    }
+  }
+  const long long c1 = clock64();
+  out[threadIdx.x] = acc;
+  if (threadIdx.x == 0) *cyc = c1 - c0;
+}
+
 int main() {
   double* out;
   long long* cyc;
@@ -252,5 +378,16 @@ int main() {
   rd(k_d<true, 0, 1>, "(h) runtime seg + test_wait spin");
   rd(k_i<false>, "(i) test one stage ahead");
   rd(k_i<true>, "(j) test ahead, no memory clobber");
+  rd(k_n<2>, "(n2) waits batched per 2 stages");
+  rd(k_n<4>, "(n4) waits batched per 4 stages");
+  rd(k_n<8>, "(n8) waits batched per 8 stages");
+  rd(k_k<0>, "(k) shared flag poll, ld.acquire");
+  rd(k_k<1>, "(l) shared flag poll, ld.volatile");
+  for (int kind = 0; kind < 2; ++kind) {
+    k_m<<<1, 32>>>(out, cyc, kind);
+    k_m<<<1, 32>>>(out, cyc, kind);
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("(m%d) mbarrier %s dependent latency: %.1f cycles\n", kind, kind ? "test_wait" : "try_wait", h / 1000.0);
+  }
   return 0;
 }

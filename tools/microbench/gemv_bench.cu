@@ -33,7 +33,7 @@ int main(int argc, char** argv) {
     const int L = hl.size();
     int runs = 0; for (int t = 0; t < L; ++t) if (t == 0 || hl[t] != hl[t-1] + 1) ++runs;
     CK(cudaMemcpy(list, hl.data(), L * 4, cudaMemcpyHostToDevice));
-    for (int maxw : {12}) {
+    for (int maxw : {4, 5, 12}) {
       for (int rep = 0; rep < 3; ++rep) {
         cudaEventRecord(e0);
         for (int it = 0; it < 20; ++it) k_blocked<<<nb, 384, kRingSmemBytes>>>(Q, m, R, list, vals, L, y, maxw);
