@@ -14,7 +14,7 @@
 //        f, stop tests, stall counter (nqp.hpp:257-275)                     -> barrier
 //   D/C  vector CTA: den chain, alpha (exact_step, nqp.hpp:162-173), candidate
 //        max(0, x - alpha g) and the changed set C (nqp.hpp:294-303)        -> barrier
-//   P2   row CTAs: gd = Q[:, C] delta_C (nqp.hpp:305)                       -> barrier
+//   P2   row CTAs: gd = Q[:, C] delta_C (nqp.hpp:305)        -> (own rows only)
 //   F/U  row CTAs: g_next = g + gd on own rows (ping-pong buffer, so doing it
 //        before the decision is safe); vector CTA: df chain (nqp.hpp:307),
 //        accept -> x[C] = cand, next passive mask from g + gd, trace record;
@@ -746,7 +746,9 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
     // ===== P2, speculative update, next passive lists ====================================
     const int cl = __ldcg(&a.ctrl->chg_len);
     if (!leader) gemv_rows(ring, qblk, R, true, row0, nrows, a.chg, a.dC, cl, a.gd);
-    grid.sync();  // B2
+    // no grid barrier after P2: row_apply reads only its own rows of gd, and the
+    // leader's df chain reads gdC only after B0
+    __syncthreads();
     if (leader && threadIdx.x == 0) phase_mark(L, 4);
     if (!leader) row_apply(a, RS, blk, row0, nrows, xb[xp], gb[xp], xb[xp ^ 1], gb[xp ^ 1], cl);
     grid.sync();  // B_cnt

@@ -17,7 +17,7 @@ for _ in range(3):
 sm = s.last_summary()
 it = sm.iterations
 ph = s.phase_times()
-names = ["A: P1 || chains+stop", "B1 wait", "den", "changed", "P2+B2", "apply+Bcnt", "lists+B0", "-"]
+names = ["A: P1 || chains+stop", "B1 wait", "den", "changed", "-", "P2+apply+Bcnt", "lists+B0", "-"]
 print(name, "iters", it, "loop_ms", sm.t_loop_s * 1e3, "us/iter", sm.t_loop_s * 1e6 / max(1, it))
 for nm, v in zip(names, ph):
     print(f"  {nm:24s} {v * 1e6 / max(1, it):7.2f} us/iter")
