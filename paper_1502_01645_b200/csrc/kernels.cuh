@@ -28,6 +28,7 @@ struct LoopCtrl {
   int act;          // phase-A decision: continue / stop / roll back the pending step
   int state2;       // phase-B decision: P2 / no move / stop
   int g_parity;     // which gradient buffer holds the maintained gradient
+  unsigned int p1_done;  // row CTAs that finished P1 (monotonic within a launch)
   unsigned long long phase_ns[8];  // accumulated leader-side phase times
 };
 

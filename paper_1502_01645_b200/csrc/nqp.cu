@@ -50,6 +50,7 @@ struct LeaderState {
   int nonfinite;
   int tries;
   int mask_len;
+  int act;  // phase-A decision (LoopAct), for the whole vector CTA
   unsigned long long t_mark;
   unsigned long long ph[8];
   double red[kWarps];
@@ -541,6 +542,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
     a.ctrl->mult_total = 0;
     a.ctrl->numeric_failure = 0;
     a.ctrl->g_parity = 0;
+    a.ctrl->p1_done = 0;
     L.best_gbs = __longlong_as_double(0x7ff0000000000000LL);  // +inf
     L.since_best = 0;
     L.t_mark = t0;
@@ -555,12 +557,19 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
   }
 
   unsigned long long k = 0;  // iteration whose stop test runs next (vector CTA)
+  unsigned int npass = 0;    // phase-A passes (identical in every CTA)
   for (;;) {
     // ===== phase A: P1 (row CTAs) || stop-test chains + pending df (vector CTA) =====
+    ++npass;
     if (!leader) {
       // u = Q g_bar over own rows, also compacted to the passive list for den
       gemv_rows(ring, qblk, R, true, row0, nrows, ls[lp].mask, ls[lp].gP, ml_l[lp], a.u,
                 RS.lpos[lp], a.uP);
+      __syncthreads();
+      if (threadIdx.x == 0) {  // publish: uP of own rows is complete (release)
+        __threadfence();
+        atomicAdd(&a.ctrl->p1_done, 1u);
+      }
     } else {
       __shared__ int s_ml, s_bad;
       __shared__ double s_mn;
@@ -655,21 +664,29 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
         L.elapsed = el;
         L.mask_len = ml;
         a.ctrl->act = act;
+        L.act = act;
         phase_mark(L, 0);
         __threadfence();
+        // the den chain needs every row CTA's P1 (no grid barrier here: the row
+        // CTAs go straight on to B_C, where they learn act and the changed set)
+        if (act == kActCont) {
+          const unsigned int target = npass * (unsigned int)nblk;
+          while (ld_acquire_u32(&a.ctrl->p1_done) < target) {
+          }
+        }
+        phase_mark(L, 1);
       }
+      __syncthreads();
     }
-    grid.sync();  // B1
-    const int act = __ldcg(&a.ctrl->act);  // after the grid barrier: L2 read, no sys-scope volatile
-    if (act == kActStop) break;
-    if (act == kActRollback) {  // back to the state before the rejected step
+    // rows: act is read after B_C; the leader acts on it now
+    int act = leader ? L.act : 0;
+    if (leader && act == kActRollback) {  // back to the state before the rejected step
       xp ^= 1;
       lp ^= 1;
     }
-    if (leader && threadIdx.x == 0) phase_mark(L, 1);
 
     // ===== phase B (vector CTA): den chain, alpha, changed set ==========================
-    if (leader) {
+    if (leader && act != kActStop) {
       const ListSet cur = ls[lp];
       __shared__ int s_zc;
       if (act == kActCont) {
@@ -739,6 +756,14 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
       }
     }
     grid.sync();  // B_C
+    if (!leader) {
+      act = __ldcg(&a.ctrl->act);  // after the grid barrier: L2 read, no sys-scope volatile
+      if (act == kActRollback) {
+        xp ^= 1;
+        lp ^= 1;
+      }
+    }
+    if (act == kActStop) break;
     const int st2 = __ldcg(&a.ctrl->state2);
     if (st2 == kS2Stop) break;
     if (st2 == kS2NoMove) continue;
