@@ -72,9 +72,60 @@ __device__ __forceinline__ void phase_mark(LeaderState& L, int idx) {
 }
 
 // One thread: s = ((s + p0) + p1) + ... over n products in shared memory.
-// Double-buffered register prefetch with 16-byte shared loads keeps the
-// dependent DADD (8 cycles on B200) the only thing on the critical path.
+// Two register blocks alternate (no register copies): the 16-byte loads of the
+// next block issue ahead of the current block's chain, so the dependent DADD
+// (8 cycles on B200) is the only thing on the critical path.
 __device__ __forceinline__ double smem_chain(double s, const double* __restrict__ p, int n) {
+  constexpr int B = 16;
+  int t = 0;
+  auto load = [&](double (&r)[B], int at) {
+#pragma unroll
+    for (int k = 0; k < B; k += 2) {
+      const double2 d = *reinterpret_cast<const double2*>(p + at + k);
+      r[k] = d.x;
+      r[k + 1] = d.y;
+    }
+  };
+  if (n >= 2 * B) {
+    double ra[B], rb[B];
+    load(ra, 0);
+    for (; t + 3 * B <= n; t += 2 * B) {
+      load(rb, t + B);
+#pragma unroll
+      for (int k = 0; k < B; ++k) s = xadd(s, ra[k]);
+      load(ra, t + 2 * B);
+#pragma unroll
+      for (int k = 0; k < B; ++k) s = xadd(s, rb[k]);
+    }
+    // ra holds [t, t + B); t + B <= n < t + 3B
+    if (t + 2 * B <= n) {
+      load(rb, t + B);
+#pragma unroll
+      for (int k = 0; k < B; ++k) s = xadd(s, ra[k]);
+#pragma unroll
+      for (int k = 0; k < B; ++k) s = xadd(s, rb[k]);
+      t += 2 * B;
+    } else {
+#pragma unroll
+      for (int k = 0; k < B; ++k) s = xadd(s, ra[k]);
+      t += B;
+    }
+  }
+  while (t < n) {  // < 2B left: blocks of B with predicated loads
+    double r[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) r[k] = t + k < n ? p[t + k] : 0.0;
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+      if (t + k < n) s = xadd(s, r[k]);
+    t += B;
+  }
+  return s;
+}
+
+// Variant with one register block copied forward (the phase-A chains run hidden
+// behind P1; this form keeps the loop kernel's row-CTA code faster, measured).
+__device__ __forceinline__ double smem_chain_db(double s, const double* __restrict__ p, int n) {
   constexpr int B = 16;
   int t = 0;
   if (n >= 2 * B) {
@@ -481,7 +532,7 @@ __device__ void leader_chains_var(double* sbuf, size_t sbuf_bytes, LeaderState& 
     if (warp < K) {
       if (lane == 0) {
         const int cnt = max(0, min(CH, len[warp] - c * CH));
-        s = smem_chain(s, sbuf + (size_t)(c & 1) * K * CH + (size_t)warp * CH, cnt);
+        s = smem_chain_db(s, sbuf + (size_t)(c & 1) * K * CH + (size_t)warp * CH, cnt);
       }
     } else if (c + 1 < nch) {
       produce(c + 1, (c + 1) & 1, K * 32);
