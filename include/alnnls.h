@@ -264,6 +264,23 @@ int alnnls_residual_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, 
                                     uint64_t lda, const double* db, const double* dx, double s_in,
                                     double* s_out);
 
+/* ---- multi-GPU setup by partial Grams + one allreduce --
+ * BASELINE.json configs[4] as written: every rank forms the partial Gram of its
+ * row block and the partials are summed with one allreduce (the caller's NCCL
+ * over NVLink), then one rank runs alnnls_solve_nnls_gram_device. Replaces the
+ * reference's gram (linalg.hpp:160-174) and transpose_matvec (linalg.hpp:209-
+ * 219) for a row block; the cross-rank sum order is NCCL's, so the result is
+ * within rounding of the reference's H, not bitwise (use the row-block chain
+ * entries above for that).
+ * dH (n x n, column-major, both triangles) = A_blk^T A_blk and, when db is not
+ * NULL, datb = A_blk^T b_blk. profile ALNNLS_PROFILE_FAST forms dH on the fp64
+ * tensor cores (needs lda even and 16-byte aligned dA), EXACT with the chain
+ * SYRK. dH and datb may be adjacent in one buffer so that a single allreduce
+ * moves both. Returns after the work is complete. */
+int alnnls_gram_partial_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const double* dA,
+                               uint64_t lda, const double* db, int profile, double* dH,
+                               double* datb);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,7 @@ EXPORTS = [
     "alnnls_timer_start", "alnnls_timer_stop", "alnnls_launch_count",
     "alnnls_gram_tiles", "alnnls_gram_rowblock_device", "alnnls_atb_rowblock_device",
     "alnnls_solve_nnls_gram_device", "alnnls_residual_rowblock_device",
+    "alnnls_gram_partial_device",
     "alnnls_solve_accelerated", "alnnls_solve_accelerated_device", "alnnls_solve_anti_accelerated",
     "alnnls_solve_anti_accelerated_device",
 ]
@@ -97,6 +98,7 @@ def load():
                                            C.POINTER(abi.Summary)], i32),
         "alnnls_residual_rowblock_device": ([vp, u64, u64, vp, u64, vp, vp, C.c_double,
                                              C.POINTER(C.c_double)], i32),
+        "alnnls_gram_partial_device": ([vp, u64, u64, vp, u64, vp, i32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -273,6 +273,14 @@ class Solver:
             self._raise(st)
         return self._nnls_result() if fetch else self._summary
 
+    def gram_partial_device(self, rows, n, A_ptr, lda, b_ptr, H_ptr, atb_ptr,
+                            profile=abi.PROFILE_FAST):
+        """Partial Gram A_blk^T A_blk (n x n, both triangles) and A_blk^T b_blk of one
+        row block, for the allreduce setup (rowblock.allreduce_setup)."""
+        self._check(self.lib.alnnls_gram_partial_device(
+            self.ctx, rows, n, C.c_void_p(A_ptr), lda, C.c_void_p(b_ptr) if b_ptr else None,
+            int(profile), C.c_void_p(H_ptr), C.c_void_p(atb_ptr) if atb_ptr else None))
+
     def residual_rowblock_device(self, rows, n, A_ptr, lda, b_ptr, x_ptr, s_in=0.0):
         out = C.c_double(0.0)
         self._check(self.lib.alnnls_residual_rowblock_device(

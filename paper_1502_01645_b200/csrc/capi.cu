@@ -1285,6 +1285,34 @@ int alnnls_gram_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, cons
   return ALNNLS_OK;
 }
 
+int alnnls_gram_partial_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const double* dA,
+                               uint64_t lda, const double* db, int profile, double* dH,
+                               double* datb) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!dA || !dH || rows < 1 || n < 1 || lda < rows || (db && !datb))
+    return set_err(ctx, ALNNLS_EINVAL, "gram_partial: bad argument");
+  if (profile != ALNNLS_PROFILE_EXACT && profile != ALNNLS_PROFILE_FAST)
+    return set_err(ctx, ALNNLS_EINVAL, "gram_partial: unknown profile");
+  int st__ = ALNNLS_OK;
+  SetupArgs sa{};
+  sa.A = dA;
+  sa.lda = lda;
+  sa.b = nullptr;
+  sa.d = (int)rows;
+  sa.n = (int)n;
+  sa.H = dH;
+  if (profile == ALNNLS_PROFILE_FAST && syrk_dmma_supported(sa, 0)) {
+    CK(launch_syrk_dmma(sa, 0, ctx->stream));
+  } else {
+    if ((rc = streamk_buffers(ctx, sa, 0))) return rc;
+    CK(launch_syrk(sa, 0, ctx->stream));
+  }
+  if (db) CK(launch_atb_chain(dA, lda, (int)rows, (int)n, db, nullptr, datb, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ALNNLS_OK;
+}
+
 int alnnls_atb_rowblock_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const double* dA,
                                uint64_t lda, const double* db, const double* dpin, double* dout) {
   int rc = check_ctx(ctx);

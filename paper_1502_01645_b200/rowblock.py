@@ -92,3 +92,33 @@ def chain_relay(dist, rank, world, state, compute, sync=None):
         dist.send(out, dst=rank + 1)
         return None
     return out
+
+
+def allreduce_setup(dist, world, n, compute, device):
+    """BASELINE.json configs[4] as written (SURVEY.md §8e variant (i)): every rank
+    forms the partial Gram of its row block and its partial A^T b, and the
+    partials are summed with ONE allreduce (NCCL over NVLink between GPUs, gloo
+    in the CPU tests). H and A^T b share one buffer so the single collective
+    moves both: n*n + n doubles (H is symmetric, so its n x n view is the same
+    in either storage order).
+
+    compute(H, atb) fills this rank's partials in place. Returns the summed
+    (H, atb) on every rank. The cross-rank sum order is the collective's, so H
+    equals the reference's gram only within rounding; the pipelined_gram path
+    is the bitwise one."""
+    buf = torch.empty(n * n + n, dtype=torch.float64, device=device)
+    H = buf[: n * n].view(n, n)
+    atb = buf[n * n:]
+    compute(H, atb)
+    if dist is not None and world > 1:
+        dist.all_reduce(buf)
+    return H, atb
+
+
+def allreduce_residual(dist, world, partial, device):
+    """residual_norm_sq (nnls.hpp:115-123) as the sum of the ranks' row-block
+    partial chains (one allreduce of one scalar)."""
+    t = torch.tensor([float(partial)], dtype=torch.float64, device=device)
+    if dist is not None and world > 1:
+        dist.all_reduce(t)
+    return float(t[0])

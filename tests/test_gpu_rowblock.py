@@ -71,3 +71,76 @@ def test_rowblock_solve_and_residual_bitwise(solver):
         s = solver.residual_rowblock_device(r1 - r0, A.shape[1], dA.data_ptr() + 8 * r0, A.shape[0],
                                             db.data_ptr() + 8 * r0, dx.data_ptr(), s)
     assert same_bits([s], [ref.residual_sq])
+
+
+# ---- configs[4] as written: partial Grams + one allreduce ------------------
+def _partials(solver, A, b, blocks, profile):
+    """Every block's partial [H | A^T b] through alnnls_gram_partial_device, summed in
+    rank order on the device (what the allreduce computes for this world size)."""
+    d, n = A.shape
+    dA = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    db = torch.from_numpy(b).cuda()
+    tot = torch.zeros(n * n + n, dtype=torch.float64, device="cuda")
+    for (r0, r1) in blocks:
+        buf = torch.empty(n * n + n, dtype=torch.float64, device="cuda")
+        solver.gram_partial_device(r1 - r0, n, dA.data_ptr() + 8 * r0, d, db.data_ptr() + 8 * r0,
+                                   buf.data_ptr(), buf.data_ptr() + 8 * n * n, profile=profile)
+        tot += buf
+    return dA, db, tot[: n * n].view(n, n), tot[n * n:]
+
+
+@pytest.mark.parametrize("profile", [0, 1])
+def test_gram_partial_one_block_matches_reference(solver, oracle, profile):
+    rng = np.random.default_rng(5)
+    A = np.asfortranarray(rng.standard_normal((640, 272)))
+    b = rng.standard_normal(640)
+    _, _, H, atb = _partials(solver, A, b, [(0, 640)], profile)
+    Href = oracle.gram(A)
+    Hg = H.cpu().numpy()
+    assert np.array_equal(Hg, Hg.T)
+    if profile == 0:  # one block = the reference chain, bit for bit
+        assert same_bits(Hg.reshape(-1, order="F"), Href.reshape(-1, order="F"))
+    else:             # DMMA: within rounding
+        assert np.max(np.abs(Hg - Href)) <= 1e-13 * 640 * np.max(np.abs(Href))
+    assert same_bits(atb.cpu().numpy(), oracle.transpose_matvec(A, b))
+
+
+@pytest.mark.parametrize("profile", [0, 1])
+def test_allreduce_setup_c5_law(solver, oracle, profile):
+    """SURVEY §8d c5 variant (i): Q, q within 1e-13 (relative) of rescale(gram) of the
+    reference; the loop bitwise against the reference loop run on the GPU's own Q, q;
+    the objective and a KKT certificate end to end."""
+    from paper_1502_01645_b200 import instances
+    inst = instances.make_config("c5", d=1600, n=640)
+    A, b = inst["A"], inst["b"]
+    d, n = A.shape
+    cfg = SolverConfig(epsilon=inst["epsilon"], stall_window=10**9)
+    blocks = row_split(d, 4)
+    dA, db, H, atb = _partials(solver, A, b, blocks, profile)
+    got = solver.solve_nnls_gram_device(n, H.data_ptr(), atb.data_ptr(), cfg)
+    mine = solver._scaled()
+    ref_sys = oracle.rescale(oracle.gram(A), -oracle.transpose_matvec(A, b))
+    Qr, qr = ref_sys["Q"], ref_sys["q"]
+    assert np.max(np.abs(mine["Q"] - Qr)) <= 1e-13 * max(1.0, np.max(np.abs(Qr)))
+    assert np.max(np.abs(mine["q"] - qr)) <= 1e-13 * max(1.0, np.max(np.abs(qr)))
+    loop = oracle.solve_nqp(mine["Q"], mine["q"], cfg.to_abi())
+    assert same_bits(got.inner.x, loop["x"])
+    assert got.inner.iterations() == loop["iterations"]
+    ref = oracle.solve_nnls(A, b, cfg.to_abi())
+    f_got, f_ref = got.inner.trace[-1].f, ref["trace"][-1]["f"]
+    assert abs(f_got - f_ref) <= 1e-10 * abs(f_ref)  # BASELINE objective bar
+    # KKT certificate (acceptance.cpp:253-256) in the scaled space
+    g = mine["Q"] @ got.inner.x + mine["q"]
+    x = got.inner.x
+    viol = np.max(np.where(x > 0, np.abs(g), np.maximum(0.0, -g)))
+    assert viol <= np.sqrt(cfg.epsilon) * (1 + np.linalg.norm(mine["q"]))
+    dx = torch.from_numpy(got.x).cuda()
+    parts = [solver.residual_rowblock_device(r1 - r0, n, dA.data_ptr() + 8 * r0, d,
+                                             db.data_ptr() + 8 * r0, dx.data_ptr(), 0.0)
+             for (r0, r1) in blocks]
+    chain = 0.0  # the reference's one ordered chain (nnls.hpp:119-122) over the same x
+    for (r0, r1) in blocks:
+        chain = solver.residual_rowblock_device(r1 - r0, n, dA.data_ptr() + 8 * r0, d,
+                                                db.data_ptr() + 8 * r0, dx.data_ptr(), chain)
+    # the allreduce sums 4 partial chains instead: a different order of the same terms
+    assert abs(sum(parts) - chain) <= 1e-12 * chain

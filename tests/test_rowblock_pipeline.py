@@ -110,3 +110,38 @@ def test_rowblock_pipeline_bitwise(tmp_path):
 def test_row_split():
     assert row_split(10, 3) == [(0, 4), (4, 7), (7, 10)]
     assert row_split(32768, 8)[-1] == (28672, 32768)
+
+
+# ---- configs[4] as written: partial Grams summed with one allreduce --------------------------
+def _ar_worker(rank, world, port, out_path):
+    from paper_1502_01645_b200.rowblock import allreduce_residual, allreduce_setup
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    A, b, x = _problem()
+    r0, r1 = row_split(D, world)[rank]
+
+    def compute(H, atb):  # this rank's partials (the GPU path: alnnls_gram_partial_device)
+        Ab = A[r0:r1, :]
+        H.copy_(torch.from_numpy(Ab.T @ Ab))
+        atb.copy_(torch.from_numpy(Ab.T @ b[r0:r1]))
+
+    H, atb = allreduce_setup(dist, world, N, compute, "cpu")
+    r = A[r0:r1, :] @ x - b[r0:r1]
+    res = allreduce_residual(dist, world, float(r @ r), "cpu")
+    if rank == 0:
+        np.savez(out_path, H=H.numpy(), h=atb.numpy(), r=np.array([res]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_allreduce_setup_two_ranks(tmp_path):
+    out = str(tmp_path / "ar.npz")
+    mp.spawn(_ar_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    A, b, x = _problem()
+    assert np.allclose(got["H"], A.T @ A, rtol=1e-13, atol=1e-13)
+    assert np.array_equal(got["H"], got["H"].T)
+    assert np.allclose(got["h"], A.T @ b, rtol=1e-13, atol=1e-13)
+    r = A @ x - b
+    assert abs(got["r"][0] - float(r @ r)) <= 1e-12 * float(r @ r)
