@@ -100,7 +100,7 @@ __global__ void k_b(double* out, long long* cyc) {
 
 // (d) = (c) with a runtime segment stride, a ring of 12 slots indexed modulo,
 // and an mbarrier wait (already-complete phase) at every 64-column stage start.
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool probe_mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t done;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -111,7 +111,7 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return done != 0;
 }
-__device__ __forceinline__ bool mbar_test_nc(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool probe_mbar_test_nc(uint64_t* bar, uint32_t parity) {
   uint32_t done;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -158,7 +158,7 @@ __global__ void k_d(double* out, long long* cyc, int seg_rt, int S) {
     const int st = ((q + 2) / 2) % S;
     if (WAIT) {
       if (KIND == 0) mbar_wait(&bar[st % 12], 0);
-      else while (!mbar_test(&bar[st % 12], 0)) {}
+      else while (!probe_mbar_test(&bar[st % 12], 0)) {}
     }
 #pragma unroll
     for (int l = 0; l < H; ++l) {
@@ -197,13 +197,13 @@ __global__ void k_i(double* out, long long* cyc, int seg, int S) {
   constexpr int H = 32;
   double pa[H], pb[H];
   mbar_wait(&bar[0], 0);
-  bool rnext = mbar_test(&bar[1 % 12], 0);
+  bool rnext = probe_mbar_test(&bar[1 % 12], 0);
 #pragma unroll
   for (int l = 0; l < H; ++l) pa[l] = xmul(col[l * seg + tt], v[l]);
   for (int q = 0; q < 2 * NST - 1; q += 2) {
     const int sn = ((q + 2) / 2) % S;   // next stage
     const int snn = ((q + 4) / 2) % S;  // the one after: test it now
-    const bool rn2 = NC ? mbar_test_nc(&bar[snn % 12], 0) : mbar_test(&bar[snn % 12], 0);
+    const bool rn2 = NC ? probe_mbar_test_nc(&bar[snn % 12], 0) : probe_mbar_test(&bar[snn % 12], 0);
 #pragma unroll
     for (int l = 0; l < H; ++l) {
       pb[l] = xmul(col[(H + l) * seg + tt], v[H + l]);
@@ -224,6 +224,53 @@ __global__ void k_i(double* out, long long* cyc, int seg, int S) {
   if (threadIdx.x == 0) *cyc = c1 - c0;
 }
 
+
+// (o) = (i) with the probe placed AFTER the next half's product loads in program
+// order: ptxas hoists register-only DADDs above an mbarrier probe but keeps loads
+// below it, so a probe issued before the loads serialises products and chain.
+__global__ void k_o(double* out, long long* cyc, int seg, int S) {
+  extern __shared__ double sm[];
+  __shared__ uint64_t bar[12];
+  double* col = sm;
+  double* v = sm + G * SEG;
+  for (int e = threadIdx.x; e < G * SEG + G; e += blockDim.x) sm[e] = 1.0 + e * 1e-9;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 12; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 12; ++i) mbar_arrive(&bar[i]);
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int tt = threadIdx.x % seg;
+  double acc = 0.0;
+  const long long c0 = clock64();
+  constexpr int H = 32;
+  double pa[H], pb[H];
+  mbar_wait(&bar[0], 0);
+  bool rnext = probe_mbar_test(&bar[1 % 12], 0);
+#pragma unroll
+  for (int l = 0; l < H; ++l) pa[l] = xmul(col[l * seg + tt], v[l]);
+  for (int s = 0; s < NST; ++s) {
+#pragma unroll
+    for (int l = 0; l < H; ++l) pb[l] = xmul(col[(H + l) * seg + tt], v[H + l]);
+    const bool rn2 = s + 2 < NST ? probe_mbar_test(&bar[((s + 2) % S) % 12], 0) : true;
+#pragma unroll
+    for (int l = 0; l < H; ++l) acc = xadd(acc, pa[l]);
+    if (s + 1 < NST) {
+      if (!rnext) mbar_wait(&bar[((s + 1) % S) % 12], 0);
+#pragma unroll
+      for (int l = 0; l < H; ++l) pa[l] = xmul(col[l * seg + tt], v[l]);
+    }
+#pragma unroll
+    for (int l = 0; l < H; ++l) acc = xadd(acc, pb[l]);
+    rnext = rn2;
+  }
+  const long long c1 = clock64();
+  out[threadIdx.x] = acc;
+  if (threadIdx.x == 0) *cyc = c1 - c0;
+}
 
 // (k) = (d) with the per-stage wait replaced by a poll of a plain shared-memory
 // flag (what a relay warp that did the mbarrier wait would publish).
@@ -288,7 +335,7 @@ __global__ void k_m(double* out, long long* cyc, int kind) {
   uint32_t par = 0;
   for (int i = 0; i < 1000; ++i) {
     if (kind == 0) { par ^= mbar_try_wait(&bar[0], 0) ? 0u : 1u; }
-    else { par ^= mbar_test(&bar[0], par) ? 0u : 1u; }
+    else { par ^= probe_mbar_test(&bar[0], par) ? 0u : 1u; }
   }
   const long long c1 = clock64();
   out[threadIdx.x] = par;
@@ -378,6 +425,7 @@ int main() {
   rd(k_d<true, 0, 1>, "(h) runtime seg + test_wait spin");
   rd(k_i<false>, "(i) test one stage ahead");
   rd(k_i<true>, "(j) test ahead, no memory clobber");
+  rd(k_o, "(o) probe after the next loads");
   rd(k_n<2>, "(n2) waits batched per 2 stages");
   rd(k_n<4>, "(n4) waits batched per 4 stages");
   rd(k_n<8>, "(n8) waits batched per 8 stages");
