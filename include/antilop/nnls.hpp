@@ -61,6 +61,30 @@ inline Vector unscale(const Vector& y, const ScaledSystem& sys, std::size_t n) {
   return x;
 }
 
+namespace detail {
+
+inline SolveResult empty_solve_result() {  // nnls.hpp:107-113
+  SolveResult r;
+  r.termination = Termination::EmptyPassiveSet;
+  r.trace.push_back({0, 0.0, 0.0, 0, std::chrono::duration<double>{0.0}, std::nullopt});
+  r.min_iterate = 0.0;
+  return r;
+}
+
+/// ||A x - b||^2 (nnls.hpp:115-123): the O(d n) product on the GPU (matvec, one
+/// ordered chain per row), the O(d) ordered sum of squares here, as the reference.
+inline double residual_norm_sq(const DenseMatrix& a, const Vector& b, const Vector& x) {
+  const Vector ax = matvec(a, x);
+  double s = 0.0;
+  for (std::size_t i = 0; i < b.size(); ++i) {
+    const double r = ax[i] - b[i];
+    s += r * r;
+  }
+  return s;
+}
+
+}  // namespace detail
+
 struct NnlsResult {
   Vector x;
   double residual_sq = 0.0;

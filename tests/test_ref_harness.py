@@ -1,0 +1,66 @@
+"""The reference's own benchmark harness, unmodified, over this repo's GPU facade
+(harness integration, instance families, report formats).
+
+oracle/Makefile `harness` compiles tests/cpp/ref_harness_driver.cpp against the
+reference's bench.hpp / testgen.hpp / io.hpp / active_set.hpp in place, twice:
+over the reference's own solver headers (harness_ref, CPU) and over
+include/antilop (harness_gpu: every gram / matvec / solve_nnls /
+solve_accelerated / solve_anti_accelerated call goes through libalnnls on the
+GPU). Both print the suite's bench-report/1 JSON (bench.hpp:287-369); apart
+from wall times they must be identical: same instances (testgen T1-T6), same
+objectives, gaps, iteration counts and terminations, bit for bit, for all four
+solvers of the reference's lineup (the CPU active-set "fast" baseline included,
+its linear algebra now on the GPU)."""
+import json
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "oracle", "_ref", "harness_ref")
+GPU = os.path.join(ROOT, "oracle", "_ref", "harness_gpu")
+WALL = {"wall_s", "mean_wall_s"}
+
+
+def _strip(x):
+    if isinstance(x, dict):
+        return {k: _strip(v) for k, v in x.items() if k not in WALL}
+    if isinstance(x, list):
+        return [_strip(v) for v in x]
+    return x
+
+
+def _run(exe, args):
+    r = subprocess.run([exe] + [str(a) for a in args], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr
+    return json.loads(r.stdout)
+
+
+def _need():
+    if not (os.path.exists(REF) and os.path.exists(GPU)):
+        pytest.skip("oracle/_ref harness binaries not built (reference sources absent at build)")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [
+    # the reference's default desk suite: T1-T6 x 5 sub-tests, n=400, d=600, all solvers
+    (400, 600, 5, 1, "T1,T2,T3,T4,T5,T6", "antilop,fast,accer,anti-accer"),
+    (37, 53, 3, 11, "T1,T3,T5", "antilop,anti-accer"),
+])
+def test_reference_harness_over_gpu_facade(args):
+    _need()
+    ref = _run(REF, args)
+    gpu = _run(GPU, args)
+    assert ref["schema"] == gpu["schema"] == "bench-report/1"
+    assert len(ref["cells"]) == len(gpu["cells"]) > 0
+    for a, b in zip(ref["cells"], gpu["cells"]):
+        assert _strip(a) == _strip(b), (a, b)
+    assert _strip(ref) == _strip(gpu)
+
+
+def test_reference_harness_cpu_runs():
+    """CPU side: the harness compiled over the reference headers runs (no GPU needed)."""
+    _need()
+    rep = _run(REF, (12, 18, 2, 5, "T2", "antilop"))
+    assert rep["schema"] == "bench-report/1" and len(rep["cells"]) == 2
