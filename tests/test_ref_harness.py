@@ -64,3 +64,31 @@ def test_reference_harness_cpu_runs():
     _need()
     rep = _run(REF, (12, 18, 2, 5, "T2", "antilop"))
     assert rep["schema"] == "bench-report/1" and len(rep["cells"]) == 2
+
+
+def _trace_wo_time(path):
+    rows = [ln.split(",") for ln in open(path).read().strip().splitlines()]
+    assert rows[0][1] == "elapsed_ms"
+    return [r[:1] + r[2:] for r in rows]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n,d,sp,seed", [("T5", 30, 45, 0.2, 9), ("T2", 120, 200, 0.3, 4),
+                                              ("T6", 64, 64, 0.0, 2)])
+@pytest.mark.parametrize("solver", ["antilop", "anti-accer", "accer", "fast"])
+def test_reference_cli_bodies_over_gpu_facade(tmp_path, kind, n, d, sp, seed, solver):
+    """bench.hpp cmd_generate -> MatrixMarket instance dir (io.hpp, testgen.hpp save/load),
+    then cmd_solve through both builds: the result summary JSON (nnls.hpp:146-153) and
+    the trace CSV (nqp.hpp:345-357, minus its wall-clock column) agree bit for bit."""
+    _need()
+    a, b = tmp_path / "ref", tmp_path / "gpu"
+    subprocess.run([REF, "gen", kind, str(n), str(d), str(sp), str(seed), str(a)], check=True,
+                   capture_output=True)
+    subprocess.run([REF, "gen", kind, str(n), str(d), str(sp), str(seed), str(b)], check=True,
+                   capture_output=True)
+    out_r = subprocess.run([REF, "solve", solver, str(a)], capture_output=True, text=True)
+    out_g = subprocess.run([GPU, "solve", solver, str(b)], capture_output=True, text=True)
+    assert out_r.returncode == out_g.returncode, (out_r.stdout, out_g.stdout, out_g.stderr)
+    assert out_r.stdout == out_g.stdout
+    tr = f"trace-{solver}.csv"
+    assert _trace_wo_time(a / tr) == _trace_wo_time(b / tr)
