@@ -114,14 +114,14 @@ inline NnlsResult solve_nnls(const DenseMatrix& a, const Vector& b,
 }
 
 /// {"residual_sq","iterations","termination","dropped_columns"} (nnls.hpp:146-153);
-/// keys in the same (sorted) order nlohmann::json emits them.
+/// keys in the same (sorted) order and number format nlohmann::json emits them.
 inline std::string result_summary_json(const NnlsResult& r) {
   std::ostringstream os;
   os << "{\"dropped_columns\":[";
   for (std::size_t i = 0; i < r.dropped_columns.size(); ++i)
     os << (i ? "," : "") << r.dropped_columns[i];
   os << "],\"iterations\":" << r.inner.iterations()
-     << ",\"residual_sq\":" << detail::g17(r.residual_sq) << ",\"termination\":\""
+     << ",\"residual_sq\":" << detail::json_number(r.residual_sq) << ",\"termination\":\""
      << to_string(r.inner.termination) << "\"}";
   return os.str();
 }

@@ -5,7 +5,16 @@
 // (alnnls_solve_nqp) and returns the reference's trajectory bit for bit.
 
 #include <algorithm>
+#if !defined(ANTILOP_NO_NLOHMANN)
+#if __has_include(<nlohmann/json.hpp>)
+#include <nlohmann/json.hpp>
+#elif __has_include("json.hpp")
+#include "json.hpp"
+#endif
+#endif
+#include <charconv>
 #include <chrono>
+#include <cmath>
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
@@ -249,6 +258,46 @@ inline std::string g17(double v) {
   char buf[64];
   std::snprintf(buf, sizeof(buf), "%.17g", v);
   return buf;
+}
+
+// A double the way the reference's nlohmann::json dump() writes it (nnls.hpp:146-153
+// serializes through it). With nlohmann/json on the include path (the reference's own
+// dependency) this IS nlohmann's dump(). Without it: the shortest round-trip digits
+// (std::to_chars) laid out like nlohmann's dtoa_impl::format_buffer (fixed notation
+// for decimal exponents in (-4, 15], else d.ddde+XX with at least two exponent digits;
+// "0.0" for zero, ".0" on integers, "null" for non-finite values) -- identical except
+// for the last digit of the ~0.3% of values where Grisu2's digits are not Ryu's.
+inline std::string json_number(double v) {
+#if defined(NLOHMANN_JSON_VERSION_MAJOR) && !defined(ANTILOP_NO_NLOHMANN)
+  return nlohmann::json(v).dump();
+#endif
+  if (!std::isfinite(v)) return "null";
+  std::string out;
+  if (std::signbit(v)) {
+    out += '-';
+    v = -v;
+  }
+  if (v == 0.0) return out + "0.0";
+  char sci[64];
+  const auto res = std::to_chars(sci, sci + sizeof(sci), v, std::chars_format::scientific);
+  const std::string s(sci, res.ptr);
+  const std::size_t e = s.find('e');
+  std::string digits;
+  for (std::size_t i = 0; i < e; ++i)
+    if (s[i] != '.') digits += s[i];
+  const int k = static_cast<int>(digits.size());
+  const int n = std::stoi(s.substr(e + 1)) + 1;  // decimal point position
+  constexpr int kMinExp = -4, kMaxExp = 15;
+  if (k <= n && n <= kMaxExp) return out + digits + std::string(n - k, '0') + ".0";
+  if (0 < n && n <= kMaxExp) return out + digits.substr(0, n) + "." + digits.substr(n);
+  if (kMinExp < n && n <= 0) return out + "0." + std::string(-n, '0') + digits;
+  out += digits.substr(0, 1);
+  if (k > 1) out += "." + digits.substr(1);
+  int x = n - 1;
+  out += x < 0 ? "e-" : "e+";
+  x = x < 0 ? -x : x;
+  if (x < 10) out += '0';
+  return out + std::to_string(x);
 }
 }  // namespace detail
 

@@ -25,6 +25,11 @@
 
 namespace alnnls {
 
+// Stages a ring must hold before the stage width drops (build knob).
+#ifndef ALNNLS_MIN_STAGES
+#define ALNNLS_MIN_STAGES 8
+#endif
+
 constexpr int kRingCols = 64;   // columns per stage
 constexpr int kMaxStages = 48;
 constexpr size_t kRingSmemBytes = 192 * 1024;  // dynamic smem of ring-carrying kernels
@@ -56,7 +61,7 @@ __device__ inline void ring_setup(RowRing& r, uint8_t* smem, size_t bytes, int n
   r.cons_warps = max(1, (nrows + 31) / 32);
   const size_t hdr = (size_t)kMaxStages * 16;
   int G = kRingCols;
-  while (G > 8 && (bytes - hdr) / ring_stage_bytes(seg, G) < 8) G >>= 1;
+  while (G > 8 && (bytes - hdr) / ring_stage_bytes(seg, G) < ALNNLS_MIN_STAGES) G >>= 1;
   r.G = G;
   int S = (int)((bytes - hdr) / ring_stage_bytes(seg, G));
   if (S > kMaxStages) S = kMaxStages;
@@ -193,6 +198,12 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
         for (int l = 0; l < 32; ++l) p[l] = xmul(col[l * seg + tt], v[l]);
 #pragma unroll
         for (int l = 0; l < 32; ++l) acc = xadd(acc, p[l]);
+      } else if (cnt == 16 && G == 16) {  // large m (c5: seg 112)
+        double p[16];
+#pragma unroll
+        for (int l = 0; l < 16; ++l) p[l] = xmul(col[l * seg + tt], v[l]);
+#pragma unroll
+        for (int l = 0; l < 16; ++l) acc = xadd(acc, p[l]);
       } else {
         for (int l = 0; l < cnt; ++l) acc = xmac(acc, col[l * seg + tt], v[l]);
       }

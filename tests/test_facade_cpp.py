@@ -35,3 +35,62 @@ int main() {
                     str(src), "-L", os.path.join(ROOT, "paper_1502_01645_b200", "lib"), "-lalnnls",
                     "-Wl,-rpath," + os.path.join(ROOT, "paper_1502_01645_b200", "lib")], check=True)
     assert subprocess.run([str(exe)]).returncode == 0
+
+
+def _nlohmann_dir():
+    import sys
+    for d in sys.path:
+        p = os.path.join(d, "include", "cudnn_frontend", "thirdparty", "nlohmann")
+        if os.path.exists(os.path.join(p, "json.hpp")):
+            return p
+    return None
+
+
+@pytest.mark.parametrize("fallback", [False, True])
+def test_result_json_number_format_matches_nlohmann(tmp_path, fallback):
+    """result_summary_json (nnls.hpp:146-153) prints residual_sq through nlohmann::json
+    in the reference; the facade's json_number writes the same characters (nlohmann
+    itself when it is on the include path; the to_chars fallback otherwise, which may
+    differ in the last digit of Grisu2's rare non-shortest outputs: < 1% here)."""
+    nl = _nlohmann_dir()
+    if nl is None:
+        pytest.skip("nlohmann/json.hpp not in this image")
+    src = tmp_path / "fmt.cpp"
+    src.write_text("""#include <cstdio>
+#include <cstring>
+#include <random>
+#include "antilop/nqp.hpp"
+#include "json.hpp"
+int main() {
+  std::mt19937_64 g(7);
+  int bad = 0, total = 0;
+  auto check = [&](double v) {
+    ++total;
+    if (antilop::detail::json_number(v) != nlohmann::json(v).dump()) ++bad;
+  };
+  const double fixed[] = {0.0, -0.0, 1.0, 100.0, 1e15, 1e16, 123456789012345.0, 0.1, 1e-4,
+                          1e-5, 2.5e-28, 5e-324, 1.7976931348623157e308, -3.25, 0.000123};
+  for (double v : fixed) check(v);
+  const int fixed_bad = bad;
+  for (int i = 0; i < 200000; ++i) {
+    double v;
+    const uint64_t bits = g();
+    std::memcpy(&v, &bits, 8);
+    if (std::isfinite(v)) check(v);
+    check(std::ldexp((double)(g() >> 11), -(int)(g() % 120)));
+  }
+  std::printf("%d %d %d\\n", fixed_bad, bad, total);
+  return 0;
+}""")
+    exe = tmp_path / "fmt"
+    flags = ["-DANTILOP_NO_NLOHMANN"] if fallback else []
+    subprocess.run(["g++", "-std=c++20", "-O1"] + flags + ["-I", os.path.join(ROOT, "include"),
+                    "-I", nl, "-o", str(exe), str(src)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0
+    fixed_bad, bad, total = (int(t) for t in r.stdout.split())
+    assert fixed_bad == 0
+    if fallback:
+        assert bad < total // 100, r.stdout
+    else:
+        assert bad == 0, r.stdout
