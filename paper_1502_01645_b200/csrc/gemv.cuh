@@ -25,9 +25,11 @@
 
 namespace alnnls {
 
-// Stages a ring must hold before the stage width drops (build knob).
+// Stages a ring must hold before the stage width drops (build knob). 6 measured
+// best at c5 (seg 112 -> 32-column stages: loop 3.68 -> 3.46 s; 8 -> 16-column
+// stages, 3 -> 64-column stages 3.95 s); c2/c3 (seg 28) keep 64 columns x 13.
 #ifndef ALNNLS_MIN_STAGES
-#define ALNNLS_MIN_STAGES 8
+#define ALNNLS_MIN_STAGES 6
 #endif
 
 constexpr int kRingCols = 64;   // columns per stage
