@@ -466,6 +466,7 @@ def run_ours_rowblock(args, ws, rank, local, dist):
         iters, _ = step()
     dist.barrier()
     torch.cuda.synchronize()
+    l0 = s.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record()
@@ -473,6 +474,7 @@ def run_ours_rowblock(args, ws, rank, local, dist):
             iters, res = step()
         ev1.record()
         torch.cuda.synchronize()
+    launches = (s.launch_count() - l0) // max(1, args.steps)
     t = ev0.elapsed_time(ev1) * 1e-3
     tt = torch.tensor([t, float(iters)], device="cuda", dtype=torch.float64)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -489,7 +491,7 @@ def run_ours_rowblock(args, ws, rank, local, dist):
                    "parallelism": f"row blocks x{ws}: k-chain Gram pipeline (NCCL send/recv), "
                                   "iterations on the last rank",
                    "l2": "inputs larger than L2"},
-        "iterations": iters, "gpu_launches": None, "clocks": clk.summary(),
+        "iterations": iters, "gpu_launches": launches, "clocks": clk.summary(),
         "e2e": None,
     }
     print(json.dumps(line), flush=True)
@@ -558,6 +560,7 @@ def run_ours_allreduce(args, ws, rank, local, dist):
         tm[k_] = 0.0
     barrier()
     torch.cuda.synchronize()
+    l0 = s.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record()
@@ -565,6 +568,7 @@ def run_ours_allreduce(args, ws, rank, local, dist):
             iters, res = step()
         e1.record()
         torch.cuda.synchronize()
+    launches = (s.launch_count() - l0) // max(1, args.steps)
     t = e0.elapsed_time(e1) * 1e-3
     vals = [t, float(iters), tm["partial"], tm["allreduce"], tm["solve"]]
     tt = torch.tensor(vals, device="cuda", dtype=torch.float64)
@@ -598,7 +602,7 @@ def run_ours_allreduce(args, ws, rank, local, dist):
                      "peak_source": "measured (tools/microbench/fp64_probe.cu, DMMA)",
                      "algorithmic": f"rows*n*(n+1) + 2*rows*n = {flops_rank} flop per rank",
                      "traffic": None},
-        "gpu_launches": None, "clocks": clk.summary(), "e2e": None,
+        "gpu_launches": launches, "clocks": clk.summary(), "e2e": None,
     }
     print(json.dumps(line), flush=True)
     return 0
