@@ -557,10 +557,28 @@ struct Pending {
   unsigned long long mults;
 };
 
+// Barrier over all CTAs of the loop. Small problems launch the whole grid as ONE
+// thread-block cluster (<= 16 CTAs, same GPC): the hardware cluster barrier
+// (release/acquire at cluster scope, L1 invalidated) replaces the cooperative
+// grid barrier (1.2 us measured; a nanosleep-backoff barrier in common.cuh
+// measured slower).
+template <bool kCluster>
+struct AllCtas {
+  cg::grid_group grid;
+  __device__ AllCtas() : grid(cg::this_grid()) {}
+  __device__ __forceinline__ void sync() {
+    if constexpr (kCluster) {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                   "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else {
+      grid.sync();
+    }
+  }
+};
+
+template <bool kCluster>
 __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
-  // cooperative-groups grid barrier (1.2 us measured; a nanosleep-backoff
-  // barrier in common.cuh measured slower here)
-  cg::grid_group grid = cg::this_grid();
+  AllCtas<kCluster> grid;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ LeaderState L;
   __shared__ Pending PD;
@@ -1078,7 +1096,20 @@ size_t nqp_loop_smem_bytes() { return kRingSmemBytes; }
 
 // Rows per block of the blocked Q: the vector CTA takes one SM, the row
 // blocks share the rest.
+// Small m: the loop runs as ONE thread-block cluster, the rows split over 7 row
+// CTAs (portable cluster of 8) up to m = 448, over 15 (non-portable 16) up to
+// m = 960; at most 64 rows per row CTA. c1 (m = 300): 22.7 us/iteration on 76
+// cooperative CTAs -> 19.3 (cluster of 16) -> 18.6 (cluster of 8).
+#ifndef ALNNLS_CLUSTER_ROWS
+#define ALNNLS_CLUSTER_ROWS 64  // 0 disables the cluster launch policy (build knob)
+#endif
 int nqp_rows_per_cta(int m, int sm_count) {
+  if (ALNNLS_CLUSTER_ROWS > 0 && m <= 15 * ALNNLS_CLUSTER_ROWS) {
+    const int ctas = m <= 7 * ALNNLS_CLUSTER_ROWS ? 7 : 15;
+    int r = (m + ctas - 1) / ctas;
+    r = (r + 3) & ~3;
+    return r < 4 ? 4 : r;
+  }
   const int nb = sm_count > 1 ? sm_count - 1 : 1;
   int r = (m + nb - 1) / nb;
   r = (r + 3) & ~3;
@@ -1088,16 +1119,43 @@ int nqp_rows_per_cta(int m, int sm_count) {
 
 cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream) {
   static bool attr_set = false;
+  static bool cluster_ok = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(nqp_loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(nqp_loop_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)nqp_loop_smem_bytes());
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(nqp_loop_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)nqp_loop_smem_bytes());
+    if (e != cudaSuccess) return e;
+    cluster_ok = cudaFuncSetAttribute(nqp_loop_kernel<true>,
+                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                 cudaSuccess;
     attr_set = true;
   }
   LoopArgs args = a;
+  if (cluster_ok && num_ctas <= 16) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(num_ctas);
+    cfg.blockDim = dim3(kLoopThreads);
+    cfg.dynamicSmemBytes = nqp_loop_smem_bytes();
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = num_ctas;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, nqp_loop_kernel<true>, &cfg) == cudaSuccess &&
+        nclusters > 0)
+      return cudaLaunchKernelEx(&cfg, nqp_loop_kernel<true>, args);
+    (void)cudaGetLastError();  // no cluster of this size fits: cooperative grid instead
+  }
   void* params[] = {&args};
-  return cudaLaunchCooperativeKernel((void*)nqp_loop_kernel, dim3(num_ctas), dim3(kLoopThreads),
-                                     params, nqp_loop_smem_bytes(), stream);
+  return cudaLaunchCooperativeKernel((void*)nqp_loop_kernel<false>, dim3(num_ctas),
+                                     dim3(kLoopThreads), params, nqp_loop_smem_bytes(), stream);
 }
 
 // ---- standalone masked GEMV (masked_matvec / matvec / residual / warm start) ------------
