@@ -301,7 +301,7 @@ def run_ours(args, ws, rank, local, dist):
     anti = args.solver == "anti_acc"
     solve_dev = s.solve_anti_accelerated_device if anti else s.solve_nnls_device
     solve_host = s.solve_anti_accelerated if anti else s.solve_nnls
-    for _ in range(args.warmup):
+    for _ in range(max(1, args.warmup)):  # >= 1: the solve's iteration count for the roofline
         solve_dev(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
     summ = s.last_summary()
     iters = int(summ.iterations)

@@ -974,8 +974,9 @@ __device__ int acc_rows_list(const LoopArgs& a, RowShared& S, int blk, int nblk,
   return S.total;
 }
 
+template <bool kCluster>
 __global__ void __launch_bounds__(kLoopThreads, 1) acc_loop_kernel(LoopArgs a) {
-  cg::grid_group grid = cg::this_grid();
+  AllCtas<kCluster> grid;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ LeaderState L;
   __shared__ RowShared RS;
@@ -1117,20 +1118,23 @@ int nqp_rows_per_cta(int m, int sm_count) {
   return r;
 }
 
-cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream) {
-  static bool attr_set = false;
-  static bool cluster_ok = false;
+// One loop launch: a single thread-block cluster when the grid fits one (<= 16
+// CTAs, non-portable sizes allowed, and the occupancy query finds a GPC for it),
+// else a cooperative grid.
+template <class KC, class KG>
+cudaError_t launch_loop(KC kcluster, KG kgrid, bool& attr_set, bool& cluster_ok,
+                        const LoopArgs& a, int num_ctas, cudaStream_t stream) {
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(nqp_loop_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(kgrid, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)nqp_loop_smem_bytes());
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(nqp_loop_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(kcluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)nqp_loop_smem_bytes());
     if (e != cudaSuccess) return e;
-    cluster_ok = cudaFuncSetAttribute(nqp_loop_kernel<true>,
-                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                 cudaSuccess;
+    cluster_ok =
+        cudaFuncSetAttribute(kcluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+        cudaSuccess;
+    (void)cudaGetLastError();
     attr_set = true;
   }
   LoopArgs args = a;
@@ -1148,14 +1152,19 @@ cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, nqp_loop_kernel<true>, &cfg) == cudaSuccess &&
-        nclusters > 0)
-      return cudaLaunchKernelEx(&cfg, nqp_loop_kernel<true>, args);
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kcluster, &cfg) == cudaSuccess && nclusters > 0)
+      return cudaLaunchKernelEx(&cfg, kcluster, args);
     (void)cudaGetLastError();  // no cluster of this size fits: cooperative grid instead
   }
   void* params[] = {&args};
-  return cudaLaunchCooperativeKernel((void*)nqp_loop_kernel<false>, dim3(num_ctas),
-                                     dim3(kLoopThreads), params, nqp_loop_smem_bytes(), stream);
+  return cudaLaunchCooperativeKernel((void*)kgrid, dim3(num_ctas), dim3(kLoopThreads), params,
+                                     nqp_loop_smem_bytes(), stream);
+}
+
+cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream) {
+  static bool attr_set = false, cluster_ok = false;
+  return launch_loop(nqp_loop_kernel<true>, nqp_loop_kernel<false>, attr_set, cluster_ok, a,
+                     num_ctas, stream);
 }
 
 // ---- standalone masked GEMV (masked_matvec / matvec / residual / warm start) ------------
@@ -1218,17 +1227,9 @@ cudaError_t launch_masked_gemv_blocked(const double* Qb, int m, int R, const uin
 
 namespace alnnls {
 cudaError_t launch_acc_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(acc_loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)nqp_loop_smem_bytes());
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  LoopArgs args = a;
-  void* params[] = {&args};
-  return cudaLaunchCooperativeKernel((void*)acc_loop_kernel, dim3(num_ctas), dim3(kLoopThreads),
-                                     params, nqp_loop_smem_bytes(), stream);
+  static bool attr_set = false, cluster_ok = false;
+  return launch_loop(acc_loop_kernel<true>, acc_loop_kernel<false>, attr_set, cluster_ok, a,
+                     num_ctas, stream);
 }
 
 cudaError_t launch_frobenius(const double* Qb, int m, int R, double* out, cudaStream_t stream) {
