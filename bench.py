@@ -759,7 +759,12 @@ def run_ours_batched(args, ws, rank, local, dist):
             "peak_source": "measured (tools/microbench/fp64_probe.cu, DMMA)",
             "algorithmic": (f"2 flop x reference multiply count (masked GEMVs) = {2 * mults} "
                             "flop per launch (rank 0's columns)"),
-            "traffic": traffic_from_profiles("c4", "batched_nqp_kernel")}
+            # measured on an 8192-column launch (the kernel reads Q from L2 and each
+            # column's B / X once), scaled linearly to rank 0's columns
+            "traffic": (None if traffic_from_profiles("c4_nrhs8192", "batched_nqp_kernel") is None
+                        else int(traffic_from_profiles("c4_nrhs8192", "batched_nqp_kernel")
+                                 * kc / 8192)),
+            "traffic_note": "ncu dram bytes of an 8192-column launch scaled to the columns"}
     line = {
         "metric": C4_METRIC, "value": value, "unit": C4_UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
