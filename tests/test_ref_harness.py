@@ -92,3 +92,23 @@ def test_reference_cli_bodies_over_gpu_facade(tmp_path, kind, n, d, sp, seed, so
     assert out_r.stdout == out_g.stdout
     tr = f"trace-{solver}.csv"
     assert _trace_wo_time(a / tr) == _trace_wo_time(b / tr)
+
+
+ACC_REF = os.path.join(ROOT, "oracle", "_ref", "acceptance_ref")
+ACC_GPU = os.path.join(ROOT, "oracle", "_ref", "acceptance_gpu")
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_gate_over_gpu_facade():
+    """The reference's acceptance gate (tests/acceptance.cpp: rescaling invariants, the 2^n
+    brute-force oracle, KKT certification of the desk suite, the 2-variable contrast, the
+    linear-rate envelope, monotone descent, optimality, bit-for-bit replay), compiled over
+    the GPU facade: every criterion passes and every reported figure (worst gaps, certified
+    counts, iteration counts, ratios) equals the CPU reference build's."""
+    if not (os.path.exists(ACC_REF) and os.path.exists(ACC_GPU)):
+        pytest.skip("oracle/_ref acceptance binaries not built (reference sources absent at build)")
+    ref = subprocess.run([ACC_REF], capture_output=True, text=True, timeout=1500)
+    gpu = subprocess.run([ACC_GPU], capture_output=True, text=True, timeout=1500)
+    assert gpu.returncode == 0, gpu.stdout + gpu.stderr
+    assert "all criteria passed" in gpu.stdout
+    assert ref.stdout == gpu.stdout
