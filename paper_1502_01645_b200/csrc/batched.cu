@@ -602,10 +602,13 @@ __global__ void unscale_batched_kernel(const double* Y, int m, const double* sca
 }
 
 // residual_norm_sq per column (nnls.hpp:115-123): (A x)_i is one chain over the
-// columns of A in ascending order (matvec, linalg.hpp:182-186; zero x_j terms are
-// exact no-ops), then s += r_i^2 in ascending i. One CTA owns 64 right-hand sides
-// and walks all row tiles in order, so each column's s is a single chain.
-constexpr int kRT = 32;   // rows per tile
+// columns of A in ascending order (matvec, linalg.hpp:182-186), then s += r_i^2 in
+// ascending i. One CTA owns kRC right-hand sides and walks all row tiles in order,
+// so each column's s is a single chain. A zero x_j adds a +-0 product, an exact
+// no-op on a chain that starts at +0 (it can never become -0), so the MACs are
+// branch-free. Each thread owns a 4 x 4 block of the tile; the next k-slab of A
+// and X is loaded into registers while the current one is multiplied.
+constexpr int kRT = 64;   // rows per tile
 constexpr int kRC = 64;   // columns per CTA
 constexpr int kRK = 16;   // k slab
 __global__ void __launch_bounds__(256) residual_batched_kernel(const double* A, uint64_t lda, int d,
@@ -613,47 +616,67 @@ __global__ void __launch_bounds__(256) residual_batched_kernel(const double* A, 
                                                                const double* B, uint64_t ldb,
                                                                int ncols,
                                                                alnnls_column_result* res) {
-  __shared__ double As[kRK][kRT];
-  __shared__ double Xs[kRK][kRC + 1];
-  __shared__ double Cs[kRT][kRC + 1];
+  // the slab buffers and the finished tile share one static buffer (< 48 KB)
+  __shared__ double sbuf[kRT * (kRC + 1)];
+  double(*As)[kRK][kRT] = reinterpret_cast<double(*)[kRK][kRT]>(sbuf);
+  double(*Xs)[kRK][kRC] = reinterpret_cast<double(*)[kRK][kRC]>(sbuf + 2 * kRK * kRT);
+  double(*Cs)[kRC + 1] = reinterpret_cast<double(*)[kRC + 1]>(sbuf);
+  static_assert(2 * kRK * (kRT + kRC) <= kRT * (kRC + 1), "slab buffers fit the tile buffer");
   const int c0 = blockIdx.x * kRC;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 2 x 4 outputs per thread
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // rows tx + 16 r, columns ty + 16 c
+  const int nslab = (n + kRK - 1) / kRK;
   double ssum = 0.0;  // thread t < kRC: the running chain of column c0 + t
-  for (int i0 = 0; i0 < d; i0 += kRT) {
-    double acc[2][4];
+  // slab loader: 4 A and 4 X elements per thread
+  auto fetch = [&](int i0, int k0, double (&ra)[4], double (&rx)[4]) {
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int kk = e / kRT, r = e % kRT;
+      const int i = i0 + r, kcol = k0 + kk;
+      ra[u] = (i < d && kcol < n) ? __ldg(A + (size_t)kcol * lda + i) : 0.0;
+      const int c = e / kRK, kx = e % kRK;
+      const int col = c0 + c, kc2 = k0 + kx;
+      rx[u] = (col < ncols && kc2 < n) ? __ldg(X + (size_t)col * n + kc2) : 0.0;
+    }
+  };
+  auto stash = [&](int buf, const double (&ra)[4], const double (&rx)[4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      As[buf][e / kRT][e % kRT] = ra[u];
+      Xs[buf][e % kRK][e / kRK] = rx[u];
+    }
+  };
+  for (int i0 = 0; i0 < d; i0 += kRT) {
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-    for (int k0 = 0; k0 < n; k0 += kRK) {
-      for (int e = threadIdx.x; e < kRK * kRT; e += blockDim.x) {
-        const int kk = e / kRT, r = e % kRT;
-        const int i = i0 + r, kcol = k0 + kk;
-        As[kk][r] = (i < d && kcol < n) ? __ldg(A + (size_t)kcol * lda + i) : 0.0;
-      }
-      for (int e = threadIdx.x; e < kRK * kRC; e += blockDim.x) {
-        const int c = e / kRK, kk = e % kRK;
-        const int col = c0 + c, kcol = k0 + kk;
-        Xs[kk][c] = (col < ncols && kcol < n) ? __ldg(X + (size_t)col * n + kcol) : 0.0;
-      }
-      __syncthreads();
+    double ra[4], rx[4];
+    fetch(i0, 0, ra, rx);
+    stash(0, ra, rx);
+    __syncthreads();
+    for (int sl = 0; sl < nslab; ++sl) {
+      const int buf = sl & 1;
+      if (sl + 1 < nslab) fetch(i0, (sl + 1) * kRK, ra, rx);
 #pragma unroll
       for (int kk = 0; kk < kRK; ++kk) {
-        double av[2], xv[4];
+        double av[4], xv[4];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) av[r] = As[kk][tx + 16 * r];
+        for (int r = 0; r < 4; ++r) av[r] = As[buf][kk][tx + 16 * r];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) xv[c] = Xs[kk][ty + 16 * c];
+        for (int c = 0; c < 4; ++c) xv[c] = Xs[buf][kk][ty + 16 * c];
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (xv[c] != 0.0) acc[r][c] = xmac(acc[r][c], av[r], xv[c]);
+          for (int c = 0; c < 4; ++c) acc[r][c] = xmac(acc[r][c], av[r], xv[c]);
       }
+      if (sl + 1 < nslab) stash(buf ^ 1, ra, rx);
       __syncthreads();
     }
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+    for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) Cs[tx + 16 * r][ty + 16 * c] = acc[r][c];
     __syncthreads();
