@@ -25,6 +25,12 @@
 
 namespace alnnls {
 
+// Producer warps issuing the ring's bulk copies (build knob; 6, 8 and 11 measured
+// equal or slower than 4 at c2 and c5).
+#ifndef ALNNLS_PRODUCERS
+#define ALNNLS_PRODUCERS 4
+#endif
+
 // Stages a ring must hold before the stage width drops (build knob). 6 measured
 // best at c5 (seg 112 -> 32-column stages: loop 3.68 -> 3.46 s; 8 -> 16-column
 // stages, 3 -> 64-column stages 3.95 s); c2/c3 (seg 28) keep 64 columns x 13.
@@ -68,7 +74,7 @@ __device__ inline void ring_setup(RowRing& r, uint8_t* smem, size_t bytes, int n
   int S = (int)((bytes - hdr) / ring_stage_bytes(seg, G));
   if (S > kMaxStages) S = kMaxStages;
   r.S = S;
-  r.P = max(1, min(min(4, S), max_warps - r.cons_warps));
+  r.P = max(1, min(min(ALNNLS_PRODUCERS, S), max_warps - r.cons_warps));
   r.full = reinterpret_cast<uint64_t*>(smem);
   r.empty = r.full + kMaxStages;
   r.data = reinterpret_cast<double*>(smem + hdr);
