@@ -252,6 +252,7 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   a.bar = bar;
   CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), ctx->stream));
   a.rows_per_cta = (int)ctx->qR;
+  a.resident = solver == 0 && nqp_resident_fits((int)m, a.rows_per_cta) ? 1 : 0;
   if (a.rows_per_cta > 352)
     return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: dimension too large for one GPU row split");
   const int nctas = 1 + (int)((m + a.rows_per_cta - 1) / a.rows_per_cta);

@@ -257,6 +257,49 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
   r.pos += nst;
 }
 
+// Shared-memory bytes of a resident row-block panel (seg x m doubles) plus the
+// staged list and values (small m; see gemv_resident).
+__host__ __device__ inline size_t resident_smem_bytes(int seg, int m) {
+  return (size_t)seg * m * 8 + (size_t)(m + 8) * 12 + 64;
+}
+
+// Row-block GEMV with the CTA's Q panel resident in shared memory (small m: the
+// panel, seg x m doubles, is copied in once per solve). y[row0 + t] = sum over the
+// list of Qs[list[s] * seg + t] * vals[s]: thread t owns row t and runs its one
+// chain in list order (the rounded products of a 64-column block, then their
+// dependent DADDs), bitwise the ring GEMV's result without its per-stage waits.
+// The list and values are staged into shared memory first. Whole CTA; starts and
+// ends with a block barrier.
+__device__ inline void gemv_resident(const double* Qs, int seg, uint32_t* sl, double* sv,
+                                     int row0, int nrows, const uint32_t* __restrict__ list,
+                                     const double* __restrict__ vals, int len,
+                                     double* __restrict__ out, const int* opos = nullptr,
+                                     double* __restrict__ out_c = nullptr) {
+  __syncthreads();  // the previous call's readers are done with sl / sv
+  for (int e = threadIdx.x; e < len; e += blockDim.x) {
+    sl[e] = __ldcg(list + e);
+    sv[e] = __ldcg(vals + e);
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < nrows) {
+    const double* q = Qs + t;
+    double acc = 0.0;
+    int s = 0;
+    for (; s + 64 <= len; s += 64) {
+      double p[64];
+#pragma unroll
+      for (int l = 0; l < 64; ++l) p[l] = xmul(q[(size_t)sl[s + l] * seg], sv[s + l]);
+#pragma unroll
+      for (int l = 0; l < 64; ++l) acc = xadd(acc, p[l]);
+    }
+    for (; s < len; ++s) acc = xmac(acc, q[(size_t)sl[s] * seg], sv[s]);
+    out[row0 + t] = acc;
+    if (opos && opos[t] >= 0) out_c[opos[t]] = acc;
+  }
+  __syncthreads();
+}
+
 // Blocked-layout index of Q(i, j) with block rows R (m x m logical).
 __host__ __device__ inline size_t blk_index(uint64_t i, uint64_t j, uint64_t m, uint64_t R) {
   return (i / R) * R * m + j * R + (i % R);

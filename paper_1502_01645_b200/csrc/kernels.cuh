@@ -74,6 +74,7 @@ struct LoopArgs {
   LoopCtrl* ctrl;
   unsigned int* bar;  // grid barrier words {count, generation}, zeroed before launch
   int rows_per_cta;
+  int resident;     // row CTAs keep their Q panel in shared memory (small m, gemv_resident)
   // accelerated (Nesterov) solver only (accelerated.hpp:21-117)
   double* y;        // extrapolated point (m)
   double* xn;       // projected step from y (m)
@@ -94,6 +95,8 @@ cudaError_t launch_acc_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream
 cudaError_t launch_frobenius(const double* Qb, int m, int R, double* out, cudaStream_t stream);
 int nqp_rows_per_cta(int m, int sm_count);
 size_t nqp_loop_smem_bytes();
+// true when a row CTA's Q panel (R x m) and the staged list fit its shared memory
+bool nqp_resident_fits(int m, int R);
 
 // Exact masked GEMV over a row range: y[i] = sum_t M[i, list[t]] * vals[t].
 cudaError_t launch_masked_gemv(const double* M, uint64_t ld, int rows, const uint32_t* list,

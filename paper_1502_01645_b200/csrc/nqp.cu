@@ -35,6 +35,10 @@ namespace alnnls {
 
 namespace {
 
+#ifndef ALNNLS_RESIDENT_Q
+#define ALNNLS_RESIDENT_Q 1  // build knob: Q panels resident in shared memory when they fit
+#endif
+
 constexpr int kLoopThreads = 384;  // 168 registers/thread at one CTA per SM: no spills
 constexpr int kWarps = kLoopThreads / 32;
 enum LoopState { kStateP2 = 1, kStateNoMove = 2, kStateNext = 3, kStateStop = 4 };
@@ -592,7 +596,21 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
   const int nrows = leader ? 0 : max(0, min(a.m - row0, R));
   const double* qblk = a.Q + (size_t)(leader ? 0 : blk) * R * a.m;
   RowRing ring;
-  if (!leader) ring_setup(ring, smem, kRingSmemBytes, nrows, R, kWarps);
+  // small m: the row block of Q stays in shared memory for the whole solve
+  const bool resident = a.resident != 0;
+  double* Qs = reinterpret_cast<double*>(smem);
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(Qs + (size_t)R * a.m);
+  double* s_vals = reinterpret_cast<double*>(s_list + ((a.m + 8) & ~1));
+  if (!leader) {
+    if (resident) {
+      const double2* src = reinterpret_cast<const double2*>(qblk);
+      double2* dst = reinterpret_cast<double2*>(Qs);
+      for (int e = threadIdx.x; e < R * a.m / 2; e += blockDim.x) dst[e] = __ldg(src + e);
+      __syncthreads();
+    } else {
+      ring_setup(ring, smem, kRingSmemBytes, nrows, R, kWarps);
+    }
+  }
   double* sbuf = reinterpret_cast<double*>(smem);
   double* xb[2] = {a.x, a.x_alt};
   double* gb[2] = {a.g, a.g_alt};
@@ -632,8 +650,12 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
     ++npass;
     if (!leader) {
       // u = Q g_bar over own rows, also compacted to the passive list for den
-      gemv_rows(ring, qblk, R, true, row0, nrows, ls[lp].mask, ls[lp].gP, ml_l[lp], a.u,
-                RS.lpos[lp], a.uP);
+      if (resident)
+        gemv_resident(Qs, R, s_list, s_vals, row0, nrows, ls[lp].mask, ls[lp].gP, ml_l[lp], a.u,
+                      RS.lpos[lp], a.uP);
+      else
+        gemv_rows(ring, qblk, R, true, row0, nrows, ls[lp].mask, ls[lp].gP, ml_l[lp], a.u,
+                  RS.lpos[lp], a.uP);
       __syncthreads();
       if (threadIdx.x == 0) {  // publish: uP of own rows is complete (release)
         __threadfence();
@@ -839,7 +861,10 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
 
     // ===== P2, speculative update, next passive lists ====================================
     const int cl = __ldcg(&a.ctrl->chg_len);
-    if (!leader) gemv_rows(ring, qblk, R, true, row0, nrows, a.chg, a.dC, cl, a.gd);
+    if (!leader) {
+      if (resident) gemv_resident(Qs, R, s_list, s_vals, row0, nrows, a.chg, a.dC, cl, a.gd);
+      else gemv_rows(ring, qblk, R, true, row0, nrows, a.chg, a.dC, cl, a.gd);
+    }
     // no grid barrier after P2: row_apply reads only its own rows of gd, and the
     // leader's df chain reads gdC only after B0
     __syncthreads();
@@ -1094,6 +1119,9 @@ __global__ void __launch_bounds__(kLoopThreads, 1) frobenius_kernel(const double
 }  // namespace
 
 size_t nqp_loop_smem_bytes() { return kRingSmemBytes; }
+bool nqp_resident_fits(int m, int R) {
+  return ALNNLS_RESIDENT_Q && R <= kLoopThreads && resident_smem_bytes(R, m) <= kRingSmemBytes;
+}
 
 // Rows per block of the blocked Q: the vector CTA takes one SM, the row
 // blocks share the rest.
