@@ -12,7 +12,7 @@
 // A^T B), 256 threads = 8 warps as 2 (M) x 4 (N), warp tile 64 x 32 = 4 x 4
 // m16n8k8 accumulators; k slabs of 16 staged by cp.async (16 B chunks) through
 // a 4-deep ring. Shared tiles are [column][k] with the 16 B chunk index XOR-
-// swizzled by (column & 7), so both fragment loads are bank-conflict-free.
+// swizzled by 2 (column & 3), so both fragment loads are bank-conflict-free.
 #include "common.cuh"
 #include "gemv.cuh"
 #include "kernels.cuh"
@@ -54,7 +54,13 @@ __device__ __forceinline__ void dmma(double (&c)[4], const double (&a)[4], const
 }
 
 // element (col r, k) of a swizzled [TB][TK] slab
-__device__ __forceinline__ int swz(int r, int k) { return r * TK + ((((k >> 1) ^ (r & 7))) << 1) + (k & 1); }
+// The XOR pattern spreads the 4 rows x 4 k of a half-warp's fragment load over all
+// 32 banks: ((r & 3) << 1) maps the two 16 B chunks a row contributes to 8 distinct
+// chunks (an (r & 7) pattern left the rows r and r ^ 1 on the same banks: 2-way
+// conflicts on every fragment load, 207.6 M in the c2 capture).
+__device__ __forceinline__ int swz(int r, int k) {
+  return r * TK + ((((k >> 1) ^ ((r & 3) << 1))) << 1) + (k & 1);
+}
 
 // Output element (i, j) of the Gram / A^T B with the same epilogues as the
 // exact kernel (setup.cu syrk_exact_kernel).
