@@ -1127,13 +1127,20 @@ bool nqp_resident_fits(int m, int R) {
 // blocks share the rest.
 // Small m: the loop runs as ONE thread-block cluster, the rows split over 7 row
 // CTAs (portable cluster of 8) up to m = 448, over 15 (non-portable 16) up to
-// m = 960; at most 64 rows per row CTA. c1 (m = 300): 22.7 us/iteration on 76
+// m = 640; at most 64 rows per row CTA. Larger m: the cooperative grid (whose row
+// CTAs keep their Q panels resident in shared memory up to m ~ 1870). c1 (m = 300): 22.7 us/iteration on 76
 // cooperative CTAs -> 19.3 (cluster of 16) -> 18.6 (cluster of 8).
 #ifndef ALNNLS_CLUSTER_ROWS
 #define ALNNLS_CLUSTER_ROWS 64  // 0 disables the cluster launch policy (build knob)
 #endif
+#ifndef ALNNLS_CLUSTER16_MAX_M
+#define ALNNLS_CLUSTER16_MAX_M 640  // build knob: top of the 16-CTA cluster tier
+#endif
 int nqp_rows_per_cta(int m, int sm_count) {
-  if (ALNNLS_CLUSTER_ROWS > 0 && m <= 15 * ALNNLS_CLUSTER_ROWS) {
+  // measured (tools/ab_run.sh, us/iteration, cluster of 16 vs grid with resident Q
+  // panels): m = 500 18.2 vs 21.3, 600 22.9 vs 23.7, 800 28.3 vs 25.0, 900 28.1 vs 25.9
+  if (ALNNLS_CLUSTER_ROWS > 0 && m <= ALNNLS_CLUSTER16_MAX_M &&
+      m <= 15 * ALNNLS_CLUSTER_ROWS) {
     const int ctas = m <= 7 * ALNNLS_CLUSTER_ROWS ? 7 : 15;
     int r = (m + ctas - 1) / ctas;
     r = (r + 3) & ~3;

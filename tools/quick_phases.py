@@ -6,7 +6,9 @@ sys.path.insert(0, ".")
 from paper_1502_01645_b200 import instances
 from paper_1502_01645_b200.api import Solver, SolverConfig
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-inst = instances.make_config(name)
+dd = int(sys.argv[2]) if len(sys.argv) > 2 else None   # optional scaled shape (d, n)
+nn = int(sys.argv[3]) if len(sys.argv) > 3 else None
+inst = instances.make_config(name, d=dd, n=nn)
 A, b = inst["A"], inst["b"]
 d, n = A.shape
 dA = torch.from_numpy(np.ascontiguousarray(A.T)).cuda(); db = torch.from_numpy(b).cuda()
