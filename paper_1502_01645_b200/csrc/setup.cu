@@ -203,6 +203,93 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
   }
 }
 
+// Small n (few 128 x 128 tiles; e.g. the c4 Gram, n = 256: 3 tiles for 148 SMs):
+// 32 x 32 output tiles, 64 threads, 4 x 4 outputs per thread, every output ONE
+// ascending-k chain (rounded product, then rounded sum; zero-filled k beyond d
+// add +0, an exact no-op). The next 32-k slab is loaded into registers while the
+// current one is multiplied. Modes 0 (H) and 1 (fused rescale), same epilogue
+// as syrk_piece.
+constexpr int SB = 32, SK = 32, ST = 64;
+__global__ void __launch_bounds__(ST) syrk_small_kernel(SetupArgs s, int mode) {
+  __shared__ double As[2][SK][SB + 1];
+  __shared__ double Bs[2][SK][SB + 1];
+  int ti, tj;
+  tri_tile(blockIdx.x, ti, tj);
+  const int i0 = ti * SB, j0 = tj * SB;
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;  // rows tx + 8 r, columns ty + 8 c
+  double ra[16], rb[16];
+  auto fetch = [&](int k0) {  // element e = tid + 64 u: column e / SK, k = k0 + e % SK
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = threadIdx.x + ST * u, col = e / SK, k = k0 + e % SK;
+      const bool kv = k < s.d;
+      ra[u] = kv && i0 + col < s.n ? __ldg(s.A + (size_t)(i0 + col) * s.lda + k) : 0.0;
+      rb[u] = kv && j0 + col < s.n ? __ldg(s.A + (size_t)(j0 + col) * s.lda + k) : 0.0;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = threadIdx.x + ST * u;
+      As[buf][e % SK][e / SK] = ra[u];
+      Bs[buf][e % SK][e / SK] = rb[u];
+    }
+  };
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+  const int nk = (s.d + SK - 1) / SK;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  for (int kb = 0; kb < nk; ++kb) {
+    const int buf = kb & 1;
+    if (kb + 1 < nk) fetch((kb + 1) * SK);
+#pragma unroll
+    for (int kk = 0; kk < SK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = As[buf][kk][tx + 8 * r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = Bs[buf][kk][ty + 8 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        double p[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) p[c] = xmul(a[r], b[c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = xadd(acc[r][c], p[c]);
+      }
+    }
+    if (kb + 1 < nk) stash(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + tx + 8 * r, j = j0 + ty + 8 * c;
+      const double v = acc[r][c];
+      if (i > j || j >= s.n) continue;
+      if (mode == 0) {
+        s.H[(size_t)j * s.n + i] = v;
+        s.H[(size_t)i * s.n + j] = v;
+      } else {
+        const int pi = s.pos[i], pj = s.pos[j];
+        if (pi < 0 || pj < 0) continue;
+        if (i == j) {
+          s.Q[blk_index(pi, pi, s.m, s.qR)] = 1.0;  // nnls.hpp:72
+        } else {
+          const double qv = xdiv(v, xmul(s.scale[pi], s.scale[pj]));  // nnls.hpp:75
+          s.Q[blk_index(pi, pj, s.m, s.qR)] = qv;
+          s.Q[blk_index(pj, pi, s.m, s.qR)] = qv;
+        }
+      }
+    }
+}
+
 // One CTA per output tile.
 __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode) {
   extern __shared__ __align__(16) double syrk_sm[];
@@ -553,6 +640,12 @@ __global__ void negate_kernel(const double* x, int n, double* y) {
   if (i < n) y[i] = -x[i];
 }
 
+// Build knob: the 32 x 32-tile SYRK runs when the 128 x 128 tiles number fewer than
+// half this many (0 disables it).
+#ifndef ALNNLS_SYRK_SMALL
+#define ALNNLS_SYRK_SMALL 148
+#endif
+
 int syrk_streamk_ctas(const SetupArgs& s, int mode, int sm_count) {
   const int nt = (s.n + BM - 1) / BM;
   const long long tiles = mode == 2 ? (long long)nt * ((s.nrhs + BM - 1) / BM) : (long long)nt * (nt + 1) / 2;
@@ -585,6 +678,11 @@ cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream) {
     void* args[] = {&sa, &md, &tl};
     return cudaLaunchCooperativeKernel((const void*)syrk_streamk_kernel, dim3(s.sk_ctas), dim3(NT),
                                        args, kSyrkSmem, stream);
+  }
+  if (ALNNLS_SYRK_SMALL && mode != 2 && !s.tpin && !s.tpout && 2 * tiles < ALNNLS_SYRK_SMALL) {
+    const int nt32 = (s.n + SB - 1) / SB;
+    syrk_small_kernel<<<nt32 * (nt32 + 1) / 2, ST, 0, stream>>>(s, mode);
+    return cudaGetLastError();
   }
   syrk_exact_kernel<<<tiles, NT, kSyrkSmem, stream>>>(s, mode);
   return cudaGetLastError();
