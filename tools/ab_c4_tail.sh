@@ -1,3 +1,5 @@
+# Batched tail A/B (under gpurun): a rank-sized 8192-column shard vs the full 65536
+# columns, for the in-tree build and one variant (build/var/noskip).
 mkdir -p gpurun_out/ab
 for v in base noskip; do
   if [ $v = base ]; then L=""; else L=build/var/$v/libalnnls.so; fi
