@@ -40,7 +40,10 @@ namespace alnnls {
 
 constexpr int kRingCols = 64;   // columns per stage
 constexpr int kMaxStages = 48;
-constexpr size_t kRingSmemBytes = 192 * 1024;  // dynamic smem of ring-carrying kernels
+#ifndef ALNNLS_RING_KB
+#define ALNNLS_RING_KB 208  // build knob (c5: 7 instead of 6 32-column stages, 503 -> 497 us/iteration)
+#endif
+constexpr size_t kRingSmemBytes = ALNNLS_RING_KB * 1024;  // dynamic smem of ring-carrying kernels
 
 struct RowRing {
   uint64_t* full;

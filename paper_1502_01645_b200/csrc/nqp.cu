@@ -39,6 +39,10 @@ namespace {
 #define ALNNLS_RESIDENT_Q 1  // build knob: Q panels resident in shared memory when they fit
 #endif
 
+#ifndef ALNNLS_CHAIN_CH
+#define ALNNLS_CHAIN_CH 1024  // build knob: vector-CTA chain chunk (products per buffer)
+#endif
+
 constexpr int kLoopThreads = 384;  // 168 registers/thread at one CTA per SM: no spills
 constexpr int kWarps = kLoopThreads / 32;
 enum LoopState { kStateP2 = 1, kStateNoMove = 2, kStateNext = 3, kStateStop = 4 };
@@ -166,7 +170,7 @@ __device__ __forceinline__ double smem_chain_db(double s, const double* __restri
 template <int K, class F>
 __device__ void leader_chains(double* sbuf, size_t sbuf_bytes, LeaderState& L, int len, F prod) {
   // small chunks so the chain starts after the first 1024 products are formed
-  const int CH = min(1024, (int)(sbuf_bytes / (2 * K * sizeof(double))) & ~1);
+  const int CH = min(ALNNLS_CHAIN_CH, (int)(sbuf_bytes / (2 * K * sizeof(double))) & ~1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = (len + CH - 1) / CH;
   // 4 positions per thread per round: all their operand loads are in flight
@@ -501,7 +505,7 @@ __device__ int row_lists(const LoopArgs& a, RowShared& S, int blk, int nblk, int
 template <int K, class F>
 __device__ void leader_chains_var(double* sbuf, size_t sbuf_bytes, LeaderState& L,
                                   const int (&len)[K], F prod) {
-  const int CH = min(1024, (int)(sbuf_bytes / (2 * K * sizeof(double))) & ~1);
+  const int CH = min(ALNNLS_CHAIN_CH, (int)(sbuf_bytes / (2 * K * sizeof(double))) & ~1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int mx = 0;
 #pragma unroll
