@@ -703,17 +703,11 @@ int batched_cols_per_cta(int m) {
 cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream) {
   const int NB = batched_cols_per_cta(a.m);
   if (NB == 0) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
+  {
     const int mx = (int)batch_smem_bytes(1024, 4);  // the largest configuration
-    cudaError_t e = cudaFuncSetAttribute(batched_nqp_kernel<16>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(batched_nqp_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(batched_nqp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    if (e != cudaSuccess) return e;
-    attr = true;
+    if (cudaError_t e = smem_optin(batched_nqp_kernel<16>, mx)) return e;
+    if (cudaError_t e = smem_optin(batched_nqp_kernel<8>, mx)) return e;
+    if (cudaError_t e = smem_optin(batched_nqp_kernel<4>, mx)) return e;
   }
   const size_t smem = batch_smem_bytes(a.m, NB);
   int grid = sm_count;

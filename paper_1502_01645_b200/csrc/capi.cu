@@ -5,6 +5,7 @@
 // Validation mirrors the reference preconditions (linalg.hpp:22-24, :42-52,
 // :74-85; nqp.hpp:35-41, :84-98, :227-230; nnls.hpp:43-56, :131) so that the
 // same inputs fail with the same category (EINVAL / ERANGE / ENUMERIC).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -41,7 +42,7 @@ struct alnnls_ctx {
   DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
   DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
       hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb, uP, gdC, skp, skf,
-      ay, axn, aw, avy, apc, tst;
+      ay, axn, aw, avy, apc, tst, fgb0, fgb1, fpart, fden, fkl, fkv, fkc;
 
   // last solve
   bool last_nnls = false;
@@ -100,6 +101,11 @@ T* ensure(alnnls_ctx* ctx, DevBuf& b, size_t count, int* st) {
   if (st__ != ALNNLS_OK) return st__
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+// device trace / multiply-count capacity caps (records): 4 Mi trace records
+// (192 MiB) and 16 Mi multiply counts (128 MiB)
+constexpr uint64_t kTraceCapMax = (uint64_t)1 << 22;
+constexpr uint64_t kMultCapMax = (uint64_t)1 << 24;
 
 // doubles of a blocked m x m matrix with block rows R (gemv.cuh blk_index)
 uint64_t blocked_size(uint64_t m, uint64_t R) { return round_up(m, R) * m; }
@@ -183,12 +189,16 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   double* minx = part + 160;
   LoopCtrl* ctrl = ENSURE(LoopCtrl, ctrl, 2);  // [1] holds the grid-barrier words
   unsigned int* bar = reinterpret_cast<unsigned int*>(ctrl + 1);
-  const uint64_t tcap = r.max_iters / r.trace_every + 2;
+  // The reference's trace grows as needed; the device buffers are sized up front
+  // from max_iters, capped (overflow-safe) so an "unlimited" max_iters cannot wrap
+  // or exhaust HBM. Past the cap the last slot always holds the newest record
+  // (so the final record survives) and trace_len / mult_len are clamped.
+  const uint64_t tcap = std::min(r.max_iters / r.trace_every, kTraceCapMax - 2) + 2;
   alnnls_iter_record* trace = ENSURE(alnnls_iter_record, trace, tcap);
   uint64_t mcap = 0;
   uint64_t* mults = nullptr;
   if (cfg->record_multiplies) {
-    mcap = r.max_iters + 1;
+    mcap = std::min(r.max_iters, kMultCapMax - 1) + 1;
     mults = ENSURE(uint64_t, mults, mcap);
   }
   cudaStream_t s = ctx->stream;
@@ -272,8 +282,47 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
     CK(cudaStreamSynchronize(s));
     a.alpha = 1.0 / hn;  // :83 (host IEEE division, same rounding)
   }
+  // FAST profile: the one-pass bandwidth-bound loop (fastloop.cu) when its
+  // shared-memory staging fits (m up to ~26k); otherwise the exact loop.
+  const bool fast = solver == 0 && cfg->profile == ALNNLS_PROFILE_FAST &&
+                    fast_loop_supported((int)m, a.rows_per_cta);
+  FastArgs fa{};
+  if (fast) {
+    const int nblk = (int)((m + a.rows_per_cta - 1) / a.rows_per_cta);
+    fa.Q = Q;
+    fa.m = (int)m;
+    fa.R = a.rows_per_cta;
+    fa.q = q;
+    fa.x[0] = x;
+    fa.x[1] = x_alt;
+    fa.g[0] = g;
+    fa.g[1] = g_alt;
+    fa.gbar[0] = ENSURE(double, fgb0, mp);
+    fa.gbar[1] = ENSURE(double, fgb1, mp);
+    FastPart* fp = ENSURE(FastPart, fpart, 2 * nblk);
+    fa.part[0] = fp;
+    fa.part[1] = fp + nblk;
+    fa.den = ENSURE(double, fden, nblk);
+    fa.kl = ENSURE(uint32_t, fkl, (size_t)nblk * a.rows_per_cta);
+    fa.kv = ENSURE(double, fkv, (size_t)nblk * a.rows_per_cta);
+    fa.kc = ENSURE(int, fkc, nblk);
+    fa.eps = a.eps;
+    fa.max_iters = a.max_iters;
+    fa.has_time_cap = a.has_time_cap;
+    fa.time_cap_s = a.time_cap_s;
+    fa.stall_window = a.stall_window;
+    fa.trace_every = a.trace_every;
+    fa.trace = trace;
+    fa.trace_cap = tcap;
+    fa.mults = mults;
+    fa.mults_cap = mcap;
+    fa.ctrl = ctrl;
+    CK(cudaMemsetAsync(ctrl, 0, sizeof(LoopCtrl), s));
+  }
   CK(cudaEventRecord(ctx->ev[2], s));
-  if (solver == 1) {
+  if (fast) {
+    CK(launch_fast_loop(fa, s));
+  } else if (solver == 1) {
     CK(launch_acc_loop(a, nctas, s));
   } else {
     CK(launch_nqp_loop(a, nctas, s));
@@ -288,8 +337,8 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   out->termination = hc.termination;
   out->numeric_failure = hc.numeric_failure;
   out->iterations = hc.iterations;
-  out->trace_len = hc.trace_len;
-  out->mult_len = cfg->record_multiplies ? hc.mult_len : 0;
+  out->trace_len = std::min<uint64_t>(hc.trace_len, tcap);
+  out->mult_len = cfg->record_multiplies ? std::min<uint64_t>(hc.mult_len, mcap) : 0;
   out->multiplies_total = hc.mult_total;
   out->min_iterate = hc.min_iterate;
   out->f_final = hc.f_final;
@@ -699,7 +748,8 @@ void alnnls_destroy(alnnls_ctx* ctx) {
                     &ctx->X,      &ctx->x_alt, &ctx->mask2,   &ctx->gP2,   &ctx->xP2,  &ctx->qP2,
                     &ctx->part,   &ctx->resb,  &ctx->yb,      &ctx->qb,   &ctx->uP,   &ctx->gdC,
                     &ctx->skp,    &ctx->skf,   &ctx->ay,      &ctx->axn,   &ctx->aw,
-                    &ctx->avy,    &ctx->apc,   &ctx->tst};
+                    &ctx->avy,    &ctx->apc,   &ctx->tst,   &ctx->fgb0,  &ctx->fgb1,
+                    &ctx->fpart,  &ctx->fden,  &ctx->fkl,   &ctx->fkv,   &ctx->fkc};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
@@ -777,9 +827,33 @@ int alnnls_solve_nqp_device(alnnls_ctx* ctx, uint64_t m, const double* dQ, uint6
   if (rc) return rc;
   if (!cfg || !dQ || !dq) return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: null argument");
   if (m < 1) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  if (ldq < m) return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: ldq < m");
+  int st__ = ALNNLS_OK;
+  {
+    // the reference's construction-time checks, in its order, on the device copies:
+    // finite Q and q (linalg.hpp:42-52, :84), symmetric Q (nqp.hpp:37-41); after the
+    // config (nqp.hpp:219-222): a finite, nonnegative start (nqp.hpp:227-230)
+    int* flag = ENSURE(int, flag, 8);
+    CK(cudaMemsetAsync(flag, 0, sizeof(int) * 5, ctx->stream));
+    CK(launch_check_finite(dQ, m, m, ldq, flag + 0, ctx->stream));
+    CK(launch_check_finite(dq, m, 1, m, flag + 1, ctx->stream));
+    CK(launch_check_matrix(dQ, m, m, ldq, 0, flag + 2, ctx->stream));
+    if (dstart) {
+      CK(launch_check_finite(dstart, m, 1, m, flag + 3, ctx->stream));
+      CK(launch_check_matrix(dstart, m, 1, m, 1, flag + 4, ctx->stream));
+    }
+    int hf[5] = {0, 0, 0, 0, 0};
+    if ((rc = copy_out(ctx, hf, flag, sizeof(hf)))) return rc;
+    if (hf[0]) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
+    if (hf[1]) return set_err(ctx, ALNNLS_EINVAL, "Vector: non-finite entry");
+    if (hf[2]) return set_err(ctx, ALNNLS_EINVAL, "NqpProblem: Q must be symmetric");
+    Resolved r0;
+    if ((rc = resolve(ctx, cfg, m, &r0))) return rc;
+    if (hf[3]) return set_err(ctx, ALNNLS_EINVAL, "Vector: non-finite entry");
+    if (hf[4]) return set_err(ctx, ALNNLS_EINVAL, "solve_nqp: start must be nonnegative");
+  }
   Resolved r;
   if ((rc = resolve(ctx, cfg, m, &r))) return rc;
-  int st__ = ALNNLS_OK;
   ctx->qR = (uint64_t)nqp_rows_per_cta((int)m, ctx->sm_count);
   double* Qd = ENSURE(double, Q, blocked_size(m, ctx->qR));
   CK(launch_to_blocked(dQ, ldq, (int)m, (int)ctx->qR, Qd, ctx->stream));
@@ -867,14 +941,16 @@ int alnnls_get_final_grad(alnnls_ctx* ctx, double* g, uint64_t len) {
 
 int alnnls_get_trace(alnnls_ctx* ctx, alnnls_iter_record* rec, uint64_t cap) {
   if (!ctx || !rec) return ALNNLS_EINVAL;
-  const uint64_t n = ctx->last.trace_len;
+  // never past what the device buffer holds (trace_len is clamped by run_nqp too)
+  const uint64_t n = std::min<uint64_t>(ctx->last.trace_len,
+                                        ctx->trace.bytes / sizeof(alnnls_iter_record));
   if (cap < n) return set_err(ctx, ALNNLS_ECAPACITY, "get_trace: buffer too small");
   return copy_out(ctx, rec, ctx->trace.p, sizeof(alnnls_iter_record) * n);
 }
 
 int alnnls_get_multiplies(alnnls_ctx* ctx, uint64_t* mults, uint64_t cap) {
   if (!ctx || !mults) return ALNNLS_EINVAL;
-  const uint64_t n = ctx->last.mult_len;
+  const uint64_t n = std::min<uint64_t>(ctx->last.mult_len, ctx->mults.bytes / sizeof(uint64_t));
   if (cap < n) return set_err(ctx, ALNNLS_ECAPACITY, "get_multiplies: buffer too small");
   return copy_out(ctx, mults, ctx->mults.p, sizeof(uint64_t) * n);
 }

@@ -8,11 +8,37 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <cuda_runtime.h>
 
 namespace alnnls {
 
 constexpr int kMaxThreads = 512;
+
+// cudaFuncSetAttribute once per (kernel, attribute, device). Function attributes
+// are per device, and one process may drive several devices (one context per
+// GPU), so a process-wide "done" flag would leave the second device's launches
+// without the shared-memory opt-in. Thread-safe.
+inline cudaError_t func_attr_once(const void* func, cudaFuncAttribute attr, int value) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(func, (int)attr, dev);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, attr, value);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
+}
+template <class K>
+inline cudaError_t smem_optin(K* kernel, int bytes) {
+  return func_attr_once(reinterpret_cast<const void*>(kernel),
+                        cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
 
 __device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }

@@ -206,13 +206,7 @@ cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream) 
   const int tiles = mode == 2 ? nt * ((s.nrhs + TB - 1) / TB) : nt * (nt + 1) / 2;
   if (tiles == 0) return cudaSuccess;
   if (!syrk_dmma_supported(s, mode)) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(syrk_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kDmmaSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = smem_optin(syrk_dmma_kernel, (int)kDmmaSmem)) return e;
   syrk_dmma_kernel<<<tiles, TT, kDmmaSmem, stream>>>(s, mode);
   return cudaGetLastError();
 }

@@ -98,6 +98,40 @@ size_t nqp_loop_smem_bytes();
 // true when a row CTA's Q panel (R x m) and the staged list fit its shared memory
 bool nqp_resident_fits(int m, int R);
 
+// FAST-profile single-RHS loop (fastloop.cu): one streaming pass over the passive
+// columns of Q per iteration (one-pass update), fixed-tree reductions.
+struct FastPart {  // one CTA's partial sums of a state (and of the try that produced it)
+  double gbs, xg, qx, minx, df, el;
+  int cnt, bad, nchg, pad;
+};
+struct FastArgs {
+  const double* Q;  // blocked m x m (gemv.cuh blk_index, block rows R)
+  int m;
+  int R;
+  const double* q;
+  double* x[2];     // ping-pong states; [0] holds the start point
+  double* g[2];
+  double* gbar[2];  // g on the passive set, 0 elsewhere (m)
+  FastPart* part[2];  // [nblk] per state slot
+  double* den;      // [nblk]
+  uint32_t* kl;     // [nblk * R] clamped columns per CTA
+  double* kv;       // [nblk * R] their coefficients alpha g - x
+  int* kc;          // [nblk]
+  double eps;
+  uint64_t max_iters;
+  int has_time_cap;
+  double time_cap_s;
+  uint64_t stall_window;
+  uint64_t trace_every;
+  alnnls_iter_record* trace;
+  uint64_t trace_cap;
+  uint64_t* mults;
+  uint64_t mults_cap;
+  LoopCtrl* ctrl;
+};
+bool fast_loop_supported(int m, int R);
+cudaError_t launch_fast_loop(const FastArgs& a, cudaStream_t stream);
+
 // Exact masked GEMV over a row range: y[i] = sum_t M[i, list[t]] * vals[t].
 cudaError_t launch_masked_gemv(const double* M, uint64_t ld, int rows, const uint32_t* list,
                                const double* vals, int len, double* y, int sm_count,
@@ -189,6 +223,10 @@ cudaError_t launch_add(const double* y, const double* q, double* g, int m, cudaS
 // any non-finite entry among `count` doubles (strided columns) -> *flag = 1
 cudaError_t launch_check_finite(const double* p, uint64_t rows, uint64_t cols, uint64_t ld,
                                 int* flag, cudaStream_t stream);
+// kind 0: any asymmetric pair of the square rows x rows matrix, kind 1: any entry
+// that is not >= 0 (negative or NaN) -> *flag = 1
+cudaError_t launch_check_matrix(const double* p, uint64_t rows, uint64_t cols, uint64_t ld,
+                                int kind, int* flag, cudaStream_t stream);
 // pads: copy a rows x cols col-major block into a buffer with leading dimension ld_dst.
 cudaError_t launch_copy_pad(const double* src, uint64_t ld_src, double* dst, uint64_t ld_dst,
                             uint64_t rows, uint64_t cols, cudaStream_t stream);

@@ -315,7 +315,7 @@ __device__ void write_record(const LoopArgs& a, unsigned long long k, double f, 
                              int pc, double elapsed, double alpha, int has_alpha) {
   LoopCtrl* c = a.ctrl;
   const unsigned long long idx = c->trace_len;
-  if (idx < a.trace_cap) {
+  if (a.trace_cap > 0) {  // past the capacity the last slot keeps the newest record
     alnnls_iter_record r;
     r.iter = k;
     r.f = f;
@@ -324,7 +324,7 @@ __device__ void write_record(const LoopArgs& a, unsigned long long k, double f, 
     r.elapsed_s = elapsed;
     r.alpha = has_alpha ? alpha : 0.0;
     r.has_alpha = has_alpha;
-    a.trace[idx] = r;
+    a.trace[idx < a.trace_cap ? idx : a.trace_cap - 1] = r;
   }
   c->trace_len = idx + 1;
 }
@@ -1161,27 +1161,22 @@ int nqp_rows_per_cta(int m, int sm_count) {
 // CTAs, non-portable sizes allowed, and the occupancy query finds a GPC for it),
 // else a cooperative grid.
 template <class KC, class KG>
-cudaError_t launch_loop(KC kcluster, KG kgrid, bool& attr_set, bool& cluster_ok,
-                        const LoopArgs& a, int num_ctas, cudaStream_t stream) {
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kgrid, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)nqp_loop_smem_bytes());
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kcluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)nqp_loop_smem_bytes());
-    if (e != cudaSuccess) return e;
-    cluster_ok =
-        cudaFuncSetAttribute(kcluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-        cudaSuccess;
-    (void)cudaGetLastError();
-    attr_set = true;
-  }
+cudaError_t launch_loop(KC kcluster, KG kgrid, const LoopArgs& a, int num_ctas,
+                        cudaStream_t stream, size_t smem_bytes = nqp_loop_smem_bytes(),
+                        int threads = kLoopThreads) {
+  // attributes are per device (func_attr_once keys them by the current device)
+  if (cudaError_t e = smem_optin(kgrid, (int)smem_bytes)) return e;
+  if (cudaError_t e = smem_optin(kcluster, (int)smem_bytes)) return e;
+  const bool cluster_ok =
+      func_attr_once(reinterpret_cast<const void*>(kcluster),
+                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+  (void)cudaGetLastError();
   LoopArgs args = a;
   if (cluster_ok && num_ctas <= 16) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(num_ctas);
-    cfg.blockDim = dim3(kLoopThreads);
-    cfg.dynamicSmemBytes = nqp_loop_smem_bytes();
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem_bytes;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1196,14 +1191,12 @@ cudaError_t launch_loop(KC kcluster, KG kgrid, bool& attr_set, bool& cluster_ok,
     (void)cudaGetLastError();  // no cluster of this size fits: cooperative grid instead
   }
   void* params[] = {&args};
-  return cudaLaunchCooperativeKernel((void*)kgrid, dim3(num_ctas), dim3(kLoopThreads), params,
-                                     nqp_loop_smem_bytes(), stream);
+  return cudaLaunchCooperativeKernel((void*)kgrid, dim3(num_ctas), dim3(threads), params,
+                                     smem_bytes, stream);
 }
 
 cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream) {
-  static bool attr_set = false, cluster_ok = false;
-  return launch_loop(nqp_loop_kernel<true>, nqp_loop_kernel<false>, attr_set, cluster_ok, a,
-                     num_ctas, stream);
+  return launch_loop(nqp_loop_kernel<true>, nqp_loop_kernel<false>, a, num_ctas, stream);
 }
 
 // ---- standalone masked GEMV (masked_matvec / matvec / residual / warm start) ------------
@@ -1229,14 +1222,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1)
 cudaError_t gemv_launch(const double* M, uint64_t ld, int rows, int rpc, int blocked,
                         const uint32_t* list, const double* vals, int len, double* y,
                         cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(masked_gemv_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)nqp_loop_smem_bytes());
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (cudaError_t e = smem_optin(masked_gemv_kernel, (int)nqp_loop_smem_bytes())) return e;
   if (rows <= 0) return cudaSuccess;
   if (rpc > 352) return cudaErrorInvalidValue;  // 11 consumer warps + 1 producer
   const int grid = (rows + rpc - 1) / rpc;
@@ -1266,19 +1252,11 @@ cudaError_t launch_masked_gemv_blocked(const double* Qb, int m, int R, const uin
 
 namespace alnnls {
 cudaError_t launch_acc_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream) {
-  static bool attr_set = false, cluster_ok = false;
-  return launch_loop(acc_loop_kernel<true>, acc_loop_kernel<false>, attr_set, cluster_ok, a,
-                     num_ctas, stream);
+  return launch_loop(acc_loop_kernel<true>, acc_loop_kernel<false>, a, num_ctas, stream);
 }
 
 cudaError_t launch_frobenius(const double* Qb, int m, int R, double* out, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(frobenius_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)nqp_loop_smem_bytes());
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (cudaError_t e = smem_optin(frobenius_kernel, (int)nqp_loop_smem_bytes())) return e;
   frobenius_kernel<<<1, kLoopThreads, nqp_loop_smem_bytes(), stream>>>(Qb, m, R, out);
   return cudaGetLastError();
 }

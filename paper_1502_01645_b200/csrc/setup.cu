@@ -529,6 +529,26 @@ __global__ void check_finite_kernel(const double* p, uint64_t rows, uint64_t col
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
 }
 
+// Device-side checks of NqpProblem (nqp.hpp:37-41) and the warm start
+// (nqp.hpp:227-230) for the device-pointer entries. kind 0: exact symmetry of the
+// m x m matrix (ld), kind 1: every entry >= 0 (NaN fails).
+__global__ void check_matrix_kernel(const double* p, uint64_t rows, uint64_t cols, uint64_t ld,
+                                    int kind, int* flag) {
+  const uint64_t total = rows * cols;
+  int bad = 0;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = e / rows, r = e % rows;
+    const double v = p[c * ld + r];
+    if (kind == 0) {
+      if (r < c && !(v == p[r * ld + c])) bad = 1;
+    } else if (!(v >= 0.0)) {
+      bad = 1;
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
 __global__ void copy_pad_kernel(const double* src, uint64_t ld_src, double* dst, uint64_t ld_dst,
                                 uint64_t rows, uint64_t cols) {
   const uint64_t total = rows * cols;
@@ -571,14 +591,7 @@ cudaError_t launch_from_blocked(const double* src, int m, int R, double* dst, ui
 
 cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream) {
   if (s.n <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(colchain_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kColChainSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = smem_optin(colchain_kernel, (int)kColChainSmem)) return e;
   colchain_kernel<<<(s.n + 31) / 32, 256, kColChainSmem, stream>>>(
       s.A, s.lda, s.d, s.n, s.b, s.diag, s.b ? s.hvec_scratch : nullptr, nullptr);
   return cudaGetLastError();
@@ -587,14 +600,7 @@ cudaError_t launch_gram_diag(const SetupArgs& s, cudaStream_t stream) {
 cudaError_t launch_atb_chain(const double* A, uint64_t lda, int rows, int n, const double* b,
                              const double* atb0, double* atb, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(colchain_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kColChainSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = smem_optin(colchain_kernel, (int)kColChainSmem)) return e;
   colchain_kernel<<<(n + 31) / 32, 256, kColChainSmem, stream>>>(A, lda, rows, n, b, nullptr, atb,
                                                                  atb0);
   return cudaGetLastError();
@@ -660,16 +666,8 @@ cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream) {
   const int nt = (s.n + BM - 1) / BM;
   const int tiles = mode == 2 ? nt * ((s.nrhs + BM - 1) / BM) : nt * (nt + 1) / 2;
   if (tiles == 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(syrk_exact_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(syrk_streamk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kSyrkSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = smem_optin(syrk_exact_kernel, (int)kSyrkSmem)) return e;
+  if (cudaError_t e = smem_optin(syrk_streamk_kernel, (int)kSyrkSmem)) return e;
   if (s.sk_part && s.sk_flag && s.sk_ctas > 0) {
     cudaError_t e = cudaMemsetAsync(s.sk_flag, 0, sizeof(int) * s.sk_ctas, stream);
     if (e != cudaSuccess) return e;
@@ -733,6 +731,15 @@ cudaError_t launch_check_finite(const double* p, uint64_t rows, uint64_t cols, u
   return cudaGetLastError();
 }
 
+cudaError_t launch_check_matrix(const double* p, uint64_t rows, uint64_t cols, uint64_t ld,
+                                int kind, int* flag, cudaStream_t stream) {
+  if (rows * cols == 0) return cudaSuccess;
+  uint64_t blocks = (rows * cols + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  check_matrix_kernel<<<(unsigned)blocks, 256, 0, stream>>>(p, rows, cols, ld, kind, flag);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy_pad(const double* src, uint64_t ld_src, double* dst, uint64_t ld_dst,
                             uint64_t rows, uint64_t cols, cudaStream_t stream) {
   if (rows * cols == 0) return cudaSuccess;
@@ -752,13 +759,7 @@ uint64_t gram_tiles(uint64_t n) {
 cudaError_t launch_syrk_rowblock(const SetupArgs& s, int tile_lo, int ntiles, const double* pin,
                                  double* pout, cudaStream_t stream) {
   if (ntiles <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(syrk_rowblock_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = smem_optin(syrk_rowblock_kernel, (int)kSyrkSmem)) return e;
   syrk_rowblock_kernel<<<ntiles, NT, kSyrkSmem, stream>>>(s, tile_lo, pin, pout);
   return cudaGetLastError();
 }

@@ -27,6 +27,17 @@ def row_split(d, world):
     return out
 
 
+def _finish_send(work, device):
+    """Blocks the HOST until an isend has completed. With NCCL, Work.wait() only
+    makes torch's current stream wait for the collective stream; the compute
+    callbacks write their output buffers on the library's own stream, which is
+    not ordered after that wait, so reusing a send buffer needs the host to see
+    the send finish first (gloo's wait() already blocks the host)."""
+    work.wait()
+    if torch.device(device).type == "cuda":
+        torch.cuda.current_stream(torch.device(device)).synchronize()
+
+
 def pipelined_gram(dist, rank, world, ntiles, batch, tile_doubles, compute, device,
                    sync=None):
     """Runs the row-block Gram pipeline over `ntiles` tiles in batches.
@@ -66,14 +77,14 @@ def pipelined_gram(dist, rank, world, ntiles, batch, tile_doubles, compute, devi
             compute(t0, t1, pin, None)
         else:
             if b >= 2 and sends[b - 2] is not None:
-                sends[b - 2].wait()  # bout[b % 2] is free again
+                _finish_send(sends[b - 2], device)  # bout[b % 2] is free again
                 sends[b - 2] = None
             pout = bout[b % 2][:cnt]
             compute(t0, t1, pin, pout)
             sends[b] = dist.isend(pout, dst=rank + 1)
     for w in sends:
         if w is not None:
-            w.wait()
+            _finish_send(w, device)
 
 
 def chain_relay(dist, rank, world, state, compute, sync=None):
