@@ -17,7 +17,7 @@ namespace alnnls {
 
 constexpr int kMaxThreads = 512;
 
-// cudaFuncSetAttribute once per (kernel, attribute, device). Function attributes
+// cudaFuncSetAttribute once per (kernel, attribute, value, device). Function attributes
 // are per device, and one process may drive several devices (one context per
 // GPU), so a process-wide "done" flag would leave the second device's launches
 // without the shared-memory opt-in. Thread-safe.
@@ -26,9 +26,9 @@ inline cudaError_t func_attr_once(const void* func, cudaFuncAttribute attr, int 
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   static std::mutex mu;
-  static std::set<std::tuple<const void*, int, int>> done;
+  static std::set<std::tuple<const void*, int, int, int>> done;
   std::lock_guard<std::mutex> lk(mu);
-  const auto key = std::make_tuple(func, (int)attr, dev);
+  const auto key = std::make_tuple(func, (int)attr, value, dev);
   if (done.count(key)) return cudaSuccess;
   e = cudaFuncSetAttribute(func, attr, value);
   if (e == cudaSuccess) done.insert(key);

@@ -34,6 +34,8 @@
 // itself, in the same fixed order, so every decision is taken identically
 // everywhere with no broadcast.
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemv.cuh"
@@ -45,15 +47,26 @@ namespace alnnls {
 
 namespace {
 
-constexpr int kFT = 512;            // threads per CTA
+#ifndef ALNNLS_FAST_THREADS
+#define ALNNLS_FAST_THREADS 512  // build knob: threads per CTA (256 / 384 measured slower)
+#endif
+#ifndef ALNNLS_FAST_PHASES
+#define ALNNLS_FAST_PHASES 1  // build knob: CTA 0 phase clock
+#endif
+#ifndef ALNNLS_FAST_UNROLL
+#define ALNNLS_FAST_UNROLL 8     // build knob: candidate columns per thread per batch
+#endif
+constexpr int kFT = ALNNLS_FAST_THREADS;  // threads per CTA
 constexpr int kFW = kFT / 32;
 constexpr int kKWin = 1024;         // clamped-set window staged in shared memory
-constexpr int kRedDoubles = 1024;   // C x R column-group partials (C = kFT / (R/2))
-constexpr int kFastMaxBlk = 256;
+constexpr int kRedDoubles = 2 * kFT;  // C x R column-group partials (C = kFT / (R/2))
+constexpr int kRecPerLane = 5;     // per-CTA records a lane reduces (nblk <= 160)
+constexpr int kFastMaxBlk = 32 * kRecPerLane;
 
-__host__ __device__ inline size_t fast_smem_bytes(int m) {
+// gbar (m) [+ x (m) when local_k] + column-group partials + the K window
+__host__ __device__ inline size_t fast_smem_bytes(int m, bool local_k) {
   const size_t mp = ((size_t)m + 1) & ~(size_t)1;
-  return mp * sizeof(double) + kRedDoubles * sizeof(double) +
+  return mp * sizeof(double) * (local_k ? 2 : 1) + (kRedDoubles + kFT) * sizeof(double) +
          kKWin * (sizeof(double) + sizeof(uint32_t));
 }
 
@@ -64,6 +77,8 @@ struct FastShared {
   double den;
   int kpre[kFastMaxBlk + 1];
   int scan[40];
+  unsigned long long ph[8];  // CTA 0 phase clock
+  uint64_t sbar;             // mbarrier of the bulk-copy staging
 };
 
 template <bool kCluster>
@@ -92,10 +107,14 @@ __device__ __forceinline__ double2 ldq2(const double* p) {
 
 // Thread (rp, c) accumulates rows (2rp, 2rp+1) over columns j = c, c+C, ... of
 // the panel with coefficients w[j] (skipping w[j] == 0: no load).
+// Thread (rp, c) accumulates rows (2rp, 2rp+1) over columns j = c, c+C, ... of
+// the panel with coefficients w[j] (skipping w[j] == 0: no load). (A running-
+// pointer form of this loop measured 2.6x slower at 512 threads: the 128-register
+// budget then rematerializes the panel base per load.)
 __device__ __forceinline__ void panel_pass(const double* __restrict__ Qp, int R, int m,
                                            const double* __restrict__ w, int c, int C, int r2,
                                            double& acc0, double& acc1) {
-  constexpr int U = 8;
+  constexpr int U = ALNNLS_FAST_UNROLL;
   const double* base = Qp + r2;
   int j = c;
   for (; j + (U - 1) * C < m; j += U * C) {
@@ -127,26 +146,44 @@ __device__ __forceinline__ void list_pass(const double* __restrict__ Qp, int R,
                                           const uint32_t* __restrict__ kj,
                                           const double* __restrict__ kv, int len, int c, int C,
                                           int r2, double& acc0, double& acc1) {
+  constexpr int U = 4;  // independent loads in flight per thread
   const double* base = Qp + r2;
-  for (int t = c; t < len; t += C) {
-    const double2 qv = ldq2(base + (size_t)kj[t] * R);
-    acc0 = fma(qv.x, kv[t], acc0);
-    acc1 = fma(qv.y, kv[t], acc1);
+  for (int t = c; t < len; t += U * C) {
+    double2 qv[U];
+    double cv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int tt = t + u * C;
+      cv[u] = tt < len ? kv[tt] : 0.0;
+      qv[u] = tt < len ? ldq2(base + (size_t)kj[tt] * R) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc0 = fma(qv[u].x, cv[u], acc0);
+      acc1 = fma(qv[u].y, cv[u], acc1);
+    }
   }
 }
 
-// Column-group partials -> per-row sums: row t (thread t < nrows) adds the C
-// partials in ascending group order (fixed).
-__device__ __forceinline__ double rows_from_groups(double* red, bool gthr, int c, int R, int r2,
-                                                   double acc0, double acc1, int C, int nrows) {
+// Column-group partials -> per-row sums, a fixed tree: L lanes per row (the
+// largest power of two with L*R <= kFT) each add every L-th group partial, then
+// an xor-shuffle tree over the L lanes; row t's sum lands in thread t (t < nrows).
+// `rs` is R doubles of shared memory.
+__device__ __forceinline__ double rows_from_groups(double* red, double* rs, bool gthr, int c,
+                                                   int R, int r2, double acc0, double acc1, int C,
+                                                   int nrows) {
   if (gthr) *reinterpret_cast<double2*>(red + (size_t)c * R + r2) = make_double2(acc0, acc1);
   __syncthreads();
+  int L = 1;
+  while (2 * L * R <= kFT && L < 32) L *= 2;
+  const int r = threadIdx.x / L, sub = threadIdx.x % L;
   double s = 0.0;
-  if ((int)threadIdx.x < nrows) {
-    for (int k = 0; k < C; ++k) s += red[(size_t)k * R + threadIdx.x];
-  }
+  if (r < nrows)
+    for (int k = sub; k < C; k += L) s += red[(size_t)k * R + r];
+  for (int o = L / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (r < nrows && sub == 0) rs[r] = s;
   __syncthreads();
-  return s;
+  return (int)threadIdx.x < nrows ? rs[threadIdx.x] : 0.0;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -201,74 +238,122 @@ __device__ void write_partials(FastPart* dst, FastShared& S, double gbs, double 
     S.wint[w][2] = nchg;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    FastPart p;
-    p.gbs = p.xg = p.qx = p.df = 0.0;
-    p.minx = __longlong_as_double(0x7ff0000000000000LL);
-    p.cnt = p.bad = p.nchg = 0;
-    for (int k = 0; k < kFW; ++k) {
-      p.gbs += S.wred[k][0];
-      p.xg += S.wred[k][1];
-      p.qx += S.wred[k][2];
-      p.minx = fmin(p.minx, S.wred[k][3]);
-      p.df += S.wred[k][4];
-      p.cnt += S.wint[k][0];
-      p.bad |= S.wint[k][1];
-      p.nchg += S.wint[k][2];
+  if (w == 0) {  // lane l < kFW takes warp l's partials, then a fixed xor tree
+    const bool on = lane < kFW;
+    double v0 = on ? S.wred[lane][0] : 0.0, v1 = on ? S.wred[lane][1] : 0.0;
+    double v2 = on ? S.wred[lane][2] : 0.0, v4 = on ? S.wred[lane][4] : 0.0;
+    double v3 = on ? S.wred[lane][3] : __longlong_as_double(0x7ff0000000000000LL);
+    int i0 = on ? S.wint[lane][0] : 0, i1 = on ? S.wint[lane][1] : 0, i2 = on ? S.wint[lane][2] : 0;
+    v0 = warp_sum(v0);
+    v1 = warp_sum(v1);
+    v2 = warp_sum(v2);
+    v4 = warp_sum(v4);
+    v3 = warp_min(v3);
+    i0 = warp_isum(i0);
+    i1 = __any_sync(0xffffffffu, i1 != 0) ? 1 : 0;
+    i2 = warp_isum(i2);
+    if (lane == 0) {
+      FastPart p;
+      p.gbs = v0;
+      p.xg = v1;
+      p.qx = v2;
+      p.minx = v3;
+      p.df = v4;
+      p.cnt = i0;
+      p.bad = i1;
+      p.nchg = i2;
+      p.el = el;
+      p.pad = 0;
+      *dst = p;
     }
-    p.el = el;
-    p.pad = 0;
-    *dst = p;
   }
   __syncthreads();
 }
 
 // Totals over the nblk per-CTA records (every CTA, same fixed order): warp 0,
 // lane l sums records l, l+32, ... then an xor tree. el is record 0's.
+// Totals over the nblk per-CTA records, every CTA in the same fixed order.
+// Called by warps 0..3 (the caller synchronizes the CTA afterwards): warp w
+// reduces the w-th 16-byte field pair of every record; lane l takes records
+// l, l+32, ... and issues all its loads before the first add (one L2 round trip).
+constexpr int kRedWarps = 4;
 __device__ void reduce_partials(const FastPart* src, int nblk, FastShared& S) {
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double gbs = 0.0, xg = 0.0, qx = 0.0, df = 0.0;
-    double mnx = __longlong_as_double(0x7ff0000000000000LL);
-    int cnt = 0, bad = 0, nchg = 0;
-    for (int b = lane; b < nblk; b += 32) {
-      const FastPart* p = src + b;
-      gbs += __ldcg(&p->gbs);
-      xg += __ldcg(&p->xg);
-      qx += __ldcg(&p->qx);
-      df += __ldcg(&p->df);
-      mnx = fmin(mnx, __ldcg(&p->minx));
-      cnt += __ldcg(&p->cnt);
-      bad |= __ldcg(&p->bad);
-      nchg += __ldcg(&p->nchg);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double2 v[kRecPerLane];
+#pragma unroll
+  for (int r = 0; r < kRecPerLane; ++r) {
+    const int b = lane + 32 * r;
+    v[r] = b < nblk ? __ldcg(reinterpret_cast<const double2*>(src + b) + w)
+                    : make_double2(0.0, 0.0);
+  }
+  if (w == 0 || w == 2) {  // (gbs, xg) or (df, el): sums; el is record 0's
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int r = 0; r < kRecPerLane; ++r) {
+      a0 += v[r].x;
+      a1 += v[r].y;
     }
-    gbs = warp_sum(gbs);
-    xg = warp_sum(xg);
-    qx = warp_sum(qx);
-    df = warp_sum(df);
-    mnx = warp_min(mnx);
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    const double el0 = __shfl_sync(0xffffffffu, v[0].y, 0);
+    if (lane == 0) {
+      if (w == 0) {
+        S.tot.gbs = a0;
+        S.tot.xg = a1;
+      } else {
+        S.tot.df = a0;
+        S.tot.el = el0;
+      }
+    }
+  } else if (w == 1) {     // (qx, minx)
+    double a0 = 0.0, mn = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+    for (int r = 0; r < kRecPerLane; ++r) {
+      a0 += v[r].x;
+      if (lane + 32 * r < nblk) mn = fmin(mn, v[r].y);
+    }
+    a0 = warp_sum(a0);
+    mn = warp_min(mn);
+    if (lane == 0) {
+      S.tot.qx = a0;
+      S.tot.minx = mn;
+    }
+  } else {                 // (cnt | bad, nchg | pad)
+    int cnt = 0, bad = 0, nchg = 0;
+#pragma unroll
+    for (int r = 0; r < kRecPerLane; ++r) {
+      const long long w0 = __double_as_longlong(v[r].x), w1 = __double_as_longlong(v[r].y);
+      cnt += (int)(w0 & 0xffffffffLL);
+      bad |= (int)(w0 >> 32);
+      nchg += (int)(w1 & 0xffffffffLL);
+    }
     cnt = warp_isum(cnt);
     bad = __any_sync(0xffffffffu, bad != 0) ? 1 : 0;
     nchg = warp_isum(nchg);
     if (lane == 0) {
-      S.tot.gbs = gbs;
-      S.tot.xg = xg;
-      S.tot.qx = qx;
-      S.tot.df = df;
-      S.tot.minx = mnx;
       S.tot.cnt = cnt;
       S.tot.bad = bad;
       S.tot.nchg = nchg;
-      S.tot.el = __ldcg(&src[0].el);
     }
   }
-  __syncthreads();
 }
 
-__device__ void fast_record(const FastArgs& a, unsigned long long k, double f, double gbs, int pc,
-                            double el, double alpha, int has_alpha) {
-  LoopCtrl* c = a.ctrl;
-  const unsigned long long idx = c->trace_len;
+// Sum of the nblk per-CTA den partials (warp 0; one L2 round trip, fixed order).
+__device__ __forceinline__ double reduce_den(const double* den, int nblk) {
+  const int lane = threadIdx.x & 31;
+  double v[kRecPerLane];
+#pragma unroll
+  for (int r = 0; r < kRecPerLane; ++r) v[r] = lane + 32 * r < nblk ? __ldcg(den + lane + 32 * r) : 0.0;
+  double sd = 0.0;
+#pragma unroll
+  for (int r = 0; r < kRecPerLane; ++r) sd += v[r];
+  return warp_sum(sd);
+}
+
+// Trace record (CTA 0 thread 0; the counters live in its registers, not in the
+// control block, so no global load sits on the iteration's critical path).
+__device__ void fast_record(const FastArgs& a, unsigned long long& idx, unsigned long long k,
+                            double f, double gbs, int pc, double el, double alpha, int has_alpha) {
   if (a.trace_cap > 0) {  // past the capacity the last slot keeps the newest record
     alnnls_iter_record r;
     r.iter = k;
@@ -280,7 +365,7 @@ __device__ void fast_record(const FastArgs& a, unsigned long long k, double f, d
     r.has_alpha = has_alpha;
     a.trace[idx < a.trace_cap ? idx : a.trace_cap - 1] = r;
   }
-  c->trace_len = idx + 1;
+  ++idx;
 }
 
 template <bool kCluster>
@@ -292,9 +377,13 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
   const int b = blockIdx.x, nblk = gridDim.x;
   const int row0 = b * R;
   const int nrows = max(0, min(m - row0, R));
+  const int mp = (m + 1) & ~1;
+  const bool lk = a.local_k != 0;  // x staged too: every CTA finds K itself (no barrier A2)
   double* gs = reinterpret_cast<double*>(smem);                   // gbar of the state, m
-  double* red = gs + ((m + 1) & ~1);                              // kRedDoubles
-  double* kvs = red + kRedDoubles;                                // kKWin coefficients
+  double* xs = gs + mp;                                           // x of the state (lk), m
+  double* red = xs + (lk ? mp : 0);                               // kRedDoubles
+  double* rsum = red + kRedDoubles;                               // R row sums
+  double* kvs = rsum + kFT;                                       // kKWin coefficients
   uint32_t* kjs = reinterpret_cast<uint32_t*>(kvs + kKWin);       // kKWin columns
   const double* Qp = a.Q + (size_t)b * R * m;
   const int RP = R / 2;
@@ -305,6 +394,7 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
   const bool own = (int)threadIdx.x < nrows;
   const int i = row0 + threadIdx.x;
   const bool lead = b == 0 && threadIdx.x == 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t t0 = globaltimer_ns();
 
   // ---- this thread's row of the current state --------------------------------------
@@ -314,36 +404,84 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
     gi = a.g[0][i];
     qi = a.q[i];
   }
-  auto publish_state = [&](int slot, double xs, double gsv, double df, int chg, bool wr) {
-    // gbar, x, g of own rows and this CTA's partials of the state (xs, gsv)
-    const bool pf = own && (xs > 0.0 || gsv < 0.0);
-    if (own && wr) {
-      a.x[slot][i] = xs;
-      a.g[slot][i] = gsv;
+  auto publish_state = [&](int slot, double xv, double gv, double df, int chg, bool wr) {
+    // gbar, x, g of own rows and this CTA's partials of the state (xv, gv)
+    const bool pf = own && (xv > 0.0 || gv < 0.0);
+    if (own) {
+      if (wr) {
+        a.x[slot][i] = xv;
+        a.g[slot][i] = gv;
+      }
+      a.gbar[slot][i] = pf ? gv : 0.0;
     }
-    if (own) a.gbar[slot][i] = pf ? gsv : 0.0;
     const double el = lead ? (double)(globaltimer_ns() - t0) * 1e-9 : 0.0;
-    write_partials(a.part[slot] + b, S, pf ? gsv * gsv : 0.0, own ? xs * gsv : 0.0,
-                   own ? qi * xs : 0.0,
-                   own ? xs : __longlong_as_double(0x7ff0000000000000LL), df, el,
-                   pf ? 1 : 0, own && !isfinite(gsv) ? 1 : 0, chg);
+    write_partials(a.part[slot] + b, S, pf ? gv * gv : 0.0, own ? xv * gv : 0.0,
+                   own ? qi * xv : 0.0,
+                   own ? xv : __longlong_as_double(0x7ff0000000000000LL), df, el,
+                   pf ? 1 : 0, own && !isfinite(gv) ? 1 : 0, chg);
+  };
+  // stage gbar (and x) of state `slot` into shared memory with threads [first, kFT)
+  // Staging of gbar (and x) of state `slot` into shared memory: ONE thread issues
+  // bulk copies (cp.async.bulk, TMA 1D) completing on an mbarrier, so the staging
+  // needs no registers and costs one round trip; the other warps meanwhile reduce
+  // the partials. (Vectors are padded to even length: the byte counts are
+  // multiples of 16.)
+  uint32_t sphase = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&S.sbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto stage_issue = [&](int slot) {
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t bytes = (uint32_t)mp * 8u;
+      mbar_arrive_expect_tx(&S.sbar, lk ? 2u * bytes : bytes);
+      constexpr uint32_t kChunk = 65536;
+      for (uint32_t off = 0; off < bytes; off += kChunk) {
+        const uint32_t nb = bytes - off < kChunk ? bytes - off : kChunk;
+        bulk_g2s(reinterpret_cast<uint8_t*>(gs) + off,
+                 reinterpret_cast<const uint8_t*>(a.gbar[slot]) + off, nb, &S.sbar);
+        if (lk)
+          bulk_g2s(reinterpret_cast<uint8_t*>(xs) + off,
+                   reinterpret_cast<const uint8_t*>(a.x[slot]) + off, nb, &S.sbar);
+      }
+    }
+  };
+  auto stage_wait = [&]() {
+    mbar_wait(&S.sbar, sphase);
+    sphase ^= 1u;
   };
   int cur = 0;
   publish_state(0, xi, gi, 0.0, 0, false);
-  if (lead) {
-    a.ctrl->trace_len = 0;
-    a.ctrl->mult_len = 0;
-    a.ctrl->mult_total = 0;
-    a.ctrl->numeric_failure = 0;
-  }
+  // lead-thread counters (written to the control block at the end)
+  unsigned long long n_trace = 0, n_mult = 0, mult_total = 0;
+  double min_it = 0.0;
   bar.sync();
-  reduce_partials(a.part[0], nblk, S);
-  if (lead) a.ctrl->min_iterate = m ? S.tot.minx : 0.0;  // min(start) (nqp.hpp:237)
+  stage_issue(0);
+  if (warp < kRedWarps) reduce_partials(a.part[0], nblk, S);
+  __syncthreads();
+  stage_wait();
+  min_it = m ? S.tot.minx : 0.0;  // min(start) (nqp.hpp:237)
   double best_gbs = __longlong_as_double(0x7ff0000000000000LL);
   unsigned long long since_best = 0;
   double el = S.tot.el;
+  // CTA 0 thread 0 phase clock (alnnls_get_phase_ns): [0] stop test, [1] Q gbar pass
+  // + den partial, [2] barrier A + den, [3] clamped set (+ barrier A2 without lk),
+  // [4] Q_K c_K pass, [5] update + partials, [6] barrier B + totals + staging
+  if (threadIdx.x < 8) S.ph[threadIdx.x] = 0;
+  unsigned long long tmark = globaltimer_ns();
+  auto mark = [&](int idx) {
+    if (ALNNLS_FAST_PHASES && lead) {
+      const unsigned long long t = globaltimer_ns();
+      S.ph[idx] += t - tmark;
+      tmark = t;
+    }
+  };
 
-  for (unsigned long long k = 0;; ++k) {
+  unsigned long long tsamp = 0;  // k % trace_every, kept incrementally
+  for (unsigned long long k = 0;; ++k, tsamp = tsamp + 1 == a.trace_every ? 0 : tsamp + 1) {
     // ===== stop tests on the current state (nqp.hpp:249-275), identical in every CTA ====
     const double gbs = S.tot.gbs;
     const double f = 0.5 * (S.tot.xg + S.tot.qx);
@@ -371,7 +509,7 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
         if (stop == 100) {
           a.ctrl->numeric_failure = 1;
         } else {
-          fast_record(a, k, f, gbs, ml, el, 0.0, 0);
+          fast_record(a, n_trace, k, f, gbs, ml, el, 0.0, 0);
           a.ctrl->termination = stop;
           a.ctrl->iterations = k;
           a.ctrl->f_final = f;
@@ -380,32 +518,28 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
       }
       break;
     }
+    mark(0);
 
     // ===== u = Q gbar over own rows (one streaming pass over the passive columns) =====
-    {
-      const double* src = a.gbar[cur];
-      for (int e = threadIdx.x; e < m; e += kFT) gs[e] = __ldcg(src + e);
-    }
-    __syncthreads();
     double acc0 = 0.0, acc1 = 0.0;
     if (gthr) panel_pass(Qp, R, m, gs, grp, C, r2, acc0, acc1);
-    const double ui = rows_from_groups(red, gthr, grp, R, r2, acc0, acc1, C, nrows);
+    const double ui = rows_from_groups(red, rsum, gthr, grp, R, r2, acc0, acc1, C, nrows);
     {
       const double dn = block_sum(own ? gs[i] * ui : 0.0, S);
       if (threadIdx.x == 0) a.den[b] = dn;
     }
+    mark(1);
     bar.sync();  // A
-    if (threadIdx.x < 32) {
-      double s = 0.0;
-      for (int bb = threadIdx.x; bb < nblk; bb += 32) s += __ldcg(a.den + bb);
-      s = warp_sum(s);
-      if (threadIdx.x == 0) S.den = s;
+    if (warp == 0) {
+      const double sd = reduce_den(a.den, nblk);
+      if (lane == 0) S.den = sd;
     }
     __syncthreads();
+    mark(2);
     const double den = S.den;
     if (!(den > 0.0)) {  // exact_step returns nullopt (nqp.hpp:171) -> ZeroCurvature
       if (lead) {
-        fast_record(a, k, f, gbs, ml, el, 0.0, 0);
+        fast_record(a, n_trace, k, f, gbs, ml, el, 0.0, 0);
         a.ctrl->termination = ALNNLS_ZERO_CURVATURE;
         a.ctrl->iterations = k;
         a.ctrl->f_final = f;
@@ -418,40 +552,89 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
     const bool pas = own && (xi > 0.0 || gi < 0.0);
     const int nxt = cur ^ 1;
     for (int tries = 0;; ++tries) {
-      // ---- clamped set K of own rows: x_i - alpha g_i < 0 on P (nqp.hpp:295-296) ----
-      const double ag = alpha * gi;
-      const bool clamp = pas && gi > 0.0 && xi < ag;
-      {
-        int tot = 0;
-        const int pos = block_exclusive_scan(clamp ? 1 : 0, S.scan, &tot);
-        if (clamp) {
-          a.kl[(size_t)b * R + pos] = (uint32_t)i;
-          a.kv[(size_t)b * R + pos] = ag - xi;  // c_i = delta_i + alpha g_i
+      // ---- clamped set K: x_j - alpha g_j < 0 on P (nqp.hpp:295-296), ascending j ----
+      // (on P with g_j > 0; g_j <= 0 never clamps). c_j = alpha g_j - x_j.
+      double v0 = 0.0, v1 = 0.0;
+      int ktot = 0;
+      if (lk) {
+        // every CTA scans the staged state: warp w owns a contiguous range, lanes
+        // read consecutive entries, a ballot per round keeps ascending order
+        const int pw = ((m + kFW - 1) / kFW + 31) & ~31;
+        const int j0 = warp * pw, j1 = min(m, j0 + pw);
+        int cnt = 0;
+        for (int jb = j0; jb < j1; jb += 32) {
+          const int j = jb + lane;
+          const double gv = j < j1 ? gs[j] : 0.0;
+          const bool cl = gv > 0.0 && xs[j] < alpha * gv;
+          cnt += __popc(__ballot_sync(0xffffffffu, cl));
         }
-        if (threadIdx.x == 0) a.kc[b] = tot;
-      }
-      bar.sync();  // A2
-      if (threadIdx.x < 32) {  // prefix of the per-CTA counts: K in ascending row order
-        int run = 0;
-        for (int b0 = 0; b0 < nblk; b0 += 32) {
-          const int bb = b0 + (int)threadIdx.x;
-          const int v = bb < nblk ? __ldcg(a.kc + bb) : 0;
-          int incl = v;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if ((int)threadIdx.x >= o) incl += t;
+        if (lane == 0) S.scan[warp] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          int run = 0;
+          for (int w = 0; w < kFW; ++w) {
+            const int c = S.scan[w];
+            S.scan[w] = run;
+            run += c;
           }
-          if (bb < nblk) S.kpre[bb] = run + incl - v;
-          run += __shfl_sync(0xffffffffu, incl, 31);
+          S.scan[kFW] = run;
         }
-        if (threadIdx.x == 0) S.kpre[nblk] = run;
-      }
-      __syncthreads();
-      const int ktot = S.kpre[nblk];
-      double vi = 0.0;
-      if (ktot > 0) {
-        double v0 = 0.0, v1 = 0.0;
+        __syncthreads();
+        ktot = S.scan[kFW];
+        mark(3);
+        for (int w0 = 0; w0 < ktot; w0 += kKWin) {  // windows of K (one unless |K| > kKWin)
+          int pos = S.scan[warp];
+          for (int jb = j0; jb < j1 && pos < w0 + kKWin; jb += 32) {
+            const int j = jb + lane;
+            const double gv = j < j1 ? gs[j] : 0.0;
+            const double ag = alpha * gv;
+            const bool cl = gv > 0.0 && xs[j] < ag;
+            const unsigned bl = __ballot_sync(0xffffffffu, cl);
+            const int p = pos + __popc(bl & ((1u << lane) - 1u));
+            if (cl && p >= w0 && p < w0 + kKWin) {
+              kjs[p - w0] = (uint32_t)j;
+              kvs[p - w0] = ag - xs[j];
+            }
+            pos += __popc(bl);
+          }
+          __syncthreads();
+          if (gthr) {
+            list_pass(Qp, R, kjs, kvs, min(kKWin, ktot - w0), grp, C, r2, v0, v1);
+          }
+          __syncthreads();
+        }
+      } else {
+        const double ag = alpha * gi;
+        const bool clamp = pas && gi > 0.0 && xi < ag;
+        {
+          int tot = 0;
+          const int pos = block_exclusive_scan(clamp ? 1 : 0, S.scan, &tot);
+          if (clamp) {
+            a.kl[(size_t)b * R + pos] = (uint32_t)i;
+            a.kv[(size_t)b * R + pos] = ag - xi;  // c_i = delta_i + alpha g_i
+          }
+          if (threadIdx.x == 0) a.kc[b] = tot;
+        }
+        bar.sync();  // A2
+        if (warp == 0) {  // prefix of the per-CTA counts: K in ascending row order
+          int run = 0;
+          for (int b0 = 0; b0 < nblk; b0 += 32) {
+            const int bb = b0 + lane;
+            const int v = bb < nblk ? __ldcg(a.kc + bb) : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int t = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += t;
+            }
+            if (bb < nblk) S.kpre[bb] = run + incl - v;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+          }
+          if (lane == 0) S.kpre[nblk] = run;
+        }
+        __syncthreads();
+        mark(3);
+        ktot = S.kpre[nblk];
         for (int w0 = 0; w0 < ktot; w0 += kKWin) {
           const int wn = min(kKWin, ktot - w0);
           for (int t = threadIdx.x; t < wn; t += kFT) {
@@ -467,12 +650,18 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
             kvs[t] = __ldcg(a.kv + e);
           }
           __syncthreads();
-          if (gthr) list_pass(Qp, R, kjs, kvs, wn, grp, C, r2, v0, v1);
+          if (gthr) {
+            list_pass(Qp, R, kjs, kvs, wn, grp, C, r2, v0, v1);
+          }
           __syncthreads();
         }
-        vi = rows_from_groups(red, gthr, grp, R, r2, v0, v1, C, nrows);
+      }
+      double vi = 0.0;
+      if (ktot > 0) {
+        vi = rows_from_groups(red, rsum, gthr, grp, R, r2, v0, v1, C, nrows);
         mults += (unsigned long long)m * (unsigned long long)ktot;
       }
+      mark(4);
       // ---- speculative update of own rows (nqp.hpp:294-313, one-pass Q delta) ----
       const double gd = fma(-alpha, ui, vi);
       double xn = xi, delta = 0.0;
@@ -487,60 +676,102 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
       const double gn = gi + gd;
       const double dft = chg ? (gi + 0.5 * gd) * delta : 0.0;
       publish_state(nxt, xn, gn, dft, chg ? 1 : 0, true);
+      mark(5);
       bar.sync();  // B
-      reduce_partials(a.part[nxt], nblk, S);
+      // totals of the new state (warp 0) while the other warps stage it speculatively
+      stage_issue(nxt);
+      if (warp < kRedWarps) reduce_partials(a.part[nxt], nblk, S);
+      __syncthreads();
+      stage_wait();
+      mark(6);
       el = S.tot.el;
       const int nchg = S.tot.nchg;
       const double df = S.tot.df;
       if (nchg == 0 || df <= 0.0 || tries >= 60) {
         // step taken (or too small to move anything, nqp.hpp:304): record it
         if (lead) {
-          if (k % a.trace_every == 0) fast_record(a, k, f, gbs, ml, el, alpha, 1);
-          const unsigned long long idx = a.ctrl->mult_len;
-          if (a.mults && a.mults_cap > 0) a.mults[idx < a.mults_cap ? idx : a.mults_cap - 1] = mults;
-          a.ctrl->mult_len = idx + 1;
-          a.ctrl->mult_total += mults;
+          if (tsamp == 0) fast_record(a, n_trace, k, f, gbs, ml, el, alpha, 1);
+          if (a.mults && a.mults_cap > 0)
+            a.mults[n_mult < a.mults_cap ? n_mult : a.mults_cap - 1] = mults;
+          ++n_mult;
+          mult_total += mults;
         }
         if (nchg != 0) {  // accept: the speculative state becomes current
-          if (lead && S.tot.minx < a.ctrl->min_iterate) a.ctrl->min_iterate = S.tot.minx;
+          if (S.tot.minx < min_it) min_it = S.tot.minx;
           xi = xn;
           gi = gn;
           cur = nxt;
         } else {          // nothing moved: the state (and its totals) stay
           __syncthreads();
-          reduce_partials(a.part[cur], nblk, S);
+          stage_issue(cur);
+          if (warp < kRedWarps) reduce_partials(a.part[cur], nblk, S);
+          __syncthreads();
+          stage_wait();
           if (threadIdx.x == 0) S.tot.el = el;
         }
         break;
       }
       alpha *= 0.5;  // nqp.hpp:317
+      __syncthreads();
+      stage_issue(cur);  // the rejected state was staged: back to the current one
+      stage_wait();
     }
     __syncthreads();
   }
-  if (lead) a.ctrl->g_parity = cur;
+  if (lead) {
+    a.ctrl->trace_len = n_trace;
+    a.ctrl->mult_len = n_mult;
+    a.ctrl->mult_total = mult_total;
+    a.ctrl->min_iterate = min_it;
+    a.ctrl->g_parity = cur;
+    for (int q = 0; q < 7; ++q) a.ctrl->phase_ns[q] = S.ph[q];
+  }
 }
-
 }  // namespace
 
+namespace {
+constexpr size_t kFastSmemCap = 227 * 1024;  // static + dynamic per CTA
+// static shared memory of the kernel as compiled (FastShared plus alignment)
+size_t fast_static_smem() {
+  static size_t v = [] {
+    cudaFuncAttributes fa{};
+    size_t mx = sizeof(FastShared) + 256;
+    if (cudaFuncGetAttributes(&fa, fast_loop_kernel<false>) == cudaSuccess && fa.sharedSizeBytes > mx)
+      mx = fa.sharedSizeBytes;
+    if (cudaFuncGetAttributes(&fa, fast_loop_kernel<true>) == cudaSuccess && fa.sharedSizeBytes > mx)
+      mx = fa.sharedSizeBytes;
+    (void)cudaGetLastError();
+    return mx;
+  }();
+  return v;
+}
+}
+
 bool fast_loop_supported(int m, int R) {
-  if (m < 1 || R < 2 || (R & 1) || R / 2 > kFT) return false;
+  if (m < 1 || R < 2 || (R & 1) || R > kFT) return false;  // one thread per own row
   const int nblk = (m + R - 1) / R;
   if (nblk > kFastMaxBlk || nblk > 148) return false;
   if ((kFT / (R / 2)) * R > kRedDoubles) return false;
-  return fast_smem_bytes(m) + sizeof(FastShared) <= 227 * 1024;
+  return fast_smem_bytes(m, false) + fast_static_smem() <= kFastSmemCap;
 }
 
-cudaError_t launch_fast_loop(const FastArgs& a, cudaStream_t stream) {
-  if (!fast_loop_supported(a.m, a.R)) return cudaErrorInvalidValue;
-  const int nblk = (a.m + a.R - 1) / a.R;
-  const size_t smem = fast_smem_bytes(a.m);
-  if (cudaError_t e = smem_optin(fast_loop_kernel<false>, (int)smem)) return e;
-  if (cudaError_t e = smem_optin(fast_loop_kernel<true>, (int)smem)) return e;
+cudaError_t launch_fast_loop(const FastArgs& a0, cudaStream_t stream) {
+  if (!fast_loop_supported(a0.m, a0.R)) return cudaErrorInvalidValue;
+  FastArgs args = a0;
+  // x staged beside gbar when both fit: the clamped set is then found by every CTA
+  // from shared memory, without the extra barrier (m up to ~13k)
+  args.local_k = fast_smem_bytes(args.m, true) + fast_static_smem() <= kFastSmemCap ? 1 : 0;
+  if (getenv("ALNNLS_FAST_FORCE_A2")) args.local_k = 0;  // test hook: the large-m path
+  const int nblk = (args.m + args.R - 1) / args.R;
+  const size_t smem = fast_smem_bytes(args.m, args.local_k != 0);
+  // opt in once for the largest staging any m can need (the size varies with m)
+  const int smax = (int)(kFastSmemCap - fast_static_smem());
+  if (cudaError_t e = smem_optin(fast_loop_kernel<false>, smax)) return e;
+  if (cudaError_t e = smem_optin(fast_loop_kernel<true>, smax)) return e;
   const bool cluster_ok =
       func_attr_once(reinterpret_cast<const void*>(fast_loop_kernel<true>),
                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
   (void)cudaGetLastError();
-  FastArgs args = a;
   if (cluster_ok && nblk <= 16) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(nblk);
@@ -555,14 +786,23 @@ cudaError_t launch_fast_loop(const FastArgs& a, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, fast_loop_kernel<true>, &cfg) == cudaSuccess &&
-        nclusters > 0)
-      return cudaLaunchKernelEx(&cfg, fast_loop_kernel<true>, args);
-    (void)cudaGetLastError();
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, fast_loop_kernel<true>, &cfg);
+    if (e == cudaSuccess && nclusters > 0) {
+      e = cudaLaunchKernelEx(&cfg, fast_loop_kernel<true>, args);
+      if (e == cudaSuccess) return e;
+    }
+    if (getenv("ALNNLS_DEBUG"))
+      fprintf(stderr, "fast_loop: cluster %d launch not used (%s, %d clusters)\n", nblk,
+              cudaGetErrorString(e), nclusters);
+    (void)cudaGetLastError();  // no cluster of this size fits: cooperative grid instead
   }
   void* params[] = {&args};
-  return cudaLaunchCooperativeKernel((void*)fast_loop_kernel<false>, dim3(nblk), dim3(kFT), params,
-                                     smem, stream);
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)fast_loop_kernel<false>, dim3(nblk), dim3(kFT),
+                                              params, smem, stream);
+  if (e != cudaSuccess && getenv("ALNNLS_DEBUG"))
+    fprintf(stderr, "fast_loop: cooperative %d x %d smem %zu: %s\n", nblk, kFT, smem,
+            cudaGetErrorString(e));
+  return e;
 }
 
 }  // namespace alnnls

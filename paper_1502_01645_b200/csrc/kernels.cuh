@@ -117,6 +117,7 @@ struct FastArgs {
   uint32_t* kl;     // [nblk * R] clamped columns per CTA
   double* kv;       // [nblk * R] their coefficients alpha g - x
   int* kc;          // [nblk]
+  int local_k;      // set by launch_fast_loop: x staged in shared memory too
   double eps;
   uint64_t max_iters;
   int has_time_cap;

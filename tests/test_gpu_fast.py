@@ -1,22 +1,45 @@
-"""FAST profile (Gram and A^T B on the fp64 tensor cores, dmma.cu) against the
-reference oracle, with the tolerances BASELINE.json's north star states:
-relative objective difference <= 1e-10, ||x_gpu - x_ref||_inf <= 1e-8 max(1,
-||x_ref||_inf), identical passive set except entries within 1e-12 of zero, and
-iteration count within +-1 (tests/parity.py baseline_tolerances).
+"""FAST profile: the Gram and A^T B on the fp64 tensor cores (dmma.cu) and the
+one-pass bandwidth-bound single-RHS loop (fastloop.cu), graded against the
+reference with the four tolerances BASELINE.json's north star states
+(tests/parity.py baseline_tolerances):
+  relative objective difference <= 1e-10; ||x_gpu - x_ref||_inf <= 1e-8 max(1,
+  ||x_ref||_inf); identical passive set except entries within 1e-12 of zero;
+  iteration count within +-1.
+Where FAST meets all four (c2 at full size and its law scaled down, the FAST
+loop on the reference's own Q) all four are asserted. The slowly converging
+laws (c1, c5) are chaotic under ulp perturbations (the
+reference recompiled with -march=native goes 1064 -> 285 iterations on c1), so
+there the objective and a KKT certificate (acceptance.cpp:248-256) are
+asserted and the other three are reported.
 """
+import os
+
 import numpy as np
 import pytest
 
 from paper_1502_01645_b200 import abi, instances
-from paper_1502_01645_b200.api import SolverConfig
-from tests.parity import baseline_tolerances
+from paper_1502_01645_b200.api import NumericFailure, SolverConfig
+from tests.parity import baseline_tolerances, same_bits
 
 pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+ALL4 = ("objective_ok", "x_ok", "support_ok", "iter_ok")
 
 
 def fast(cfg):
     cfg.profile = abi.PROFILE_FAST
     return cfg
+
+
+def assert_all4(tol):
+    bad = [k for k in ALL4 if not tol[k]]
+    assert not bad, (bad, tol)
+
+
+def kkt_ok(oracle, Q, q, x, eps):
+    """acceptance.cpp:253-256: kkt_error <= sqrt(eps) (1 + ||q||_2)."""
+    return oracle.kkt_error(Q, q, x) <= np.sqrt(eps) * (1.0 + np.linalg.norm(q))
 
 
 def check_fast(solver, oracle, A, b, cfg):
@@ -26,15 +49,99 @@ def check_fast(solver, oracle, A, b, cfg):
                               got.inner.iterations(), exp["iterations"])
     print(f"FAST tolerances d={A.shape[0]} n={A.shape[1]}: {tol} term {got.inner.termination} "
           f"{exp['termination']} it {got.inner.iterations()} {exp['iterations']}")
-    assert tol["rel_objective"] <= 1e-7, tol
+    assert tol["objective_ok"], tol
     return got, exp, tol
 
 
-@pytest.mark.parametrize("name,d,n", [("c1", 600, 300), ("c2", 1024, 512), ("c5", 1024, 512)])
-def test_fast_within_tolerance(solver, oracle, name, d, n):
+def test_fast_c2_full_size_all_four_tolerances(solver):
+    """BASELINE.json configs[1] at full size against the reference's own run
+    (tests/golden/full_c2.npz): all four tolerances."""
+    g = np.load(os.path.join(GOLDEN, "full_c2.npz"))
+    inst = instances.make_config("c2")
+    A, b = inst["A"], inst["b"]
+    if instances.sha256(np.asfortranarray(A), b) != str(g["input_sha256"]):
+        pytest.skip("generated inputs differ from the fixture's")
+    cfg = fast(SolverConfig(epsilon=inst["epsilon"], max_iters=inst["max_iters"],
+                            stall_window=10**9))
+    r = solver.solve_nnls(A, b, cfg)
+    tol = baseline_tolerances(r.x, g["x"], r.inner.trace[-1].f, float(g["last_f"]),
+                              r.inner.iterations(), int(g["iterations"]))
+    print("FAST c2 full:", tol)
+    assert r.inner.termination == str(g["termination"])
+    assert_all4(tol)
+
+
+def test_fast_c2_law_scaled_all_four(solver, oracle):
+    inst = instances.make_config("c2", d=1024, n=512)
+    cfg = SolverConfig(epsilon=inst["epsilon"], max_iters=inst["max_iters"], stall_window=10**9)
+    _, _, tol = check_fast(solver, oracle, inst["A"], inst["b"], cfg)
+    assert_all4(tol)
+
+
+def test_fast_loop_on_reference_q_all_four(solver, oracle):
+    """The FAST loop alone (one pass per iteration, tree reductions) on the
+    reference's rescaled system: all four tolerances against the reference loop."""
+    inst = instances.make_config("c2", d=2048, n=1024)
+    sc = solver.setup(inst["A"], inst["b"])  # bitwise the reference's rescale(gram)
+    Q, q = sc["Q"], sc["q"]
+    cfg = SolverConfig(epsilon=1e-8, stall_window=10**9)
+    exp = oracle.solve_nqp(Q, q, cfg.to_abi())
+    got = solver.solve_nqp(Q, q, fast(SolverConfig(epsilon=1e-8, stall_window=10**9)))
+    tol = baseline_tolerances(got.x, exp["x"], got.trace[-1].f, exp["trace"][-1]["f"],
+                              got.iterations(), exp["iterations"])
+    assert got.termination == exp["termination"]
+    assert_all4(tol)
+
+
+def test_fast_deterministic(solver):
+    """Fixed reduction trees: two runs are bit-identical (SURVEY §8b threading)."""
+    inst = instances.make_config("c5", d=1024, n=512)
+    cfg = SolverConfig(epsilon=inst["epsilon"], stall_window=10**9, profile=abi.PROFILE_FAST)
+    r1 = solver.solve_nnls(inst["A"], inst["b"], cfg)
+    r2 = solver.solve_nnls(inst["A"], inst["b"], cfg)
+    assert r1.inner.iterations() == r2.inner.iterations()
+    assert same_bits(r1.x, r2.x) and same_bits(r1.inner.final_grad, r2.inner.final_grad)
+
+
+def test_fast_large_m_path_matches(solver):
+    """The clamped set found per CTA and broadcast (the large-m path, one more
+    barrier) gives the same bits as the shared-memory scan every CTA runs itself."""
+    inst = instances.make_config("c5", d=1200, n=600)
+    cfg = SolverConfig(epsilon=inst["epsilon"], stall_window=10**9, profile=abi.PROFILE_FAST)
+    r1 = solver.solve_nnls(inst["A"], inst["b"], cfg)
+    os.environ["ALNNLS_FAST_FORCE_A2"] = "1"
+    try:
+        r2 = solver.solve_nnls(inst["A"], inst["b"], cfg)
+    finally:
+        del os.environ["ALNNLS_FAST_FORCE_A2"]
+    assert r1.inner.iterations() == r2.inner.iterations()
+    assert same_bits(r1.x, r2.x) and same_bits(r1.inner.final_grad, r2.inner.final_grad)
+    assert np.array_equal(r1.inner.multiplies_per_iter, r2.inner.multiplies_per_iter)
+
+
+@pytest.mark.parametrize("name,d,n", [("c1", 600, 300), ("c5", 1024, 512)])
+def test_fast_chaotic_laws_objective_and_kkt(solver, oracle, name, d, n):
     inst = instances.make_config(name, d=d, n=n)
     cfg = SolverConfig(epsilon=inst["epsilon"], max_iters=inst["max_iters"], stall_window=10**9)
-    check_fast(solver, oracle, inst["A"], inst["b"], cfg)
+    got, exp, tol = check_fast(solver, oracle, inst["A"], inst["b"], cfg)
+    assert got.inner.termination == exp["termination"] == "GradientBelowEpsilon"
+    sc = solver.setup(inst["A"], inst["b"])
+    assert kkt_ok(oracle, sc["Q"], sc["q"], got.inner.x, inst["epsilon"])
+
+
+def test_fast_c3_law_at_the_cap(solver, oracle):
+    """c3's law (kappa = 1e6, eps 1e-10) stops at the 5n iteration cap on both
+    paths, at two different points of a path that is still converging: the
+    objectives agree to ~1e-8 relative, not 1e-10 (reported)."""
+    inst = instances.make_config("c3", d=512, n=512)
+    cfg = SolverConfig(epsilon=inst["epsilon"], max_iters=inst["max_iters"], stall_window=10**9)
+    got = solver.solve_nnls(inst["A"], inst["b"], fast(cfg))
+    exp = oracle.solve_nnls(inst["A"], inst["b"], SolverConfig(
+        epsilon=inst["epsilon"], max_iters=inst["max_iters"], stall_window=10**9).to_abi())
+    assert got.inner.termination == exp["termination"] == "MaxIters"
+    assert got.inner.iterations() == exp["iterations"]
+    f_g, f_r = got.inner.trace[-1].f, exp["trace"][-1]["f"]
+    assert abs(f_g - f_r) <= 1e-6 * abs(f_r)
 
 
 @pytest.mark.parametrize("d,n", [(131, 77), (257, 200), (300, 129)])  # ragged tiles, odd d
@@ -44,6 +151,78 @@ def test_fast_ragged_shapes(solver, oracle, d, n):
     x_true = np.where(rng.uniform(size=n) < 0.5, 0.0, rng.uniform(size=n))
     b = A @ x_true + 0.01 * rng.standard_normal(d)
     check_fast(solver, oracle, A, b, SolverConfig(epsilon=1e-8, stall_window=10**9))
+
+
+# ---- the reference's known-answer cases through the FAST loop (test_nqp.cpp) ----------
+
+def test_fast_known_answers(solver):
+    F = abi.PROFILE_FAST
+    r = solver.solve_nqp(np.eye(2), [-1.0, -2.0], SolverConfig(profile=F))  # :123-133
+    assert r.termination == "GradientBelowEpsilon" and r.iterations() == 1
+    assert r.x[0] == 1.0 and r.x[1] == 2.0
+    r = solver.solve_nqp(np.eye(2), [3.0, 4.0], SolverConfig(profile=F))  # :135-144
+    assert r.termination == "EmptyPassiveSet" and r.iterations() == 0 and r.trace[-1].alpha is None
+    Q = np.array([[1.0, 1.0 / 30.0], [1.0 / 30.0, 1.0]])  # coupled, :146-156
+    r = solver.solve_nqp(Q, [-4.0, -5.0 / 3.0], SolverConfig(epsilon=1e-22, profile=F))
+    assert abs(r.x[0] - 3550.0 / 899.0) <= 1e-9 and abs(r.x[1] - 1380.0 / 899.0) <= 1e-9
+    Ql = np.array([[1.0, 0.1], [0.1, 9.0]])
+    r = solver.solve_nqp(Ql, [-4.0, -5.0], SolverConfig(epsilon=1e-10, max_iters=100000, profile=F),
+                         start=[30.0, 2.0])  # warm start, :158-177
+    assert abs(r.x[0] - 35.5 / 8.99) <= 1e-4 and abs(r.x[1] - 4.6 / 8.99) <= 1e-4
+
+
+@pytest.mark.parametrize("case", ["max_iters", "time_cap", "stall", "zero_curv"])
+def test_fast_terminations(solver, case):  # test_nqp.cpp:179-215
+    F = abi.PROFILE_FAST
+    if case == "max_iters":
+        r = solver.solve_nqp(np.array([[1.0, 0.1], [0.1, 9.0]]), [-4.0, -5.0],
+                             SolverConfig(epsilon=1e-30, max_iters=3, stall_window=1000, profile=F))
+        assert r.termination == "MaxIters" and r.iterations() == 3 and len(r.trace) == 4
+    elif case == "time_cap":
+        r = solver.solve_nqp(np.eye(2), [-1.0, -2.0], SolverConfig(time_cap=0.0, profile=F))
+        assert r.termination == "TimeCap" and r.iterations() == 0
+    elif case == "stall":
+        Q = np.array([[1.0, 1.0 / 30.0], [1.0 / 30.0, 1.0]])
+        r = solver.solve_nqp(Q, [-4.0, -5.0 / 3.0], SolverConfig(epsilon=5e-324, max_iters=1000000,
+                                                                 stall_window=5, profile=F))
+        assert r.termination == "Stalled" and r.iterations() < 1000000
+    else:
+        r = solver.solve_nqp(np.zeros((2, 2)), [-1.0, -1.0], SolverConfig(profile=F))
+        assert r.termination == "ZeroCurvature" and r.iterations() == 0
+
+
+def test_fast_numeric_failure(solver):  # test_nqp.cpp:217-226
+    with pytest.raises(NumericFailure) as ei:
+        solver.solve_nqp(np.eye(2), [-1e308, -1.0], SolverConfig(profile=abi.PROFILE_FAST))
+    assert ei.value.trace == []
+
+
+def test_fast_halving_safeguard(solver):  # test_nqp.cpp:349-389
+    Q = np.array([[1.0, 0.9], [0.9, 1.0]])
+    q = np.array([1.49, -2.69])
+    cfg = SolverConfig(epsilon=1e-18, max_iters=10000, stall_window=1000000, profile=abi.PROFILE_FAST)
+    res = solver.solve_nqp(Q, q, cfg, start=[0.52, 0.35])
+    g0 = Q @ np.array([0.52, 0.35]) + q
+    full = (g0 @ g0) / (g0 @ Q @ g0)
+    assert res.trace[0].alpha is not None and res.trace[0].alpha <= 0.5 * full
+    for k in range(1, len(res.trace)):
+        prev = res.trace[k - 1].f
+        assert res.trace[k].f <= prev + 1e-12 * max(1.0, abs(prev))
+    assert res.termination == "GradientBelowEpsilon" and res.min_iterate >= 0.0
+    assert res.x[0] == 0.0 and abs(res.x[1] - 2.69) <= 1e-9
+
+
+def test_fast_trace_sampling(solver):
+    Ql = np.array([[1.0, 0.1], [0.1, 9.0]])
+    F = abi.PROFILE_FAST
+    full = solver.solve_nqp(Ql, [-4.0, -5.0], SolverConfig(epsilon=1e-18, max_iters=100000,
+                                                           stall_window=1000000, profile=F))
+    s = solver.solve_nqp(Ql, [-4.0, -5.0], SolverConfig(epsilon=1e-18, max_iters=100000,
+                                                        stall_window=1000000, trace_every=4, profile=F))
+    assert same_bits(s.x, full.x) and s.iterations() == full.iterations()
+    assert s.trace[-1].alpha is None
+    for k in range(len(s.trace) - 1):
+        assert s.trace[k].iter % 4 == 0 and s.trace[k].alpha is not None
 
 
 def test_fast_gram_close_to_exact(solver):
@@ -70,4 +249,4 @@ def test_fast_batched_within_tolerance(solver):
     for j in range(inst["B"].shape[1]):
         tol = baseline_tolerances(Xf[:, j], Xe[:, j], cf[j]["f_final"], ce[j]["f_final"],
                                   cf[j]["iterations"], ce[j]["iterations"])
-        assert tol["rel_objective"] <= 1e-7, (j, tol)
+        assert tol["objective_ok"], (j, tol)
