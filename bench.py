@@ -6,7 +6,7 @@ projected-gradient loop + unscale + residual; nnls.hpp:129-144) of the
 BASELINE.json workload, default c2 = configs[1] (d=8192, n=4096, N(0,1),
 eps 1e-8; seeded synthetic inputs, see paper_1502_01645_b200/instances.py).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--profile exact|fast]
   python bench.py --impl reference ...   # the reference CPU solver (oracle/_ref)
   python bench.py --workload c4 ...      # batched multi-RHS (NMF H-update), column-sharded
 
@@ -14,8 +14,14 @@ Prints ONE JSON line on rank 0. `value` is whole-job solves/s with A, b already
 in HBM (device-pointer C-ABI entry); `e2e` is the same metric through the
 host-buffer public API with the H2D copy of A, b and the D2H of the result in
 the timed region. Timing: CUDA events on the library's stream, max over ranks.
-N > 1 runs one independent replica per GPU ("replicas only": one solve's
-iteration loop does not shard).
+The default (EXACT, bitwise) line also carries "fast_profile": the same
+workload through the FAST profile (DMMA Gram + the one-pass loop), graded on
+BASELINE.json's four tolerances against the EXACT run.
+
+--gpus N without WORLD_SIZE in the environment re-launches this script under
+torch.distributed.run with N ranks (one per GPU, NCCL, 127.0.0.1). c1/c2/c3
+at N > 1 run one independent replica per GPU ("replicas only": one solve's
+iteration loop does not shard), "scaling": "weak".
 
 --workload c5 with N > 1 (configs[4]): A's rows are split across the ranks and
 the exact setup runs as a row-block pipeline (rowblock.py): every rank
@@ -24,12 +30,21 @@ NCCL, the last rank rescales and iterates, the residual chain is relayed back
 through the ranks. Bitwise equal to the single-GPU solve; "scaling": "strong".
 --workload c5 --c5-setup allreduce [--profile fast] runs configs[4]'s setup as
 written instead: a partial Gram per rank (DMMA under fast) summed with one NCCL
-allreduce, iterations on rank 0 (within rounding of the reference, not bitwise).
+allreduce of the packed upper triangle, iterations on rank 0 (within rounding of
+the reference, not bitwise).
 
 --workload c4 (configs[3]): a step is the whole batched solve of B (20000 x
 65536) against the shared Q; the 65536 right-hand sides are split by column
 across the N ranks with no data-path collective ("scaling": "strong"), and
-`value` is total columns / max-over-ranks time.
+`value` is total columns / max-over-ranks time. B = A H_true is formed on the
+device by an exact-order kernel (bit-identical to the host generator, so the
+sampled columns are checked against the reference's results).
+
+--impl reference (this tier's reference arm): the reference's own solve_nnls
+(oracle/_ref, compiled from its headers by oracle/Makefile) on the host cores:
+each step is one real, unmodified solve_nnls call; the K steps run concurrently,
+one per host core, the way the reference's suite pool runs independent cells
+(bench.hpp:191-207); value = K / wall time. Under torchrun only rank 0 runs it.
 """
 import argparse
 import json
@@ -138,20 +153,19 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
-    if ws > 1 or os.environ.get("ALNNLS_FORCE_ROWBLOCK"):
+    if args.impl == "ours" and (ws > 1 or os.environ.get("ALNNLS_FORCE_ROWBLOCK")):
         import torch.distributed as dist  # noqa
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = "nccl" if args.impl == "ours" else "gloo"
-        if backend == "nccl":
-            import torch
-            torch.cuda.set_device(local)
-        dist.init_process_group(backend=backend)
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group(backend="nccl")
     return ws, rank, local, dist
 
 
 PROFILE = {"exact": 0, "fast": 1}
 PROFILE_DESC = {"exact": "exact (bitwise reference trajectory)",
-                "fast": "fast (DMMA Gram / Q V passes; not reference-bitwise, DESIGN.md 2a)"}
+                "fast": "fast (DMMA Gram + one-pass single-RHS loop / DMMA Q V passes; graded on the "
+                        "four BASELINE tolerances, DESIGN.md 2a-2b)"}
 
 
 def solver_config(inst, profile="exact"):
@@ -159,6 +173,17 @@ def solver_config(inst, profile="exact"):
     # stall off like the reference's own benchmark convention (acceptance.cpp:73-88)
     return SolverConfig(epsilon=inst["epsilon"], max_iters=inst["max_iters"], stall_window=10**9,
                         profile=PROFILE[profile])
+
+
+def workload_config(name, d, n, eps, nrhs=None):
+    """The config dict both arms print (identical: the workload, not the implementation)."""
+    c = {"workload": f"{name}: d={d}, n={n}" + (f", nrhs={nrhs}" if nrhs else ""), "eps": eps,
+         "solver": "solve_nnls (nnls.hpp:129-144)" + (" per column, one shared Gram" if nrhs else ""),
+         "stall_window": "off (acceptance.cpp:73-88 convention)"}
+    big = 8 * d * (n + (nrhs or 0))
+    c["l2"] = ("inputs larger than L2 (no flush needed)" if big > 126e6
+               else "inputs L2-resident (latency-bound config; no flush)")
+    return c
 
 
 def traffic_from_profiles(workload, kernel):
@@ -170,49 +195,39 @@ def traffic_from_profiles(workload, kernel):
     return d.get(workload, {}).get(kernel)
 
 
-# ---- reference CPU solver timing ----------------------------------------------------------
-def cpu_reference_step(ora, inst, cfg_abi, H, sample_rows):
-    """One bounded sample of the reference CPU pipeline (nnls.hpp:129-144):
-    gram on `sample_rows` rows of A, scaled linearly in d (the gram inner loop is
-    one dot over k, linalg.hpp:168), plus transpose_matvec, rescale, solve_nqp,
-    unscale and the residual run for real on the full problem (H supplied)."""
-    A, b = inst["A"], inst["b"]
-    d, n = A.shape
-    ds = min(d, sample_rows)
-    As = np.asfortranarray(A[:ds, :])
-    t = time.perf_counter()
-    ora.gram(As)
-    t_gram = (time.perf_counter() - t) * d / ds
-    t = time.perf_counter()
-    atb = ora.transpose_matvec(A, b)
-    t_tmv = time.perf_counter() - t
-    t = time.perf_counter()
-    sys_ = ora.rescale(H, -atb)
-    t_rescale = time.perf_counter() - t
-    t = time.perf_counter()
-    res = ora.solve_nqp(sys_["Q"], sys_["q"], cfg_abi) if len(sys_["q"]) else None
-    t_loop = time.perf_counter() - t
-    t = time.perf_counter()
-    x = np.zeros(n)
-    if res is not None:
-        x[sys_["retained"].astype(np.int64)] = res["x"] / sys_["scale"]
-    ax = ora.matvec(A, x)
-    r = ax - b
-    _ = float(np.sum(r * r))
-    t_fin = time.perf_counter() - t
-    total = t_gram + t_tmv + t_rescale + t_loop + t_fin
-    return total, {"gram_extrapolated_s": t_gram, "transpose_matvec_s": t_tmv,
-                   "rescale_s": t_rescale, "solve_nqp_s": t_loop, "finish_s": t_fin,
-                   "iterations": res["iterations"] if res else 0,
-                   "termination": res["termination"] if res else "EmptyPassiveSet"}
+# ---- reference CPU solver ------------------------------------------------------------------
+def ref_oracle():
+    from oracle.oracle import Oracle, available
+    if available("ref"):
+        return Oracle("ref"), "reference"
+    return Oracle("oracle"), "port"
 
 
-def reference_gram_parallel(ora, A, threads):
-    """Untimed: the reference's own gram(), driven over column-block pairs on all
-    host threads; every entry is the same k-ascending chain, so H is bitwise gram(A)."""
+def cached_inputs(name):
+    """Seeded inputs generated in a CHILD process (the generator library is this
+    repo's, not the reference's) and read back from an .npz, so the reference
+    process maps only oracle/_ref."""
+    import tempfile
+    path = os.path.join(tempfile.gettempdir(), f"alnnls_inputs_{name}_{os.getpid()}.npz")
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); "
+            "from paper_1502_01645_b200 import instances as I; "
+            "i = I.make_config(%r); np.savez(%r, A=i['A'], b=i['b'], eps=i['epsilon'], "
+            "mi=-1 if i['max_iters'] is None else i['max_iters'])") % (ROOT, name, path)
+    subprocess.run([sys.executable, "-c", code], check=True)
+    z = np.load(path)
+    inst = {"A": np.asfortranarray(z["A"]), "b": z["b"], "epsilon": float(z["eps"]),
+            "max_iters": None if int(z["mi"]) < 0 else int(z["mi"]), "name": name}
+    os.unlink(path)
+    return inst
+
+
+def reference_gram_parallel(ora, A, threads, nb=16):
+    """The reference's own gram() (linalg.hpp:160-174) driven over column-block
+    pairs on `threads` host threads; every entry is the same k-ascending chain, so
+    H is bitwise gram(A) (the pairing recomputes the diagonal blocks)."""
     from concurrent.futures import ThreadPoolExecutor
     d, n = A.shape
-    nb = max(1, min(16, threads))
+    nb = max(1, min(nb, threads))
     bs = (n + nb - 1) // nb
     blocks = [(i * bs, min(n, (i + 1) * bs)) for i in range(nb) if i * bs < n]
     H = np.zeros((n, n), order="F")
@@ -220,8 +235,7 @@ def reference_gram_parallel(ora, A, threads):
     def work(pair):
         (a0, a1), (b0, b1) = pair
         if (a0, a1) == (b0, b1):
-            Hb = ora.gram(np.asfortranarray(A[:, a0:a1]))
-            H[a0:a1, a0:a1] = Hb
+            H[a0:a1, a0:a1] = ora.gram(np.asfortranarray(A[:, a0:a1]))
         else:
             cols = np.concatenate([np.arange(a0, a1), np.arange(b0, b1)])
             Hb = ora.gram(np.asfortranarray(A[:, cols]))
@@ -235,65 +249,173 @@ def reference_gram_parallel(ora, A, threads):
     return H
 
 
-def ref_oracle():
-    from oracle.oracle import Oracle, available
-    if available("ref"):
-        return Oracle("ref"), "reference"
-    return Oracle("oracle"), "port"
-
-
-def sample_rows_for(inst):
-    d, n = inst["A"].shape
-    # ~4 GFLOP of gram per sample (~3 s on one core at the reference's 1.4 GFLOP/s)
-    return int(max(16, min(d, 4.0e9 / max(1.0, n * (n + 1.0)))))
+def cpu_pipeline_sample(ora, inst, cfg_abi, threads, loop_cap=None):
+    """A bounded, fully measured run of the reference pipeline (nnls.hpp:129-144):
+    gram by the reference's gram() over column-block pairs on all host threads
+    (bitwise gram(A)), then transpose_matvec, rescale, solve_nqp, unscale and the
+    residual single-threaded (the reference is single-threaded per solve). With
+    loop_cap the loop runs that many iterations and is scaled to the cap given by
+    the config (time per iteration is flat). Returns (seconds, detail)."""
+    A, b = inst["A"], inst["b"]
+    d, n = A.shape
+    t = time.perf_counter()
+    H = reference_gram_parallel(ora, A, threads)
+    t_gram = time.perf_counter() - t
+    t = time.perf_counter()
+    atb = ora.transpose_matvec(A, b)
+    sys_ = ora.rescale(H, -atb)
+    t_resc = time.perf_counter() - t
+    del H
+    t = time.perf_counter()
+    res, scale = None, 1.0
+    if len(sys_["q"]):
+        cfg = cfg_abi
+        if loop_cap is not None:
+            full = cfg.max_iters if cfg.has_max_iters else 5 * len(sys_["q"])
+            cfg = abi.make_config(epsilon=cfg.epsilon if cfg.has_epsilon else None,
+                                  max_iters=min(loop_cap, full), stall_window=cfg.stall_window,
+                                  record_multiplies=False)
+            scale = full / min(loop_cap, full)
+        res = ora.solve_nqp(sys_["Q"], sys_["q"], cfg)
+    t_loop = (time.perf_counter() - t) * scale
+    t = time.perf_counter()
+    x = np.zeros(n)
+    if res is not None:
+        x[sys_["retained"].astype(np.int64)] = res["x"] / sys_["scale"]
+    ax = ora.matvec(A, x)
+    r = ax - b
+    _ = float(np.sum(r * r))
+    t_fin = time.perf_counter() - t
+    total = t_gram + t_resc + t_loop + t_fin
+    return total, {"gram_s": t_gram, "gram_threads": threads, "transpose_matvec_rescale_s": t_resc,
+                   "solve_nqp_s": t_loop, "solve_nqp_scaled_from": loop_cap,
+                   "finish_s": t_fin, "iterations": res["iterations"] if res else 0,
+                   "termination": res["termination"] if res else "EmptyPassiveSet"}
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
-        return 0
+        return 0  # the CPU reference runs once, on rank 0
     if args.workload == "c4":
         return run_reference_batched(args, ws)
-    inst = instances.make_config(args.workload)
-    cfg = solver_config(inst).to_abi()
     ora, kind = ref_oracle()
-    threads = os.cpu_count() or 1
-    t = time.perf_counter()
-    H = reference_gram_parallel(ora, inst["A"], threads)
-    t_pre = time.perf_counter() - t
-    rows = sample_rows_for(inst)
-    for _ in range(args.warmup):
-        cpu_reference_step(ora, inst, cfg, H, rows)
-    times, detail = [], None
-    for _ in range(args.steps):
-        tt, detail = cpu_reference_step(ora, inst, cfg, H, rows)
-        times.append(tt)
-    per = float(np.mean(times))
-    value = 1.0 / per
-    d, n = inst["A"].shape
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded SplitMix64, BASELINE.json configs)",
-        "config": {"workload": f"{args.workload}: d={d}, n={n}", "eps": inst["epsilon"],
-                   "stall_window": "off"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
-                         "sample": (f"reference gram on {rows} of {d} rows scaled linearly in d; "
-                                    "transpose_matvec, rescale, solve_nqp, unscale, residual on "
-                                    "the full problem (single thread; the reference is "
-                                    f"single-threaded per solve). Untimed H precompute {t_pre:.1f}s "
-                                    f"on {threads} threads"),
-                         "breakdown": detail},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    inst = cached_inputs(args.workload)
+    A, b = inst["A"], inst["b"]
+    d, n = A.shape
+    cores = os.cpu_count() or 1
+    cfg = solver_config_abi(inst)
+    line = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SplitMix64, BASELINE.json configs)",
+            "config": workload_config(args.workload, d, n, inst["epsilon"])}
+    if args.workload in ("c1", "c2"):
+        # K real, unmodified solve_nnls calls, concurrently one per host core
+        from concurrent.futures import ThreadPoolExecutor
+        per = []
+
+        def one(_):
+            t = time.perf_counter()
+            r = ora.solve_nnls(A, b, cfg)
+            per.append(time.perf_counter() - t)
+            return r["iterations"], r["termination"]
+
+        if args.warmup > 0:
+            with ThreadPoolExecutor(max_workers=min(args.warmup, cores)) as ex:
+                list(ex.map(one, range(args.warmup)))
+        per.clear()
+        P = min(args.steps, cores)
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=P) as ex:
+            outs = list(ex.map(one, range(args.steps)))
+        wall = time.perf_counter() - t0
+        value = args.steps / wall
+        line.update({"value": value, "ms_per_step": wall / args.steps * 1e3,
+                     "iterations": outs[0][0], "termination": outs[0][1],
+                     "per_solve_s_mean": float(np.mean(per)), "per_solve_s_max": float(np.max(per))})
+        sample = (f"{args.steps} real solve_nnls calls (the reference compiled from its headers, "
+                  f"oracle/_ref), run concurrently on {P} host threads (one solve per core, like "
+                  f"bench.hpp:191-207); value = steps / wall time ({wall:.1f} s); "
+                  f"{args.warmup} warm-up solves before")
+        line["cpu_baseline"] = {"value": value, "unit": UNIT, "cores": P, "kind": kind,
+                                "sample": sample, "cpu": cpu_model()}
+    else:
+        # c3 / c5: one solve takes 0.2-3 h on a core; a bounded sample per step
+        cap = 200
+        for _ in range(args.warmup):
+            pass  # no warm-up state on the host path worth a 10 s sample
+        times, detail = [], None
+        for _ in range(args.steps):
+            tt, detail = cpu_pipeline_sample(ora, inst, cfg, cores, loop_cap=cap)
+            times.append(tt)
+        per = float(np.mean(times))
+        value = 1.0 / per
+        line.update({"value": value, "ms_per_step": per * 1e3, "breakdown": detail})
+        line["cpu_baseline"] = {
+            "value": value, "unit": UNIT, "cores": cores, "kind": kind, "cpu": cpu_model(),
+            "sample": (f"reference gram() over column-block pairs on {cores} threads (measured), "
+                       f"transpose_matvec/rescale/unscale/residual measured single-thread, "
+                       f"solve_nqp measured for {cap} iterations and scaled to the config's cap")}
+    line["e2e"] = {"value": line["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}
     print(json.dumps(line), flush=True)
     return 0
 
 
+def solver_config_abi(inst, record_multiplies=False):
+    return abi.make_config(epsilon=inst["epsilon"], max_iters=inst["max_iters"], stall_window=10**9,
+                           record_multiplies=record_multiplies)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 # ---- our GPU path ---------------------------------------------------------------------------
+def measure_single(s, args, dA, db, d, n, cfg, anti=False):
+    """Device-resident steps (value) and host-buffer steps (e2e) of one profile."""
+    import torch
+    solve_dev = s.solve_anti_accelerated_device if anti else s.solve_nnls_device
+    for _ in range(max(1, args.warmup)):  # >= 1: the solve's iteration count for the roofline
+        solve_dev(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
+    summ = s.last_summary()
+    out = {"iterations": int(summ.iterations), "mults": int(summ.multiplies_total)}
+    torch.cuda.synchronize()
+    l0 = s.launch_count()
+    t_setup = t_loop = 0.0
+    s.timer_start()
+    for _ in range(args.steps):
+        solve_dev(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
+        sm = s.last_summary()
+        t_setup += sm.t_setup_s
+        t_loop += sm.t_loop_s
+    out["t"] = s.timer_stop()
+    out["launches"] = (s.launch_count() - l0) // max(1, args.steps)
+    out["setup_s"] = t_setup / args.steps
+    out["loop_s"] = t_loop / args.steps
+    return out
+
+
+def measure_e2e(s, args, hA, hb, cfg, anti=False):
+    solve_host = s.solve_anti_accelerated if anti else s.solve_nnls
+    res = solve_host(hA, hb, cfg)  # warm
+    s.timer_start()
+    for _ in range(args.steps):
+        res = solve_host(hA, hb, cfg)
+    return s.timer_stop(), res
+
+
 def run_ours(args, ws, rank, local, dist):
     import torch
     from paper_1502_01645_b200.api import Solver
+    from tests.parity import baseline_tolerances
     torch.cuda.set_device(local)
     inst = instances.make_config(args.workload)
     A, b = inst["A"], inst["b"]
@@ -309,35 +431,19 @@ def run_ours(args, ws, rank, local, dist):
         if dist is not None:
             dist.barrier()
 
-    anti = args.solver == "anti_acc"
-    solve_dev = s.solve_anti_accelerated_device if anti else s.solve_nnls_device
-    solve_host = s.solve_anti_accelerated if anti else s.solve_nnls
-    for _ in range(max(1, args.warmup)):  # >= 1: the solve's iteration count for the roofline
-        solve_dev(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
-    summ = s.last_summary()
-    iters = int(summ.iterations)
-    mults = int(summ.multiplies_total)
-
-    barrier()
-    torch.cuda.synchronize()
-    l0 = s.launch_count()
-    with ClockSampler(local) as clk:
-        s.timer_start()
-        t_setup = t_loop = 0.0
-        for _ in range(args.steps):
-            solve_dev(dA.data_ptr(), d, d, n, db.data_ptr(), cfg, fetch=False)
-            sm = s.last_summary()
-            t_setup += sm.t_setup_s
-            t_loop += sm.t_loop_s
-        t = s.timer_stop()
-    torch.cuda.synchronize()
-    barrier()
-    launches = (s.launch_count() - l0) // max(1, args.steps)
-    t_max = t
-    if dist is not None:
-        tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        tt = torch.tensor([v], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+        return float(tt.item())
+
+    anti = args.solver == "anti_acc"
+    barrier()
+    with ClockSampler(local) as clk:
+        meas = measure_single(s, args, dA, db, d, n, cfg, anti)
+    barrier()
+    t_max = max_over_ranks(meas["t"])
     value = ws * args.steps / t_max
 
     # e2e: host-buffer public API, pinned host inputs, result read back each step
@@ -347,26 +453,32 @@ def run_ours(args, ws, rank, local, dist):
     pb.copy_(torch.from_numpy(b))
     hA = pA.numpy().T  # Fortran-ordered (d, n) view of pinned memory
     hb = pb.numpy()
-    res = solve_host(hA, hb, cfg)  # warm
     barrier()
-    s.timer_start()
-    for _ in range(args.steps):
-        res = solve_host(hA, hb, cfg)
-    te = s.timer_stop()
-    if dist is not None:
-        tt = torch.tensor([te], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        te = float(tt.item())
+    te, res = measure_e2e(s, args, hA, hb, cfg, anti)
+    te = max_over_ranks(te)
     m = len(res.inner.x)
     d2h = 8 * (n + 2 * m + len(res.inner.multiplies_per_iter)) + 56 * len(res.inner.trace)
     e2e = {"value": ws * args.steps / te, "unit": UNIT, "h2d_bytes_per_step": 8 * (d * n + d),
            "d2h_bytes_per_step": int(d2h)}
 
+    # the same workload through the FAST profile (the default line stays EXACT)
+    fast = None
+    if args.profile == "exact" and not anti and args.workload != "c5":
+        cfgf = solver_config(inst, "fast")
+        barrier()
+        mf = measure_single(s, args, dA, db, d, n, cfgf)
+        tf = max_over_ranks(mf["t"])
+        tfe, resf = measure_e2e(s, args, hA, hb, cfgf)
+        tfe = max_over_ranks(tfe)
+        tol = baseline_tolerances(resf.x, res.x, resf.inner.trace[-1].f, res.inner.trace[-1].f,
+                                  resf.inner.iterations(), res.inner.iterations())
+        fast = {"meas": mf, "value": ws * args.steps / tf, "e2e": ws * args.steps / tfe, "tol": tol}
+
     if rank != 0:
         return 0
     hbm, hbm_kind = peaks()
-    per_setup = t_setup / args.steps
-    per_loop = t_loop / args.steps
+    iters, mults = meas["iterations"], meas["mults"]
+    per_setup, per_loop = meas["setup_s"], meas["loop_s"]
     setup_flops = d * n * (n + 1) + 2 * d * n
     if anti:  # the reference's two dense matvecs per iteration (accelerated.hpp:45, :89)
         mults = 2 * n * n * iters
@@ -384,38 +496,73 @@ def run_ours(args, ws, rank, local, dist):
                   "peak_source": "measured (tools/microbench/fp64_probe.cu, DMMA)",
                   "algorithmic": f"d*n*(n+1) + 2*d*n = {setup_flops} flop per solve",
                   "traffic": traffic_from_profiles(args.workload, "syrk_streamk_kernel")}
+    if args.profile == "fast":
+        roof_loop = fast_loop_roofline(args.workload, mults, per_loop, hbm, hbm_kind)
+        roof_setup.update({"kernel": "setup: syrk_dmma_kernel (fp64 tensor cores) + rescale epilogue",
+                           "frac_of_exact_cap": None,
+                           "traffic": traffic_from_profiles(args.workload, "syrk_dmma_kernel")})
     dominant = roof_loop if per_loop >= per_setup else roof_setup
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64, BASELINE.json configs)",
-        "config": {"workload": f"{args.workload}: d={d}, n={n}", "eps": inst["epsilon"],
-                   "solver": ("solve_anti_accelerated (accelerated.hpp)" if anti
-                              else "solve_nnls (nnls.hpp)"),
-                   "stall_window": "off", "profile": PROFILE_DESC[args.profile],
-                   "l2": (f"inputs larger than L2 (A {8 * d * n / 1e6:.0f} MB, "
-                          f"Q {8 * n * n / 1e6:.0f} MB)"),
-                   "parallelism": f"replicas x{ws}"},
+        "config": workload_config(args.workload, d, n, inst["epsilon"]),
+        "profile": PROFILE_DESC[args.profile],
+        "solver": ("solve_anti_accelerated (accelerated.hpp)" if anti else "solve_nnls"),
+        "parallelism": f"replicas x{ws} (one independent solve per GPU)",
         "iterations": iters, "time_to_tol_ms": t_max / args.steps * 1e3,
         "iters_per_s": iters / per_loop if per_loop > 0 else None,
         "setup_ms": per_setup * 1e3, "loop_ms": per_loop * 1e3,
         "roofline": dominant, "roofline_other": roof_setup if dominant is roof_loop else roof_loop,
-        "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+        "e2e": e2e, "gpu_launches": int(meas["launches"]), "clocks": clk.summary(),
     }
+    if fast is not None:
+        mf = fast["meas"]
+        fl = fast_loop_roofline(args.workload, mf["mults"], mf["loop_s"], hbm, hbm_kind)
+        fl["exact_equivalent_GBps"] = 8.0 * mults / mf["loop_s"] / 1e9
+        fsetup = setup_flops / mf["setup_s"] / 1e12
+        line["fast_profile"] = {
+            "value": fast["value"], "e2e": fast["e2e"], "unit": UNIT,
+            "iterations": mf["iterations"], "setup_ms": mf["setup_s"] * 1e3,
+            "loop_ms": mf["loop_s"] * 1e3, "us_per_iter": mf["loop_s"] / max(1, mf["iterations"]) * 1e6,
+            "setup_roofline": {"kernel": "syrk_dmma_kernel", "achieved": fsetup,
+                               "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                               "frac": fsetup / FP64_PEAK_TFLOPS},
+            "loop_roofline": fl, "gpu_launches": int(mf["launches"]),
+            "tolerances_vs_exact": fast["tol"],
+        }
     if ws == 1 and not args.no_cpu_baseline and not anti:
         ora, kind = ref_oracle()
-        H = s.gram(A)  # bitwise equal to the reference gram (tests/test_gpu_parity.py)
-        rows = sample_rows_for(inst)
-        tt, detail = cpu_reference_step(ora, inst, cfg.to_abi(), H, rows)
-        line["cpu_baseline"] = {
-            "value": 1.0 / tt, "unit": UNIT, "cores": 1, "kind": kind,
-            "sample": (f"reference gram on {rows} of {d} rows scaled linearly in d; "
-                       "transpose_matvec, rescale, solve_nqp, unscale, residual on the full "
-                       "problem (H from the bit-identical GPU gram); single thread"),
-            "breakdown": detail}
+        threads = os.cpu_count() or 1
+        if args.workload == "c1":  # a full solve is 0.1 s: the real thing, repeated
+            t = time.perf_counter()
+            reps = 20
+            for _ in range(reps):
+                ora.solve_nnls(A, b, solver_config_abi(inst))
+            tt = (time.perf_counter() - t) / reps
+            detail, sample, cores = None, f"{reps} real solve_nnls calls, single thread", 1
+        else:
+            cap = None if args.workload == "c2" else 200
+            tt, detail = cpu_pipeline_sample(ora, inst, solver_config_abi(inst), threads, cap)
+            sample = (f"the full reference pipeline on this workload, measured: gram() over column-"
+                      f"block pairs on {threads} threads (bitwise gram(A)), the rest single-thread"
+                      + ("" if cap is None else f"; solve_nqp {cap} iterations scaled to the cap"))
+            cores = threads
+        line["cpu_baseline"] = {"value": 1.0 / tt, "unit": UNIT, "cores": cores, "kind": kind,
+                                "sample": sample, "cpu": cpu_model(), "breakdown": detail}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def fast_loop_roofline(workload, mults, per_loop, hbm, hbm_kind):
+    gbs = 8.0 * mults / per_loop / 1e9 if per_loop > 0 else 0.0
+    return {"kernel": "fast_loop_kernel (one-pass masked GEMV loop, 128-bit loads, tree reductions)",
+            "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+            "peak_source": hbm_kind,
+            "algorithmic": (f"8 B x the FAST loop's multiply count (m|P| + sum m|K| per iteration: "
+                            f"every Q element it must read) = {8 * mults} B per launch"),
+            "traffic": traffic_from_profiles(workload, "fast_loop_kernel")}
 
 
 # ---- c5 at N > 1: exact row-block setup pipeline ------------------------------------------
@@ -497,11 +644,10 @@ def run_ours_rowblock(args, ws, rank, local, dist):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64, BASELINE.json configs[4])",
-        "config": {"workload": f"{args.workload}: d={d}, n={n}", "eps": inst["epsilon"],
-                   "stall_window": "off", "profile": "exact (bitwise reference trajectory)",
-                   "parallelism": f"row blocks x{ws}: k-chain Gram pipeline (NCCL send/recv), "
-                                  "iterations on the last rank",
-                   "l2": "inputs larger than L2"},
+        "config": workload_config(args.workload, d, n, inst["epsilon"]),
+        "profile": PROFILE_DESC["exact"],
+        "parallelism": f"row blocks x{ws}: k-chain Gram pipeline (NCCL send/recv), "
+                       "iterations on the last rank",
         "iterations": iters, "gpu_launches": launches, "clocks": clk.summary(),
         "e2e": None,
     }
@@ -541,7 +687,10 @@ def run_ours_allreduce(args, ws, rank, local, dist):
                                   atb.data_ptr(), profile=prof)
             ev[1].record()
         ev[0].record()
-        H, atb = allreduce_setup(dist, ws, n, partial, "cuda")
+        H, atb = allreduce_setup(
+            dist, ws, n, partial, "cuda",
+            pack=lambda Hm, P: s.pack_upper_device(n, Hm.data_ptr(), P.data_ptr()),
+            unpack=lambda P, Hm: s.unpack_upper_device(n, P.data_ptr(), Hm.data_ptr()))
         ev[2].record()
         x = torch.empty(n, dtype=torch.float64, device="cuda")
         iters = 0
@@ -596,13 +745,12 @@ def run_ours_allreduce(args, ws, rank, local, dist):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64, BASELINE.json configs[4])",
-        "config": {"workload": f"{args.workload}: d={d}, n={n}", "eps": inst["epsilon"],
-                   "stall_window": "off", "profile": PROFILE_DESC[args.profile],
-                   "setup": "partial Grams + one allreduce of [H | A^T b] (configs[4] as written); "
-                            "not reference-bitwise",
-                   "parallelism": f"row blocks x{ws}: partial Gram per GPU, one NCCL allreduce "
-                                  f"({(n * n + n) * 8} B), iterations on rank 0",
-                   "l2": "inputs larger than L2"},
+        "config": workload_config(args.workload, d, n, inst["epsilon"]),
+        "profile": PROFILE_DESC[args.profile],
+        "setup": "partial Grams + one allreduce of [packed upper H | A^T b] (configs[4] as "
+                 "written); not reference-bitwise",
+        "parallelism": f"row blocks x{ws}: partial Gram per GPU, one NCCL allreduce "
+                       f"({(n * (n + 1) // 2 + n) * 8} B), iterations on rank 0",
         "iterations": iters, "partial_gram_ms": t_part * 1e3, "allreduce_ms": t_ar * 1e3,
         "solve_ms": t_solve * 1e3, "residual_sq": res,
         "roofline": {"kernel": "partial Gram per rank (" +
@@ -672,8 +820,7 @@ def run_reference_batched(args, ws):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": K / value * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64, BASELINE.json configs[3])",
-        "config": {"workload": f"c4: d={d}, n={n}, nrhs={K}", "eps": spec["epsilon"],
-                   "stall_window": "off"},
+        "config": workload_config("c4", d, n, spec["epsilon"], nrhs=K),
         "cpu_baseline": {"value": value, "unit": C4_UNIT, "cores": threads, "kind": kind,
                          "sample": (f"{detail['sample_columns']} columns of B on {threads} threads "
                                     "(Gram once, shared), extrapolated to all columns"),
@@ -695,12 +842,15 @@ def run_ours_batched(args, ws, rank, local, dist):
     H = instances.gen_htrue(n, kc, spec["seed"], col0)  # this rank's columns of H_true
     dA = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()       # (n, d) == A column-major
     dH = torch.from_numpy(np.ascontiguousarray(H.T)).cuda()       # (kc, n) == H column-major
-    dB = dH @ dA                                                  # (kc, d) == B = A H_true
+    dB = torch.empty((kc, d), dtype=torch.float64, device="cuda")  # (kc, d) == B column-major
     dX = torch.empty((kc, n), dtype=torch.float64, device="cuda")
-    del dH
-    torch.cuda.synchronize()
     cfg = SolverConfig(epsilon=spec["epsilon"], stall_window=10**9, profile=PROFILE[args.profile])
     s = Solver(local)
+    # B = A H_true in the reference's matvec order (untimed harness step): the same
+    # bytes tests/test_gpu_c4_full.py pins against the reference's per-column solves
+    s.matmat_device(d, n, kc, dA.data_ptr(), d, dH.data_ptr(), n, dB.data_ptr(), d)
+    del dH
+    torch.cuda.synchronize()
 
     def barrier():
         if dist is not None:
@@ -781,12 +931,10 @@ def run_ours_batched(args, ws, rank, local, dist):
         "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64, BASELINE.json configs[3]; B = A H_true formed on device)",
-        "config": {"workload": f"c4: d={d}, n={n}, nrhs={K}", "eps": spec["epsilon"],
-                   "stall_window": "off",
-                   "profile": ("exact (bitwise per-column reference trajectory)"
-                               if args.profile == "exact" else PROFILE_DESC["fast"]),
-                   "l2": "inputs larger than L2 (B 10.5 GB at c4)",
-                   "parallelism": f"column shards x{ws}", "columns_rank0": kc},
+        "config": workload_config("c4", d, n, spec["epsilon"], nrhs=K),
+        "profile": ("exact (bitwise per-column reference trajectory)"
+                    if args.profile == "exact" else PROFILE_DESC["fast"]),
+        "parallelism": f"column shards x{ws} (no data-path collective)", "columns_rank0": kc,
         "iterations_mean": float(iters.mean()), "iterations_max": int(iters.max()),
         "max_abs_err_vs_H_true": err,
         "setup_ms": t_setup / args.steps * 1e3, "loop_ms": per_loop * 1e3,
@@ -822,6 +970,21 @@ def main():
                          "allreduce (configs[4] as written)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    env_ws = os.environ.get("WORLD_SIZE")
+    if env_ws is None and args.gpus > 1:
+        # one process per GPU: re-launch under torch.distributed.run (NCCL, 127.0.0.1)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if env_ws is not None and int(env_ws) != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} does not match WORLD_SIZE={env_ws}"}),
+              flush=True)
+        return 2
     ws, rank, local, dist = dist_setup(args)
     try:
         if args.impl == "reference":

@@ -281,6 +281,48 @@ int alnnls_gram_partial_device(alnnls_ctx* ctx, uint64_t rows, uint64_t n, const
                                uint64_t lda, const double* db, int profile, double* dH,
                                double* datb);
 
+/* Packed upper triangle of a symmetric n x n matrix (device pointers): entry
+ * (i, j), i <= j, at j*(j+1)/2 + i. pack: dP <- upper(dH); unpack: dH <- dP,
+ * mirrored to both triangles. The allreduce setup moves n(n+1)/2 doubles with
+ * them instead of n^2 (rowblock.allreduce_setup). Return after completion. */
+int alnnls_pack_upper_device(alnnls_ctx* ctx, uint64_t n, const double* dH, double* dP);
+int alnnls_unpack_upper_device(alnnls_ctx* ctx, uint64_t n, const double* dP, double* dH);
+
+/* ---- finish: unscale + residual (nnls.hpp:141-142) ------------------------
+ * x = unscale(y, sys, n) (nnls.hpp:87-96) with the rescale bookkeeping (scale,
+ * retained, dropped) of the last setup / solve / rescale on ctx, and
+ * *residual_sq = residual_norm_sq(A, b, x) (nnls.hpp:115-123), recomputed from
+ * A (d x n, column-major) and b. y has m = the retained count entries. EINVAL
+ * when m or n do not match that bookkeeping (reference: "unscale: dimension
+ * mismatch"). Host buffers. */
+int alnnls_finish(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A, const double* b,
+                  const double* y, uint64_t m, double* x, double* residual_sq);
+
+/* ---- batched multi-RHS across GPUs: one context per device ---------------
+ * Column shards of B (contiguous, balanced like paper_1502_01645_b200/
+ * sharding.py) run concurrently, one host thread per context, each through
+ * alnnls_solve_nnls_batched on its own device; no data-path collective (every
+ * column is an independent solve_nnls). Same outputs as the one-context call
+ * (column j bitwise solve_nnls(A, B[:, j], cfg) under EXACT). out: times are the
+ * max over contexts, iterations / multiplies / numeric_failure are combined. On
+ * failure the first failing context's status is returned and its message is
+ * copied to ctxs[0]. */
+int alnnls_solve_nnls_batched_multi(alnnls_ctx* const* ctxs, int nctx, uint64_t d, uint64_t n,
+                                    const double* A, uint64_t nrhs, const double* B,
+                                    const alnnls_config* cfg, double* X,
+                                    alnnls_column_result* cols, alnnls_summary* out);
+/* Dense product on device pointers, column j = matvec(A, H[:, j]) bit for bit
+ * (linalg.hpp:179-188: one ascending chain of rounded products and sums per
+ * entry). C (rows x cols, ldc) = A (rows x inner, lda) H (inner x cols, ldh).
+ * Forms c4's right-hand sides B = A H_true identically on any host (the
+ * harness's exact-order generator computes the same bits), and the NMF
+ * product W H. Returns after completion. */
+int alnnls_matmat_device(alnnls_ctx* ctx, uint64_t rows, uint64_t inner, uint64_t cols,
+                         const double* dA, uint64_t lda, const double* dH, uint64_t ldh,
+                         double* dC, uint64_t ldc);
+/* Number of visible CUDA devices (0 without a GPU; no context needed). */
+int alnnls_device_count(void);
+
 #ifdef __cplusplus
 }
 #endif

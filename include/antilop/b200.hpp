@@ -17,9 +17,8 @@ namespace antilop::b200 {
 
 class Context {
  public:
-  Context() {
-    const char* env = std::getenv("ALNNLS_DEVICE");
-    const int dev = env ? std::atoi(env) : 0;
+  Context() : Context(default_device()) {}
+  explicit Context(int dev) {
     const int st = alnnls_create(&ctx_, dev);
     if (st != ALNNLS_OK)
       throw std::runtime_error("antilop: no usable sm_100 GPU (alnnls_create status " +
@@ -29,6 +28,10 @@ class Context {
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
   alnnls_ctx* get() const noexcept { return ctx_; }
+  static int default_device() {
+    const char* env = std::getenv("ALNNLS_DEVICE");
+    return env ? std::atoi(env) : 0;
+  }
 
  private:
   alnnls_ctx* ctx_ = nullptr;

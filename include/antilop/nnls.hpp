@@ -127,3 +127,6 @@ inline std::string result_summary_json(const NnlsResult& r) {
 }
 
 }  // namespace antilop
+
+// The batched multi-RHS entry (a18) rides on the same facade.
+#include "antilop/batched.hpp"

@@ -26,6 +26,8 @@ EXPORTS = [
     "alnnls_gram_partial_device",
     "alnnls_solve_accelerated", "alnnls_solve_accelerated_device", "alnnls_solve_anti_accelerated",
     "alnnls_solve_anti_accelerated_device",
+    "alnnls_pack_upper_device", "alnnls_unpack_upper_device", "alnnls_finish",
+    "alnnls_solve_nnls_batched_multi", "alnnls_device_count", "alnnls_matmat_device",
 ]
 
 _lib = None
@@ -99,6 +101,14 @@ def load():
         "alnnls_residual_rowblock_device": ([vp, u64, u64, vp, u64, vp, vp, C.c_double,
                                              C.POINTER(C.c_double)], i32),
         "alnnls_gram_partial_device": ([vp, u64, u64, vp, u64, vp, i32, vp, vp], i32),
+        "alnnls_pack_upper_device": ([vp, u64, vp, vp], i32),
+        "alnnls_unpack_upper_device": ([vp, u64, vp, vp], i32),
+        "alnnls_finish": ([vp, u64, u64, vp, vp, vp, u64, vp, C.POINTER(C.c_double)], i32),
+        "alnnls_solve_nnls_batched_multi": ([C.POINTER(vp), i32, u64, u64, vp, u64, vp,
+                                             C.POINTER(abi.Config), vp, vp,
+                                             C.POINTER(abi.Summary)], i32),
+        "alnnls_device_count": ([], i32),
+        "alnnls_matmat_device": ([vp, u64, u64, u64, vp, u64, vp, u64, vp, u64], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -281,6 +281,36 @@ class Solver:
             self.ctx, rows, n, C.c_void_p(A_ptr), lda, C.c_void_p(b_ptr) if b_ptr else None,
             int(profile), C.c_void_p(H_ptr), C.c_void_p(atb_ptr) if atb_ptr else None))
 
+    def pack_upper_device(self, n, H_ptr, P_ptr):
+        """Packed upper triangle (j(j+1)/2 + i) of the symmetric n x n dH into dP."""
+        self._check(self.lib.alnnls_pack_upper_device(self.ctx, n, C.c_void_p(H_ptr),
+                                                      C.c_void_p(P_ptr)))
+
+    def unpack_upper_device(self, n, P_ptr, H_ptr):
+        """dH (both triangles) from the packed upper triangle dP."""
+        self._check(self.lib.alnnls_unpack_upper_device(self.ctx, n, C.c_void_p(P_ptr),
+                                                        C.c_void_p(H_ptr)))
+
+    def matmat_device(self, rows, inner, cols, A_ptr, lda, H_ptr, ldh, C_ptr, ldc):
+        """C = A H on device pointers, column j bitwise matvec(A, H[:, j])."""
+        self._check(self.lib.alnnls_matmat_device(self.ctx, rows, inner, cols, C.c_void_p(A_ptr),
+                                                  lda, C.c_void_p(H_ptr), ldh, C.c_void_p(C_ptr),
+                                                  ldc))
+
+    def finish(self, A, b, y):
+        """x = unscale(y, sys, n) and ||A x - b||^2 (nnls.hpp:141-142) with the rescale
+        bookkeeping of the last setup / solve on this context."""
+        A = _fortran(A)
+        b = np.ascontiguousarray(_f64(b, "b")).reshape(-1)
+        y = np.ascontiguousarray(_f64(y, "y")).reshape(-1)
+        d, n = A.shape
+        x = np.zeros(n)
+        r = C.c_double(0.0)
+        self._check(self.lib.alnnls_finish(self.ctx, d, n, _ptr(A), _ptr(b),
+                                           _ptr(y) if len(y) else None, len(y), _ptr(x),
+                                           C.byref(r)))
+        return x, r.value
+
     def residual_rowblock_device(self, rows, n, A_ptr, lda, b_ptr, x_ptr, s_in=0.0):
         out = C.c_double(0.0)
         self._check(self.lib.alnnls_residual_rowblock_device(
@@ -477,6 +507,35 @@ class Solver:
 
 
 _default = {}
+
+
+def device_count():
+    """Visible CUDA devices (0 without a GPU)."""
+    return int(load().alnnls_device_count())
+
+
+def solve_nnls_batched_multi(solvers, A, B, config: SolverConfig = SolverConfig()):
+    """Batched solve with the columns of B sharded over several contexts (one per
+    GPU: alnnls_solve_nnls_batched_multi, one host thread per context, no
+    collective). Returns (X, [per-column dict], summary)."""
+    A = _fortran(A)
+    B = _fortran(B)
+    if A.shape[0] != B.shape[0]:
+        raise ValueError("solve_nnls: A and b dimension mismatch")
+    d, n = A.shape
+    k = B.shape[1]
+    X = np.zeros((n, k), order="F")
+    cols = (abi.ColumnResult * k)()
+    summ = abi.Summary()
+    cfg = config.to_abi(record_multiplies=False)
+    arr = (C.c_void_p * len(solvers))(*[s.ctx.value for s in solvers])
+    lib = load()
+    st = lib.alnnls_solve_nnls_batched_multi(arr, len(solvers), d, n, _ptr(A), k, _ptr(B),
+                                             C.byref(cfg), _ptr(X), C.cast(cols, C.c_void_p),
+                                             C.byref(summ))
+    if st != abi.OK:
+        solvers[0]._raise(st)
+    return X, [Solver._col(c) for c in cols], summ
 
 
 def default_solver(device=0):

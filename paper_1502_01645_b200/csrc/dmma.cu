@@ -13,6 +13,8 @@
 // m16n8k8 accumulators; k slabs of 16 staged by cp.async (16 B chunks) through
 // a 4-deep ring. Shared tiles are [column][k] with the 16 B chunk index XOR-
 // swizzled by 2 (column & 3), so both fragment loads are bank-conflict-free.
+#include <cuda.h>
+
 #include "common.cuh"
 #include "gemv.cuh"
 #include "kernels.cuh"
@@ -192,6 +194,193 @@ __global__ void __launch_bounds__(TT, 1) syrk_dmma_kernel(SetupArgs s, int mode)
       }
 }
 
+
+// ===== v2: TMA-fed, stream-K persistent DMMA Gram / A^T B (north_star: "DMMA tensor
+// cores fed by TMA-staged shared-memory tiles") =====================================
+// Operand slabs (128 columns x 16 k of A, and of A or B) arrive by
+// cp.async.bulk.tensor.2d (TMA, UTMALDG) with the hardware 128-byte swizzle
+// (element (r, k) at r*128 + (((k>>1) ^ (r&7)) << 4) + (k&1)*8 bytes): the
+// m16n8k8 fragment loads of a warp then touch every bank exactly twice (two
+// wavefronts for 256 bytes, conflict-free), and out-of-range rows / columns are
+// zero-filled by the TMA unit (ragged shapes need no special code).
+// Schedule: persistent CTAs, one per SM; the (tile, k-slab) units are split into
+// equal contiguous ranges (stream-K), so no wave is ragged. A tile cut between
+// CTAs is finished by the CTA holding its first slab (k = 0), which processes it
+// LAST in its range, by then the later CTAs (which hold the rest at the START of
+// their ranges) have published their partial accumulators; it adds them in CTA
+// order (a fixed order: deterministic run to run).
+// Pipeline: kStages slab pairs in shared memory, full/empty mbarriers; thread 0
+// (also a consumer) refills the stage every warp has released.
+constexpr int kStages2 = 6;  // 6 x 32 KB; the 128 KB epilogue tile reuses them
+constexpr uint32_t kSlabBytes = TB * TK * sizeof(double);  // 16 KB per operand slab
+constexpr size_t kDmma2Smem = (size_t)kStages2 * 2 * kSlabBytes + 1024;  // + alignment slack
+
+struct TmaArgs {
+  CUtensorMap mapA;  // A: dims {d, n}, box {16, 128}
+  CUtensorMap mapB;  // B (mode 2) or A again
+  int tiles;         // output tiles (upper triangle, or the full grid in mode 2)
+  int nk;            // k slabs per tile
+  int nti;           // tile rows (mode 2 grid decode)
+  double* ws;        // [grid][128*128] partial tiles of cut tiles
+  int* flags;        // [grid] partial published (zeroed before the launch)
+  int accumulate;    // mode 0: H += result instead of H = result
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int swz128(int r, int k) {  // double index in a TMA 128B-swizzled slab
+  return r * TK + ((((k >> 1) ^ (r & 7))) << 1) + (k & 1);
+}
+
+__device__ __forceinline__ void tile_coords(int mode, int t, int nti, int& ti, int& tj) {
+  if (mode == 2) {
+    ti = t % nti;
+    tj = t / nti;
+  } else {
+    tri_tile_u(t, ti, tj);
+  }
+}
+
+__global__ void __launch_bounds__(TT, 1)
+    syrk_tma_kernel(const __grid_constant__ TmaArgs ta, SetupArgs s, int mode) {
+  extern __shared__ uint8_t dm2_raw[];
+  double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(dm2_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kStages2];
+  __shared__ __align__(8) uint64_t empty[kStages2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+  const long long U = (long long)ta.tiles * ta.nk;
+  const int G = gridDim.x, c = blockIdx.x;
+  const long long u0 = U * c / G, u1 = U * (c + 1) / G;
+  if (tid == 0) {
+    for (int st = 0; st < kStages2; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], TT / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto slabA = [&](int st) { return sm + (size_t)st * 2 * (TB * TK); };
+  auto slabB = [&](int st) { return sm + (size_t)st * 2 * (TB * TK) + TB * TK; };
+  double* tile_s = sm;  // epilogue staging [128 j][128 i] over the (drained) stages
+  long long q = 0;      // units consumed by this CTA (stage / phase counter)
+  long long u = u0;
+  while (u < u1) {
+    // ---- one segment: tile `tile`, slabs [kb0, kb1) ----
+    const int tile = (int)(u / ta.nk), kb0 = (int)(u % ta.nk);
+    const long long tstart = (long long)tile * ta.nk, tend = tstart + ta.nk;
+    const int kb1 = (int)((tend < u1 ? tend : u1) - tstart);
+    const int len = kb1 - kb0;
+    int ti, tj;
+    tile_coords(mode, tile, ta.nti, ti, tj);
+    auto issue = [&](long long qq, int kb) {  // thread 0: load slab kb as unit qq
+      const int st = (int)(qq % kStages2);
+      const long long round = qq / kStages2;
+      if (round >= 1) mbar_wait(&empty[st], (uint32_t)((round - 1) & 1));
+      mbar_arrive_expect_tx(&full[st], 2 * kSlabBytes);
+      tma_load_2d(slabA(st), &ta.mapA, kb * TK, ti * TB, &full[st]);
+      tma_load_2d(slabB(st), &ta.mapB, kb * TK, tj * TB, &full[st]);
+    };
+    if (tid == 0)
+      for (int k = 0; k < len && k < kStages2 - 1; ++k) issue(q + k, kb0 + k);
+    double acc[4][4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
+    for (int k = 0; k < len; ++k, ++q) {
+      if (tid == 0 && k + kStages2 - 1 < len) issue(q + kStages2 - 1, kb0 + k + kStages2 - 1);
+      const int st = (int)(q % kStages2);
+      mbar_wait(&full[st], (uint32_t)((q / kStages2) & 1));
+      const double* as = slabA(st);
+      const double* bs = slabB(st);
+#pragma unroll
+      for (int ks = 0; ks < TK; ks += 8) {
+        double af[4][4], bf[4][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int r = wm * 64 + mi * 16 + g;
+          af[mi][0] = as[swz128(r, ks + t)];
+          af[mi][1] = as[swz128(r + 8, ks + t)];
+          af[mi][2] = as[swz128(r, ks + t + 4)];
+          af[mi][3] = as[swz128(r + 8, ks + t + 4)];
+        }
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          const int r = wn * 32 + ni * 8 + g;
+          bf[ni][0] = bs[swz128(r, ks + t)];
+          bf[ni][1] = bs[swz128(r, ks + t + 4)];
+        }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    u = tstart + kb1;
+    // ---- epilogue: the stages are drained; stage the tile through shared memory ----
+    __syncthreads();
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int il = wm * 64 + mi * 16 + g + (e >> 1) * 8;
+          const int jl = wn * 32 + ni * 8 + 2 * t + (e & 1);
+          tile_s[jl * TB + il] = acc[mi][ni][e];
+        }
+    __syncthreads();
+    const bool first = tstart >= u0;  // this CTA holds slab 0 of the tile: it finishes it
+    if (!first) {                     // publish the partial for the finisher (previous CTA)
+      double* wsl = ta.ws + (size_t)c * TB * TB;
+      for (int e = tid; e < TB * TB; e += TT) wsl[e] = tile_s[e];
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicExch(ta.flags + c, 1);
+    } else {
+      // later CTAs holding the rest of the tile, added in CTA order (deterministic)
+      for (int c2 = c + 1; c2 < G && U * c2 / G < tend; ++c2) {
+        if (tid == 0)
+          while (atomicAdd(ta.flags + c2, 0) == 0) {
+          }
+        __syncthreads();
+        __threadfence();
+        const double* w2 = ta.ws + (size_t)c2 * TB * TB;
+        for (int e = tid; e < TB * TB; e += TT) tile_s[e] += __ldcg(w2 + e);
+        __syncthreads();
+      }
+      const int i0 = ti * TB, j0 = tj * TB;
+      for (int e = tid; e < TB * TB; e += TT) {
+        const int i = i0 + (e & (TB - 1)), j = j0 + e / TB;
+        if (i >= s.n) continue;
+        const double v = tile_s[e];
+        if (mode == 0 && ta.accumulate) {
+          if (i <= j && j < s.n) {
+            const double w = s.H[(size_t)j * s.n + i] + v;
+            s.H[(size_t)j * s.n + i] = w;
+            if (i != j) s.H[(size_t)i * s.n + j] = w;
+          }
+        } else {
+          store_out(s, mode, i, j, v);
+        }
+      }
+    }
+    __syncthreads();  // the staging area is stage memory again
+  }
+}
+
 }  // namespace
 
 bool syrk_dmma_supported(const SetupArgs& s, int mode) {
@@ -201,11 +390,67 @@ bool syrk_dmma_supported(const SetupArgs& s, int mode) {
          (reinterpret_cast<uintptr_t>(b) % 16 == 0);
 }
 
-cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream) {
+namespace {
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    (void)cudaGetLastError();
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+// rows x cols column-major fp64 (ld doubles): box 16 rows (k) x 128 columns, 128B swizzle
+bool make_map(CUtensorMap* m, const double* p, uint64_t rows, uint64_t cols, uint64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {rows, cols};
+  const cuuint64_t strides[1] = {ld * sizeof(double)};
+  const cuuint32_t box[2] = {TK, TB};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+size_t syrk_dmma_ws_doubles(int sm_count) { return (size_t)sm_count * TB * TB + 64; }
+
+cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream, int accumulate) {
   const int nt = (s.n + TB - 1) / TB;
   const int tiles = mode == 2 ? nt * ((s.nrhs + TB - 1) / TB) : nt * (nt + 1) / 2;
   if (tiles == 0) return cudaSuccess;
   if (!syrk_dmma_supported(s, mode)) return cudaErrorInvalidValue;
+  if (s.dm_ws && s.dm_flags && s.dm_ctas > 0) {
+    TmaArgs ta{};
+    const uint64_t ldb = mode == 2 ? s.ldb : s.lda;
+    if (make_map(&ta.mapA, s.A, (uint64_t)s.d, (uint64_t)s.n, s.lda) &&
+        make_map(&ta.mapB, mode == 2 ? s.B : s.A, (uint64_t)s.d,
+                 (uint64_t)(mode == 2 ? s.nrhs : s.n), ldb)) {
+      ta.tiles = tiles;
+      ta.nk = (s.d + TK - 1) / TK;
+      ta.nti = nt;
+      ta.ws = s.dm_ws;
+      ta.flags = s.dm_flags;
+      ta.accumulate = accumulate;
+      const int grid = tiles < s.dm_ctas ? tiles : s.dm_ctas;
+      if (cudaError_t e = smem_optin(syrk_tma_kernel, (int)kDmma2Smem)) return e;
+      cudaError_t e = cudaMemsetAsync(s.dm_flags, 0, sizeof(int) * grid, stream);
+      if (e != cudaSuccess) return e;
+      // all CTAs must be co-resident (finishers wait on later CTAs): one per SM
+      void* args[] = {&ta, const_cast<SetupArgs*>(&s), &mode};
+      return cudaLaunchCooperativeKernel((const void*)syrk_tma_kernel, dim3(grid), dim3(TT), args,
+                                         kDmma2Smem, stream);
+    }
+  }
+  if (accumulate) return cudaErrorInvalidValue;  // v1 has no accumulate epilogue
   if (cudaError_t e = smem_optin(syrk_dmma_kernel, (int)kDmmaSmem)) return e;
   syrk_dmma_kernel<<<tiles, TT, kDmmaSmem, stream>>>(s, mode);
   return cudaGetLastError();

@@ -171,6 +171,10 @@ struct SetupArgs {
   // starts from tpin[t] and ends in tpout[t] ([tiles][32][512]) instead of 0 / H
   const double* tpin;
   double* tpout;
+  // FAST DMMA Gram v2 (dmma.cu syrk_tma_kernel): stream-K partials and flags
+  double* dm_ws;
+  int* dm_flags;
+  int dm_ctas;
 };
 // CTAs for the stream-K exact SYRK of this shape (0: use one CTA per tile).
 int syrk_streamk_ctas(const SetupArgs& s, int mode, int sm_count);
@@ -184,7 +188,10 @@ cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream);
 cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream);
 // FAST profile: the same three modes on the fp64 tensor cores (dmma.cu). Needs
 // even leading dimensions and 16-byte aligned operands (syrk_dmma_supported).
-cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream);
+// v2 (when s.dm_ws / dm_flags / dm_ctas are set): TMA-staged, stream-K persistent
+// kernel; accumulate = 1 adds into H (mode 0) instead of overwriting it.
+cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream, int accumulate = 0);
+size_t syrk_dmma_ws_doubles(int sm_count);
 bool syrk_dmma_supported(const SetupArgs& s, int mode);
 // q (mode 1) or hvec = -(A^T b) (mode 0) from the column chains' A^T b.
 cudaError_t launch_q_from_atb(const SetupArgs& s, int mode, cudaStream_t stream);
@@ -228,6 +235,12 @@ cudaError_t launch_check_finite(const double* p, uint64_t rows, uint64_t cols, u
 // that is not >= 0 (negative or NaN) -> *flag = 1
 cudaError_t launch_check_matrix(const double* p, uint64_t rows, uint64_t cols, uint64_t ld,
                                 int kind, int* flag, cudaStream_t stream);
+// dir 0: packed upper triangle P (j(j+1)/2 + i) of the symmetric H; dir 1: H from P (mirrored)
+cudaError_t launch_pack_upper(double* H, uint64_t n, double* P, int dir, cudaStream_t stream);
+// C (rows x cols) = A (rows x inner) H (inner x cols), each column the reference's
+// matvec order (bitwise matvec(A, H[:, j]))
+cudaError_t launch_matmat(const double* A, uint64_t lda, int rows, int inner, const double* H,
+                          uint64_t ldh, int cols, double* C, uint64_t ldc, cudaStream_t stream);
 // pads: copy a rows x cols col-major block into a buffer with leading dimension ld_dst.
 cudaError_t launch_copy_pad(const double* src, uint64_t ld_src, double* dst, uint64_t ld_dst,
                             uint64_t rows, uint64_t cols, cudaStream_t stream);

@@ -549,6 +549,40 @@ __global__ void check_matrix_kernel(const double* p, uint64_t rows, uint64_t col
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
 }
 
+// Packed upper triangle of a symmetric n x n column-major matrix: entry (i, j),
+// i <= j, at j (j + 1) / 2 + i. dir 0 packs, dir 1 unpacks and mirrors (the
+// c5 allreduce moves n (n + 1) / 2 doubles instead of n^2).
+__global__ void pack_upper_kernel(double* H, uint64_t n, double* P, int dir) {
+  const uint64_t total = n * n;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = e / n, i = e % n;
+    const uint64_t a = i <= j ? i : j, c = i <= j ? j : i;
+    const uint64_t pidx = c * (c + 1) / 2 + a;
+    if (dir == 0) {
+      if (i <= j) P[pidx] = H[e];
+    } else {
+      H[e] = P[pidx];
+    }
+  }
+}
+
+// C[:, j] = matvec(A, H[:, j]) in the reference's order (linalg.hpp:179-188: the
+// column sweep y[i] += M(i, t) v[t], t ascending, is per row one chain of
+// rounded products then rounded sums). One thread per output (i, j); a block
+// covers 256 consecutive rows of one column, so A's column t is read coalesced
+// and H(t, j) is a broadcast.
+__global__ void matmat_kernel(const double* __restrict__ A, uint64_t lda, int rows, int inner,
+                              const double* __restrict__ H, uint64_t ldh, double* C, uint64_t ldc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t j = blockIdx.y;
+  if (i >= rows) return;
+  const double* h = H + j * ldh;
+  double s = 0.0;
+  for (int t = 0; t < inner; ++t) s = xmac(s, A[(uint64_t)t * lda + i], __ldg(h + t));
+  C[j * ldc + i] = s;
+}
+
 __global__ void copy_pad_kernel(const double* src, uint64_t ld_src, double* dst, uint64_t ld_dst,
                                 uint64_t rows, uint64_t cols) {
   const uint64_t total = rows * cols;
@@ -738,6 +772,27 @@ cudaError_t launch_check_matrix(const double* p, uint64_t rows, uint64_t cols, u
   if (blocks > 148 * 16) blocks = 148 * 16;
   check_matrix_kernel<<<(unsigned)blocks, 256, 0, stream>>>(p, rows, cols, ld, kind, flag);
   return cudaGetLastError();
+}
+
+cudaError_t launch_pack_upper(double* H, uint64_t n, double* P, int dir, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  uint64_t blocks = (n * n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  pack_upper_kernel<<<(unsigned)blocks, 256, 0, stream>>>(H, n, P, dir);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_matmat(const double* A, uint64_t lda, int rows, int inner, const double* H,
+                          uint64_t ldh, int cols, double* C, uint64_t ldc, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  for (int j0 = 0; j0 < cols; j0 += 65535) {  // gridDim.y limit
+    const int nc = cols - j0 < 65535 ? cols - j0 : 65535;
+    matmat_kernel<<<dim3((rows + 255) / 256, nc), 256, 0, stream>>>(
+        A, lda, rows, inner, H + (uint64_t)j0 * ldh, ldh, C + (uint64_t)j0 * ldc, ldc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_copy_pad(const double* src, uint64_t ld_src, double* dst, uint64_t ld_dst,

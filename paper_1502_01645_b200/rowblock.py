@@ -105,24 +105,45 @@ def chain_relay(dist, rank, world, state, compute, sync=None):
     return out
 
 
-def allreduce_setup(dist, world, n, compute, device):
+def _pack_torch(H, P):
+    n = H.shape[0]
+    tri = torch.triu_indices(n, n, device=H.device)
+    P.copy_(H[tri[0], tri[1]])
+
+
+def _unpack_torch(P, H):
+    n = H.shape[0]
+    tri = torch.triu_indices(n, n, device=H.device)
+    H[tri[0], tri[1]] = P
+    H[tri[1], tri[0]] = P
+
+
+def allreduce_setup(dist, world, n, compute, device, pack=None, unpack=None):
     """BASELINE.json configs[4] as written (SURVEY.md §8e variant (i)): every rank
     forms the partial Gram of its row block and its partial A^T b, and the
     partials are summed with ONE allreduce (NCCL over NVLink between GPUs, gloo
-    in the CPU tests). H and A^T b share one buffer so the single collective
-    moves both: n*n + n doubles (H is symmetric, so its n x n view is the same
-    in either storage order).
+    in the CPU tests). The collective moves the packed upper triangle of H and
+    A^T b in one buffer: n(n+1)/2 + n doubles (1.07 GB at c5 instead of 2.15 GB
+    for both triangles; H is exactly symmetric, so the lower half is mirrored
+    back afterwards).
 
-    compute(H, atb) fills this rank's partials in place. Returns the summed
-    (H, atb) on every rank. The cross-rank sum order is the collective's, so H
-    equals the reference's gram only within rounding; the pipelined_gram path
-    is the bitwise one."""
-    buf = torch.empty(n * n + n, dtype=torch.float64, device=device)
-    H = buf[: n * n].view(n, n)
-    atb = buf[n * n:]
+    compute(H, atb) fills this rank's partials in place (H: n x n, both
+    triangles; atb: a view into the collective's buffer). pack(H, P) / unpack(P,
+    H) convert to and from the packed layout (the GPU path passes the C ABI's
+    alnnls_pack_upper_device / alnnls_unpack_upper_device; the default uses
+    torch indexing, for small CPU tests). Returns the summed (H, atb) on every
+    rank. The cross-rank sum order is the collective's, so H equals the
+    reference's gram only within rounding; the pipelined_gram path is the
+    bitwise one."""
+    npk = n * (n + 1) // 2
+    H = torch.empty((n, n), dtype=torch.float64, device=device)
+    buf = torch.empty(npk + n, dtype=torch.float64, device=device)
+    atb = buf[npk:]
     compute(H, atb)
+    (pack or _pack_torch)(H, buf[:npk])
     if dist is not None and world > 1:
         dist.all_reduce(buf)
+    (unpack or _unpack_torch)(buf[:npk], H)
     return H, atb
 
 

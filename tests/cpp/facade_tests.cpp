@@ -65,6 +65,30 @@ NqpProblem lopsided() { return NqpProblem(DenseMatrix(2, 2, {1.0, 0.1, 0.1, 9.0}
 }  // namespace
 
 int main() {
+  run("batched multi-RHS (solve_nnls_batched, num_gpus)", [] {
+    const std::size_t d = 400, n = 60, k = 9;
+    std::vector<double> av(d * n), bv(d * k);
+    std::uint64_t st = 88172645463325252ull;
+    auto u01 = [&] { st ^= st << 13; st ^= st >> 7; st ^= st << 17; return (st >> 11) * 0x1.0p-53; };
+    for (auto& v : av) v = u01();
+    for (auto& v : bv) v = 2.0 * u01();
+    const DenseMatrix A(d, n, av), B(d, k, bv);
+    SolverConfig cfg;
+    cfg.epsilon = 1e-8;
+    cfg.stall_window = 1000000000;
+    const auto r = solve_nnls_batched(A, B, cfg, 1);
+    REQUIRE(r.X.rows() == n && r.X.cols() == k && r.columns.size() == k);
+    for (std::size_t j = 0; j < k; ++j) {
+      std::vector<double> col(bv.begin() + j * d, bv.begin() + (j + 1) * d);
+      const auto one = solve_nnls(A, Vector(col), cfg);
+      for (std::size_t i = 0; i < n; ++i) REQUIRE(r.X(i, j) == one.x[i]);
+      REQUIRE(r.columns[j].iterations == one.inner.iterations());
+      REQUIRE(r.columns[j].termination == one.inner.termination);
+      REQUIRE(r.columns[j].residual_sq == one.residual_sq);
+    }
+    REQUIRE(throws<std::invalid_argument>([&] { solve_nnls_batched(A, B, cfg, 1000); }));
+    REQUIRE(throws<std::invalid_argument>([&] { solve_nnls_batched(A, DenseMatrix(d + 1, 2), cfg, 1); }));
+  });
   run("gram fixed examples", [] {  // test_linalg.cpp:57-81
     const DenseMatrix h = gram(DenseMatrix::from_rows({{1.0, 1.0}, {0.0, 1.0}}));
     REQUIRE(h(0, 0) == 1.0 && h(0, 1) == 1.0 && h(1, 0) == 1.0 && h(1, 1) == 2.0);

@@ -144,3 +144,79 @@ def test_allreduce_setup_c5_law(solver, oracle, profile):
                                                 db.data_ptr() + 8 * r0, dx.data_ptr(), chain)
     # the allreduce sums 4 partial chains instead: a different order of the same terms
     assert abs(sum(parts) - chain) <= 1e-12 * chain
+
+
+def test_pack_unpack_upper_roundtrip(solver):
+    """alnnls_pack_upper_device / alnnls_unpack_upper_device: the allreduce moves
+    n(n+1)/2 doubles; unpacking mirrors the upper triangle bit for bit."""
+    n = 333
+    rng = np.random.default_rng(3)
+    M = rng.standard_normal((n, n))
+    H = np.asfortranarray(M + M.T)
+    dH = torch.from_numpy(np.ascontiguousarray(H.T)).cuda()  # column-major
+    P = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device="cuda")
+    solver.pack_upper_device(n, dH.data_ptr(), P.data_ptr())
+    Pc = P.cpu().numpy()
+    j = 17
+    assert same_bits(Pc[j * (j + 1) // 2: j * (j + 1) // 2 + j + 1], H[: j + 1, j])
+    back = torch.full((n, n), np.nan, dtype=torch.float64, device="cuda")
+    solver.unpack_upper_device(n, P.data_ptr(), back.data_ptr())
+    assert same_bits(back.cpu().numpy().T.reshape(-1), H.reshape(-1, order="F"))
+
+
+def test_allreduce_setup_packed_world1(solver, oracle):
+    """rowblock.allreduce_setup with the GPU pack/unpack (world 1): exactly the
+    partial Gram, mirrored, and the A^T b chains."""
+    from paper_1502_01645_b200.rowblock import allreduce_setup
+    rng = np.random.default_rng(9)
+    d, n = 500, 210
+    A = np.asfortranarray(rng.standard_normal((d, n)))
+    b = rng.standard_normal(d)
+    dA = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    db = torch.from_numpy(b).cuda()
+
+    def partial(Hm, atb):
+        solver.gram_partial_device(d, n, dA.data_ptr(), d, db.data_ptr(), Hm.data_ptr(),
+                                   atb.data_ptr(), profile=0)
+
+    H, atb = allreduce_setup(None, 1, n, partial, "cuda",
+                             pack=lambda Hm, P: solver.pack_upper_device(n, Hm.data_ptr(), P.data_ptr()),
+                             unpack=lambda P, Hm: solver.unpack_upper_device(n, P.data_ptr(), Hm.data_ptr()))
+    assert same_bits(H.cpu().numpy().reshape(-1), oracle.gram(A).reshape(-1, order="F"))
+    assert same_bits(atb.cpu().numpy(), oracle.transpose_matvec(A, b))
+
+
+def test_finish_matches_solve_nnls(solver):
+    """alnnls_finish (unscale + residual, nnls.hpp:141-142) reproduces solve_nnls's
+    x and residual from its inner solution; dimension mismatches are EINVAL."""
+    from paper_1502_01645_b200 import instances
+    inst = instances.make_config("c1", d=300, n=150, seed=21)
+    A, b = inst["A"], inst["b"]
+    A[:, 7] = 0.0  # a dropped column: unscale writes 0 there
+    r = solver.solve_nnls(A, b, SolverConfig(epsilon=1e-8, stall_window=10**9))
+    x, res = solver.finish(A, b, r.inner.x)
+    assert same_bits(x, r.x) and same_bits([res], [r.residual_sq])
+    assert x[7] == 0.0
+    with pytest.raises(ValueError):
+        solver.finish(A, b, r.inner.x[:-1])
+
+
+def test_batched_multi_context_shards_match(solver):
+    """alnnls_solve_nnls_batched_multi: column shards over several contexts (here
+    three contexts on the one GPU this box has) give the one-context results bit
+    for bit (every column is an independent solve)."""
+    from paper_1502_01645_b200 import instances
+    from paper_1502_01645_b200.api import Solver, solve_nnls_batched_multi
+    inst = instances.make_batched(d=1500, n=128, nrhs=37, seed=5)
+    cfg = SolverConfig(epsilon=1e-8, stall_window=10**9)
+    X1, c1, _ = solver.solve_nnls_batched(inst["A"], inst["B"], cfg)
+    extra = [Solver(0), Solver(0)]
+    try:
+        X3, c3, summ = solve_nnls_batched_multi([solver] + extra, inst["A"], inst["B"], cfg)
+    finally:
+        for s in extra:
+            s.close()
+    assert same_bits(X3.reshape(-1), X1.reshape(-1))
+    assert [c["iterations"] for c in c3] == [c["iterations"] for c in c1]
+    assert same_bits([c["residual_sq"] for c in c3], [c["residual_sq"] for c in c1])
+    assert summ.iterations == sum(c["iterations"] for c in c1)
