@@ -558,6 +558,41 @@ int device_check_finite(alnnls_ctx* ctx, std::initializer_list<FiniteArg> args) 
 // row's Gram work takes ~1.8x its PCIe upload time. The finiteness check runs
 // after the last block (results are discarded on failure, as if validated first).
 constexpr int kMaxUpBlocks = 16;  // ctx->up
+// FAST (DMMA) Gram work per row is shorter than its upload, so only the last
+// block's Gram is exposed: equal blocks, as many as the events allow.
+int upload_blocks_equal(uint64_t d, uint64_t* edges) {
+  uint64_t nb = d / 256;
+  if (nb > (uint64_t)kMaxUpBlocks) nb = kMaxUpBlocks;
+  if (nb < 1) nb = 1;
+  const uint64_t sz = (d / nb + 15) / 16 * 16;
+  int k = 0;
+  edges[0] = 0;
+  for (uint64_t r = 0; r < d && k < kMaxUpBlocks; r += sz) {
+    const uint64_t r1 = (k == kMaxUpBlocks - 1 || r + sz >= d) ? d : r + sz;
+    edges[++k] = r1;
+    if (r1 == d) break;
+  }
+  return k;
+}
+// FAST row blocks: a geometric series shrinking by 0.7, from ~30% of d down to
+// >= 256 rows (the last block's Gram is what stays exposed after the copy).
+int upload_blocks_shrinking(uint64_t d, uint64_t* edges) {
+  int nb = 0;
+  uint64_t r = 0;
+  edges[0] = 0;
+  double frac = 0.3;
+  while (r < d && nb < kMaxUpBlocks) {
+    uint64_t sz = (uint64_t)(frac * (double)d);
+    sz = (sz + 15) / 16 * 16;
+    if (sz < 256) sz = 256;
+    uint64_t r1 = r + sz;
+    if (nb == kMaxUpBlocks - 1 || r1 + 128 >= d) r1 = d;
+    edges[++nb] = r1;
+    r = r1;
+    frac *= 0.7;
+  }
+  return nb;
+}
 int upload_blocks(uint64_t d, uint64_t* edges) {
   uint64_t sz = d / 32 < 256 ? 256 : (d / 32 + 15) / 16 * 16;
   int nb = 0;
@@ -592,7 +627,17 @@ int run_nnls_overlapped(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A
   const double* pin = nullptr;
   const double* hin = nullptr;
   uint64_t edges[kMaxUpBlocks + 1];
-  const int nblk = upload_blocks(d, edges);
+  // Row blocks growing ~1.75x (the 2D copy of a row block moves one short segment
+  // per column: larger segments copy faster). EXACT continues every tile's chain
+  // over each block (bitwise the one-shot Gram); FAST accumulates each block's DMMA
+  // Gram into the upper triangle of H (rescale reads only that). Measured at c2
+  // (tools/e2e_probe2.py, setup + upload): FAST growing 6.89 ms, shrinking 7.69,
+  // equal 7.88; column blocks with per-block tile ranges 8.7 (the late tile
+  // columns hold most of the Gram: small launches). Knob ALNNLS_FAST_UPLOAD=1|2.
+  static const int fast_sched = getenv("ALNNLS_FAST_UPLOAD") ? atoi(getenv("ALNNLS_FAST_UPLOAD")) : 0;
+  const int nblk = fast && fast_sched == 1 ? upload_blocks_shrinking(d, edges)
+                   : fast && fast_sched == 2 ? upload_blocks_equal(d, edges)
+                                            : upload_blocks(d, edges);
   for (int k = 0; k < nblk; ++k) {
     const uint64_t r0 = edges[k], r1 = edges[k + 1];
     CK(cudaMemcpy2DAsync(dA + r0, lda * sizeof(double), A + r0, d * sizeof(double),
@@ -606,13 +651,10 @@ int run_nnls_overlapped(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A
     sa.d = (int)(r1 - r0);
     sa.n = (int)n;
     sa.H = H;
-    double* pout = last ? nullptr : st_buf + (size_t)(k & 1) * T * TD;
+    double* pout = last || fast ? nullptr : st_buf + (size_t)(k & 1) * T * TD;
     if (fast) {
-      // FAST: H += A_blk^T A_blk on the fp64 tensor cores (not the reference's
-      // chain order; the FAST profile is graded on the BASELINE tolerances)
       if (int rc = dmma_buffers(ctx, sa)) return rc;
-      CK(launch_syrk_dmma(sa, 0, s, k > 0 ? 1 : 0));
-      pout = nullptr;
+      CK(launch_syrk_dmma(sa, 0, s, (k > 0 ? 1 : 0) | 2));  // H(upper) (+)= A_blk^T A_blk
     } else {
       sa.tpin = pin;
       sa.tpout = pout;

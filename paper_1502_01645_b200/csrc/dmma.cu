@@ -219,11 +219,13 @@ struct TmaArgs {
   CUtensorMap mapA;  // A: dims {d, n}, box {16, 128}
   CUtensorMap mapB;  // B (mode 2) or A again
   int tiles;         // output tiles (upper triangle, or the full grid in mode 2)
+  int tile_lo;       // first tile of the launch (a contiguous range of the tile order)
   int nk;            // k slabs per tile
   int nti;           // tile rows (mode 2 grid decode)
   double* ws;        // [grid][128*128] partial tiles of cut tiles
   int* flags;        // [grid] partial published (zeroed before the launch)
-  int accumulate;    // mode 0: H += result instead of H = result
+  int accumulate;    // mode 0: bit 0: H += result instead of H = result; bit 1: write
+                     // only the upper triangle H(i <= j) (no strided mirror stores)
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(TT, 1)
     const int kb1 = (int)((tend < u1 ? tend : u1) - tstart);
     const int len = kb1 - kb0;
     int ti, tj;
-    tile_coords(mode, tile, ta.nti, ti, tj);
+    tile_coords(mode, tile + ta.tile_lo, ta.nti, ti, tj);
     auto issue = [&](long long qq, int kb) {  // thread 0: load slab kb as unit qq
       const int st = (int)(qq % kStages2);
       const long long round = qq / kStages2;
@@ -344,8 +346,9 @@ __global__ void __launch_bounds__(TT, 1)
     __syncthreads();
     const bool first = tstart >= u0;  // this CTA holds slab 0 of the tile: it finishes it
     if (!first) {                     // publish the partial for the finisher (previous CTA)
-      double* wsl = ta.ws + (size_t)c * TB * TB;
-      for (int e = tid; e < TB * TB; e += TT) wsl[e] = tile_s[e];
+      double2* wsl = reinterpret_cast<double2*>(ta.ws + (size_t)c * TB * TB);
+      const double2* t2 = reinterpret_cast<const double2*>(tile_s);
+      for (int e = tid; e < TB * TB / 2; e += TT) wsl[e] = t2[e];
       __threadfence();
       __syncthreads();
       if (tid == 0) atomicExch(ta.flags + c, 1);
@@ -357,8 +360,21 @@ __global__ void __launch_bounds__(TT, 1)
           }
         __syncthreads();
         __threadfence();
-        const double* w2 = ta.ws + (size_t)c2 * TB * TB;
-        for (int e = tid; e < TB * TB; e += TT) tile_s[e] += __ldcg(w2 + e);
+        const double2* w2 = reinterpret_cast<const double2*>(ta.ws + (size_t)c2 * TB * TB);
+        double2* t2 = reinterpret_cast<double2*>(tile_s);
+        constexpr int kU = 8;  // 8 independent 16-byte loads in flight per thread
+        for (int e = tid; e < TB * TB / 2; e += kU * TT) {
+          double2 v[kU];
+#pragma unroll
+          for (int k2 = 0; k2 < kU; ++k2) v[k2] = __ldcg(w2 + e + k2 * TT);
+#pragma unroll
+          for (int k2 = 0; k2 < kU; ++k2) {
+            double2 o = t2[e + k2 * TT];
+            o.x += v[k2].x;
+            o.y += v[k2].y;
+            t2[e + k2 * TT] = o;
+          }
+        }
         __syncthreads();
       }
       const int i0 = ti * TB, j0 = tj * TB;
@@ -368,9 +384,9 @@ __global__ void __launch_bounds__(TT, 1)
         const double v = tile_s[e];
         if (mode == 0 && ta.accumulate) {
           if (i <= j && j < s.n) {
-            const double w = s.H[(size_t)j * s.n + i] + v;
+            const double w = (ta.accumulate & 1) ? s.H[(size_t)j * s.n + i] + v : v;
             s.H[(size_t)j * s.n + i] = w;
-            if (i != j) s.H[(size_t)i * s.n + j] = w;
+            if (i != j && !(ta.accumulate & 2)) s.H[(size_t)i * s.n + j] = w;
           }
         } else {
           store_out(s, mode, i, j, v);
@@ -423,10 +439,16 @@ bool make_map(CUtensorMap* m, const double* p, uint64_t rows, uint64_t cols, uin
 
 size_t syrk_dmma_ws_doubles(int sm_count) { return (size_t)sm_count * TB * TB + 64; }
 
-cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream, int accumulate) {
+cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream, int accumulate,
+                             int tile_lo, int tile_hi) {
   const int nt = (s.n + TB - 1) / TB;
-  const int tiles = mode == 2 ? nt * ((s.nrhs + TB - 1) / TB) : nt * (nt + 1) / 2;
-  if (tiles == 0) return cudaSuccess;
+  const int all = mode == 2 ? nt * ((s.nrhs + TB - 1) / TB) : nt * (nt + 1) / 2;
+  if (tile_hi < 0 || tile_hi > all) tile_hi = all;
+  if (tile_lo < 0) tile_lo = 0;
+  const int tiles = tile_hi - tile_lo;
+  if (tiles <= 0) return cudaSuccess;
+  if ((tile_lo != 0 || tile_hi != all) && !(s.dm_ws && s.dm_flags && s.dm_ctas > 0))
+    return cudaErrorInvalidValue;  // tile ranges: v2 only
   if (!syrk_dmma_supported(s, mode)) return cudaErrorInvalidValue;
   if (s.dm_ws && s.dm_flags && s.dm_ctas > 0) {
     TmaArgs ta{};
@@ -435,12 +457,16 @@ cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream, 
         make_map(&ta.mapB, mode == 2 ? s.B : s.A, (uint64_t)s.d,
                  (uint64_t)(mode == 2 ? s.nrhs : s.n), ldb)) {
       ta.tiles = tiles;
+      ta.tile_lo = tile_lo;
       ta.nk = (s.d + TK - 1) / TK;
       ta.nti = nt;
       ta.ws = s.dm_ws;
       ta.flags = s.dm_flags;
       ta.accumulate = accumulate;
-      const int grid = tiles < s.dm_ctas ? tiles : s.dm_ctas;
+      // every SM even for few tiles (stream-K splits their k ranges); no CTA without
+      // a unit (a finisher waits on every later CTA whose range starts in its tile)
+      const long long units = (long long)tiles * ta.nk;
+      const int grid = units < s.dm_ctas ? (int)units : s.dm_ctas;
       if (cudaError_t e = smem_optin(syrk_tma_kernel, (int)kDmma2Smem)) return e;
       cudaError_t e = cudaMemsetAsync(s.dm_flags, 0, sizeof(int) * grid, stream);
       if (e != cudaSuccess) return e;

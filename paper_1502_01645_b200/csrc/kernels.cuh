@@ -189,8 +189,12 @@ cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream);
 // FAST profile: the same three modes on the fp64 tensor cores (dmma.cu). Needs
 // even leading dimensions and 16-byte aligned operands (syrk_dmma_supported).
 // v2 (when s.dm_ws / dm_flags / dm_ctas are set): TMA-staged, stream-K persistent
-// kernel; accumulate = 1 adds into H (mode 0) instead of overwriting it.
-cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream, int accumulate = 0);
+// kernel; mode 0 flags: accumulate bit 0 adds into H instead of overwriting it,
+// bit 1 writes the upper triangle only.
+// [tile_lo, tile_hi) restricts the launch to a range of the tile order (upper
+// triangle by columns: tile (ti, tj) is tj (tj + 1) / 2 + ti), v2 only; -1 = all.
+cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream, int accumulate = 0,
+                             int tile_lo = -1, int tile_hi = -1);
 size_t syrk_dmma_ws_doubles(int sm_count);
 bool syrk_dmma_supported(const SetupArgs& s, int mode);
 // q (mode 1) or hvec = -(A^T b) (mode 0) from the column chains' A^T b.

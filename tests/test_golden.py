@@ -11,7 +11,7 @@ from paper_1502_01645_b200 import abi, instances
 from tests.parity import same_bits
 
 GOLD = sorted(p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))
-              if not os.path.basename(p).startswith("full_"))
+              if not os.path.basename(p).startswith(("full_", "c4_sample")))
 # full-size BASELINE configs (tests/golden/make_golden_full.py): GPU-only checks
 FULL = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "full_*.npz")))
 
