@@ -320,6 +320,24 @@ int alnnls_solve_nnls_batched_multi(alnnls_ctx* const* ctxs, int nctx, uint64_t 
 int alnnls_matmat_device(alnnls_ctx* ctx, uint64_t rows, uint64_t inner, uint64_t cols,
                          const double* dA, uint64_t lda, const double* dH, uint64_t ldh,
                          double* dC, uint64_t ldc);
+/* ---- NMF by alternating NNLS (the paper's motivating use,
+ * PAPER.md:22) -----------------------------------------------------------------
+ * V (d x N) ~ W (d x k) H (k x N), W, H >= 0. Each outer iteration solves
+ *   H <- argmin_{H >= 0} ||W H - V||_F^2   (one solve_nnls(W, V[:, j], cfg) per column)
+ *   W <- argmin_{W >= 0} ||H^T W^T - V^T||_F^2 (one solve_nnls(H^T, V^T[:, i], cfg) per row)
+ * with the batched multi-RHS solver (one shared Gram per half step; the
+ * transposes are exact copies), so under EXACT every column of every half step
+ * is bitwise the reference's solve_nnls on the same inputs. W holds the start on
+ * entry and the result on exit; H is written. objective[t] (outer_iters entries,
+ * may be NULL) = ||V - W H||_F^2 after iteration t's H update, summed over the
+ * columns' residual_norm_sq (nnls.hpp:115-123) in column order. k <= 1024 (the
+ * batched kernel's bound). Device-pointer entry (all column-major, ld = rows)
+ * and host-buffer entry. */
+int alnnls_nmf_device(alnnls_ctx* ctx, uint64_t d, uint64_t N, uint64_t k, const double* dV,
+                      double* dW, double* dH, uint64_t outer_iters, const alnnls_config* cfg,
+                      double* objective);
+int alnnls_nmf(alnnls_ctx* ctx, uint64_t d, uint64_t N, uint64_t k, const double* V, double* W,
+               double* H, uint64_t outer_iters, const alnnls_config* cfg, double* objective);
 /* Number of visible CUDA devices (0 without a GPU; no context needed). */
 int alnnls_device_count(void);
 

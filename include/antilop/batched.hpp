@@ -93,4 +93,29 @@ inline BatchedNnlsResult solve_nnls_batched(const DenseMatrix& a, const DenseMat
   return out;
 }
 
+/// NMF by alternating NNLS (the use that motivates the batched
+/// solver): V (d x N) ~ W H with W, H >= 0. Each outer iteration is
+/// two batched solves on this thread's GPU context: H from W (one solve_nnls per
+/// column of V) and W from H^T (one per row of V); objective[t] = ||V - W H||_F^2
+/// after iteration t's H update. W0 (d x k, nonnegative) is the start.
+struct NmfResult {
+  DenseMatrix W;
+  DenseMatrix H;
+  std::vector<double> objective;
+};
+
+inline NmfResult nmf(const DenseMatrix& v, const DenseMatrix& w0, std::size_t outer_iters,
+                     const SolverConfig& config = {}) {
+  detail::require(v.rows() == w0.rows(), "nmf: V and W dimension mismatch");
+  const std::size_t d = v.rows(), n = v.cols(), k = w0.cols();
+  std::vector<double> w(w0.data().begin(), w0.data().end()), h(k * n);
+  std::vector<double> obj(outer_iters ? outer_iters : 1);
+  alnnls_config cfg = b200::to_abi(config);
+  cfg.record_multiplies = 0;
+  b200::check(alnnls_nmf(b200::ctx(), d, n, k, v.data().data(), w.data(), h.data(), outer_iters,
+                         &cfg, obj.data()));
+  obj.resize(outer_iters);
+  return NmfResult{DenseMatrix(d, k, std::move(w)), DenseMatrix(k, n, std::move(h)), std::move(obj)};
+}
+
 }  // namespace antilop

@@ -28,6 +28,7 @@ EXPORTS = [
     "alnnls_solve_anti_accelerated_device",
     "alnnls_pack_upper_device", "alnnls_unpack_upper_device", "alnnls_finish",
     "alnnls_solve_nnls_batched_multi", "alnnls_device_count", "alnnls_matmat_device",
+    "alnnls_nmf_device", "alnnls_nmf",
 ]
 
 _lib = None
@@ -109,6 +110,8 @@ def load():
                                              C.POINTER(abi.Summary)], i32),
         "alnnls_device_count": ([], i32),
         "alnnls_matmat_device": ([vp, u64, u64, u64, vp, u64, vp, u64, vp, u64], i32),
+        "alnnls_nmf_device": ([vp, u64, u64, u64, vp, vp, vp, u64, C.POINTER(abi.Config), vp], i32),
+        "alnnls_nmf": ([vp, u64, u64, u64, vp, vp, vp, u64, C.POINTER(abi.Config), vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

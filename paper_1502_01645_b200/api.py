@@ -291,6 +291,23 @@ class Solver:
         self._check(self.lib.alnnls_unpack_upper_device(self.ctx, n, C.c_void_p(P_ptr),
                                                         C.c_void_p(H_ptr)))
 
+    def nmf(self, V, W0, outer_iters, config: SolverConfig = SolverConfig()):
+        """NMF by alternating NNLS (alnnls_nmf): V (d x N) ~ W H, W >= 0, H >= 0.
+        W0 (d x k, nonnegative) is the start. Returns (W, H, objective per outer
+        iteration = ||V - W H||_F^2 after its H update)."""
+        V = _fortran(V)
+        W = np.array(_fortran(W0), order="F", copy=True)
+        d, N = V.shape
+        if W.shape[0] != d:
+            raise ValueError("nmf: V and W dimension mismatch")
+        k = W.shape[1]
+        H = np.zeros((k, N), order="F")
+        obj = np.zeros(max(1, outer_iters))
+        cfg = config.to_abi(record_multiplies=False)
+        self._check(self.lib.alnnls_nmf(self.ctx, d, N, k, _ptr(V), _ptr(W), _ptr(H), outer_iters,
+                                        C.byref(cfg), _ptr(obj)))
+        return W, H, obj[:outer_iters]
+
     def matmat_device(self, rows, inner, cols, A_ptr, lda, H_ptr, ldh, C_ptr, ldc):
         """C = A H on device pointers, column j bitwise matvec(A, H[:, j])."""
         self._check(self.lib.alnnls_matmat_device(self.ctx, rows, inner, cols, C.c_void_p(A_ptr),

@@ -43,7 +43,8 @@ struct alnnls_ctx {
   DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
   DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
       hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb, uP, gdC, skp, skf,
-      ay, axn, aw, avy, apc, tst, fgb0, fgb1, fpart, fden, fkl, fkv, fkc, dmws, dmfl;
+      ay, axn, aw, avy, apc, tst, fgb0, fgb1, fpart, fden, fkl, fkv, fkc, dmws, dmfl, nvt,
+      nht, nwt, nv, nw, nh;
 
   // last solve
   bool last_nnls = false;
@@ -813,7 +814,8 @@ void alnnls_destroy(alnnls_ctx* ctx) {
                     &ctx->skp,    &ctx->skf,   &ctx->ay,      &ctx->axn,   &ctx->aw,
                     &ctx->avy,    &ctx->apc,   &ctx->tst,   &ctx->fgb0,  &ctx->fgb1,
                     &ctx->fpart,  &ctx->fden,  &ctx->fkl,   &ctx->fkv,   &ctx->fkc,
-                    &ctx->dmws,   &ctx->dmfl};
+                    &ctx->dmws,   &ctx->dmfl,  &ctx->nvt,   &ctx->nht,   &ctx->nwt,
+                    &ctx->nv,     &ctx->nw,    &ctx->nh};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
@@ -1741,6 +1743,70 @@ int alnnls_solve_nnls_batched_multi(alnnls_ctx* const* ctxs, int nctx, uint64_t 
   }
   if (out) *out = tot;
   return ALNNLS_OK;
+}
+
+// ---- NMF by alternating NNLS -------------------------------------------------------------
+
+int alnnls_nmf_device(alnnls_ctx* ctx, uint64_t d, uint64_t N, uint64_t k, const double* dV,
+                      double* dW, double* dH, uint64_t outer_iters, const alnnls_config* cfg,
+                      double* objective) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!cfg || !dV || !dW || !dH) return set_err(ctx, ALNNLS_EINVAL, "nmf: null argument");
+  if (d < 1 || N < 1 || k < 1) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  if (k > 1024) return set_err(ctx, ALNNLS_EINVAL, "nmf: k > 1024 not supported (batched solver bound)");
+  int st__ = ALNNLS_OK;
+  cudaStream_t s = ctx->stream;
+  {  // inputs: finite V, finite nonnegative start W (linalg.hpp:84, like solve_nqp's start)
+    int* flag = ENSURE(int, flag, 4);
+    CK(cudaMemsetAsync(flag, 0, sizeof(int) * 3, s));
+    CK(launch_check_finite(dV, d, N, d, flag, s));
+    CK(launch_check_finite(dW, d, k, d, flag + 1, s));
+    CK(launch_check_matrix(dW, d, k, d, 1, flag + 2, s));
+    int hf[3] = {0, 0, 0};
+    if ((rc = copy_out(ctx, hf, flag, sizeof(hf)))) return rc;
+    if (hf[0] || hf[1]) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
+    if (hf[2]) return set_err(ctx, ALNNLS_EINVAL, "nmf: W must be nonnegative");
+  }
+  double* VT = ENSURE(double, nvt, N * d);  // V^T (N x d)
+  double* HT = ENSURE(double, nht, N * k);  // H^T (N x k)
+  double* WT = ENSURE(double, nwt, k * d);  // W^T (k x d)
+  CK(launch_transpose(dV, d, (int)d, (int)N, VT, N, s));
+  std::vector<alnnls_column_result> colsH(N), colsW(d);
+  for (uint64_t t = 0; t < outer_iters; ++t) {
+    // H <- argmin ||W H - V||: columns of V against A = W
+    alnnls_summary sum{};
+    if ((rc = run_batched(ctx, d, k, dW, d, N, dV, d, cfg, dH, colsH.data(), &sum))) return rc;
+    if (objective) {
+      double obj = 0.0;
+      for (uint64_t j = 0; j < N; ++j) obj += colsH[j].residual_sq;
+      objective[t] = obj;
+    }
+    // W <- argmin ||H^T W^T - V^T||: columns of V^T against A = H^T
+    CK(launch_transpose(dH, k, (int)k, (int)N, HT, N, s));
+    if ((rc = run_batched(ctx, N, k, HT, N, d, VT, N, cfg, WT, colsW.data(), &sum))) return rc;
+    CK(launch_transpose(WT, k, (int)k, (int)d, dW, d, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  return ALNNLS_OK;
+}
+
+int alnnls_nmf(alnnls_ctx* ctx, uint64_t d, uint64_t N, uint64_t k, const double* V, double* W,
+               double* H, uint64_t outer_iters, const alnnls_config* cfg, double* objective) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!cfg || !V || !W || !H) return set_err(ctx, ALNNLS_EINVAL, "nmf: null argument");
+  if (d < 1 || N < 1 || k < 1) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: rows and cols must be >= 1");
+  int st__ = ALNNLS_OK;
+  cudaStream_t s = ctx->stream;
+  double* dV = ENSURE(double, nv, d * N);
+  double* dW = ENSURE(double, nw, d * k);
+  double* dH = ENSURE(double, nh, k * N);
+  CK(cudaMemcpyAsync(dV, V, sizeof(double) * d * N, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dW, W, sizeof(double) * d * k, cudaMemcpyHostToDevice, s));
+  if ((rc = alnnls_nmf_device(ctx, d, N, k, dV, dW, dH, outer_iters, cfg, objective))) return rc;
+  if ((rc = copy_out(ctx, W, dW, sizeof(double) * d * k))) return rc;
+  return copy_out(ctx, H, dH, sizeof(double) * k * N);
 }
 
 }  // extern "C"

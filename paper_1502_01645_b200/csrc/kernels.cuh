@@ -245,6 +245,9 @@ cudaError_t launch_pack_upper(double* H, uint64_t n, double* P, int dir, cudaStr
 // matvec order (bitwise matvec(A, H[:, j]))
 cudaError_t launch_matmat(const double* A, uint64_t lda, int rows, int inner, const double* H,
                           uint64_t ldh, int cols, double* C, uint64_t ldc, cudaStream_t stream);
+// dst (cols x rows) = src^T (rows x cols), column-major both
+cudaError_t launch_transpose(const double* src, uint64_t ld_src, int rows, int cols, double* dst,
+                             uint64_t ld_dst, cudaStream_t stream);
 // pads: copy a rows x cols col-major block into a buffer with leading dimension ld_dst.
 cudaError_t launch_copy_pad(const double* src, uint64_t ld_src, double* dst, uint64_t ld_dst,
                             uint64_t rows, uint64_t cols, cudaStream_t stream);

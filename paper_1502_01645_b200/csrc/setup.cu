@@ -583,6 +583,23 @@ __global__ void matmat_kernel(const double* __restrict__ A, uint64_t lda, int ro
   C[j * ldc + i] = s;
 }
 
+// dst (cols x rows, ld_dst) = src^T (src rows x cols, ld_src), 32 x 32 tiles through
+// shared memory (both sides coalesced). Pure data movement: no arithmetic.
+__global__ void transpose_kernel(const double* __restrict__ src, uint64_t ld_src, int rows,
+                                 int cols, double* __restrict__ dst, uint64_t ld_dst) {
+  __shared__ double tile[32][33];
+  const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = r0 + threadIdx.x, c = c0 + k;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = src[(uint64_t)c * ld_src + r];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = c0 + threadIdx.x, r = r0 + k;  // dst column r, row c
+    if (r < rows && c < cols) dst[(uint64_t)r * ld_dst + c] = tile[threadIdx.x][k];
+  }
+}
+
 __global__ void copy_pad_kernel(const double* src, uint64_t ld_src, double* dst, uint64_t ld_dst,
                                 uint64_t rows, uint64_t cols) {
   const uint64_t total = rows * cols;
@@ -789,6 +806,19 @@ cudaError_t launch_matmat(const double* A, uint64_t lda, int rows, int inner, co
     const int nc = cols - j0 < 65535 ? cols - j0 : 65535;
     matmat_kernel<<<dim3((rows + 255) / 256, nc), 256, 0, stream>>>(
         A, lda, rows, inner, H + (uint64_t)j0 * ldh, ldh, C + (uint64_t)j0 * ldc, ldc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_transpose(const double* src, uint64_t ld_src, int rows, int cols, double* dst,
+                             uint64_t ld_dst, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  for (int c0 = 0; c0 < cols; c0 += 32 * 65535) {  // gridDim.y limit
+    const int nc = cols - c0 < 32 * 65535 ? cols - c0 : 32 * 65535;
+    transpose_kernel<<<dim3((rows + 31) / 32, (nc + 31) / 32), dim3(32, 8), 0, stream>>>(
+        src + (uint64_t)c0 * ld_src, ld_src, rows, nc, dst + c0, ld_dst);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -65,6 +65,27 @@ NqpProblem lopsided() { return NqpProblem(DenseMatrix(2, 2, {1.0, 0.1, 0.1, 9.0}
 }  // namespace
 
 int main() {
+  run("NMF by alternating NNLS (nmf)", [] {
+    const std::size_t d = 120, n = 90, k = 4;
+    std::uint64_t st = 0x9E3779B97F4A7C15ull;
+    auto u01 = [&] { st ^= st << 13; st ^= st >> 7; st ^= st << 17; return (st >> 11) * 0x1.0p-53; };
+    std::vector<double> wt(d * k), ht(k * n), w0(d * k), vv(d * n, 0.0);
+    for (auto& x : wt) x = u01();
+    for (auto& x : ht) x = u01();
+    for (auto& x : w0) x = u01();
+    for (std::size_t j = 0; j < n; ++j)
+      for (std::size_t t = 0; t < k; ++t)
+        for (std::size_t i = 0; i < d; ++i) vv[j * d + i] += wt[t * d + i] * ht[j * k + t];
+    SolverConfig cfg;
+    cfg.epsilon = 1e-10;
+    cfg.stall_window = 1000000000;
+    const auto r = nmf(DenseMatrix(d, n, vv), DenseMatrix(d, k, w0), 20, cfg);
+    REQUIRE(r.W.rows() == d && r.W.cols() == k && r.H.rows() == k && r.H.cols() == n);
+    REQUIRE(r.objective.size() == 20 && r.objective.back() < 1e-2 * r.objective.front());
+    for (std::size_t t = 1; t < r.objective.size(); ++t)
+      REQUIRE(r.objective[t] <= r.objective[t - 1] * (1 + 1e-9) + 1e-12);
+    REQUIRE(throws<std::invalid_argument>([&] { nmf(DenseMatrix(d, n, vv), DenseMatrix(d + 1, k), 1, cfg); }));
+  });
   run("batched multi-RHS (solve_nnls_batched, num_gpus)", [] {
     const std::size_t d = 400, n = 60, k = 9;
     std::vector<double> av(d * n), bv(d * k);
