@@ -26,6 +26,7 @@
 #include <string_view>
 #include <vector>
 
+#include "antilop/io.hpp"  // as the reference's nqp.hpp:23: fmt_g17 and the file I/O
 #include "antilop/linalg.hpp"
 
 namespace antilop {
@@ -254,11 +255,6 @@ inline SolveResult solve_nqp(const NqpProblem& p, const SolverConfig& config = {
 
 // ---- trace serialization (nqp.hpp:345-357): %.17g, alpha blank on the final record
 namespace detail {
-inline std::string g17(double v) {
-  char buf[64];
-  std::snprintf(buf, sizeof(buf), "%.17g", v);
-  return buf;
-}
 
 // A double the way the reference's nlohmann::json dump() writes it (nnls.hpp:146-153
 // serializes through it). With nlohmann/json on the include path (the reference's own
@@ -304,15 +300,14 @@ inline std::string json_number(double v) {
 inline void write_trace_csv(std::ostream& os, const SolveTrace& trace) {
   os << "iter,elapsed_ms,f,grad_bar_sq,passive_count,alpha\n";
   for (const auto& r : trace) {
-    os << r.iter << ',' << detail::g17(r.elapsed.count() * 1e3) << ',' << detail::g17(r.f) << ','
-       << detail::g17(r.grad_bar_sq) << ',' << r.passive_count << ','
-       << (r.alpha ? detail::g17(*r.alpha) : std::string()) << '\n';
+    os << r.iter << ',' << fmt_g17(r.elapsed.count() * 1e3) << ',' << fmt_g17(r.f) << ','
+       << fmt_g17(r.grad_bar_sq) << ',' << r.passive_count << ','
+       << (r.alpha ? fmt_g17(*r.alpha) : std::string()) << '\n';
   }
 }
 
 inline void write_trace_csv_file(const std::filesystem::path& path, const SolveTrace& trace) {
-  std::ofstream f(path);
-  if (!f) throw std::runtime_error("cannot open " + path.string());
+  auto f = detail::open_out(path);
   write_trace_csv(f, trace);
 }
 

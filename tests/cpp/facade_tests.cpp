@@ -4,6 +4,7 @@
 // reference exposes; every hot-path call runs on the GPU through the C ABI.
 // Needs a GPU: run by tests/test_facade_cpp.py (pytest -m gpu).
 #include <cmath>
+#include <filesystem>
 #include <cstdio>
 #include <functional>
 #include <limits>
@@ -65,6 +66,41 @@ NqpProblem lopsided() { return NqpProblem(DenseMatrix(2, 2, {1.0, 0.1, 0.1, 9.0}
 }  // namespace
 
 int main() {
+  run("io: MatrixMarket / CSV round trips and errors", [] {  // test_io.cpp cases
+    const DenseMatrix m = DenseMatrix::from_rows({{1.0, -2.5}, {1.0 / 3.0, 4e-300}, {7.0, 8.0}});
+    std::stringstream ss;
+    write_matrix_market(ss, m);
+    const DenseMatrix back = read_matrix_market(ss);
+    REQUIRE(back.rows() == 3 && back.cols() == 2);
+    for (std::size_t j = 0; j < 2; ++j)
+      for (std::size_t i = 0; i < 3; ++i) REQUIRE(back(i, j) == m(i, j));
+    std::stringstream vs;
+    write_matrix_market(vs, Vector{0.1, 0.2});
+    const Vector vb = read_matrix_market_vector(vs);
+    REQUIRE(vb.size() == 2 && vb[0] == 0.1 && vb[1] == 0.2);
+    std::istringstream comment("%%MatrixMarket matrix array real general\n% note\n\n2 1\n1.5\n-2\n");
+    const DenseMatrix c = read_matrix_market(comment);
+    REQUIRE(c(0, 0) == 1.5 && c(1, 0) == -2.0);
+    for (const char* bad : {"", "%%MatrixMarket matrix coordinate real general\n1 1\n1\n",
+                            "hello\n1 1\n1\n", "%%MatrixMarket matrix array real general\n2 2\n1\n2\n",
+                            "%%MatrixMarket matrix array real general\n1 1\nx\n"}) {
+      std::istringstream is(bad);
+      REQUIRE(throws<std::runtime_error>([&] { read_matrix_market(is); }));
+    }
+    std::stringstream cs;
+    write_csv(cs, m);
+    const DenseMatrix cb = read_csv_matrix(cs);
+    REQUIRE(cb.rows() == 3 && cb.cols() == 2 && cb(1, 0) == 1.0 / 3.0);
+    std::istringstream ragged("1,2\n3\n");
+    REQUIRE(throws<std::runtime_error>([&] { read_csv_matrix(ragged); }));
+    REQUIRE(fmt_g17(0.1) == "0.10000000000000001");
+    const auto dir = std::filesystem::temp_directory_path();
+    save_matrix(dir / "antilop_io_test.mtx", m);
+    save_vector(dir / "antilop_io_test.csv", Vector{1.0, 2.0});
+    REQUIRE(load_matrix(dir / "antilop_io_test.mtx")(2, 1) == 8.0);
+    REQUIRE(load_vector(dir / "antilop_io_test.csv")[1] == 2.0);
+    REQUIRE(throws<std::runtime_error>([&] { load_matrix(dir / "antilop_no_such_file.mtx"); }));
+  });
   run("NMF by alternating NNLS (nmf)", [] {
     const std::size_t d = 120, n = 90, k = 4;
     std::uint64_t st = 0x9E3779B97F4A7C15ull;

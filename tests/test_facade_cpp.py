@@ -94,3 +94,26 @@ int main() {
         assert bad < total // 100, r.stdout
     else:
         assert bad == 0, r.stdout
+
+
+def test_cpp_facade_io_visible_from_nqp(tmp_path):
+    """As in the reference (nqp.hpp:23 includes io.hpp), including the facade's
+    nqp.hpp makes fmt_g17 and the MatrixMarket / CSV I/O visible; they run on the
+    host (no GPU needed)."""
+    src = tmp_path / "io.cpp"
+    src.write_text('''#include <sstream>
+#include "antilop/nqp.hpp"
+int main() {
+  using namespace antilop;
+  const DenseMatrix m = DenseMatrix::from_rows({{1.0, 2.0}, {3.0, 0.1}});
+  std::stringstream ss;
+  write_matrix_market(ss, m);
+  const DenseMatrix b = read_matrix_market(ss);
+  if (!(b(1, 1) == 0.1 && b(1, 0) == 3.0)) return 1;
+  return fmt_g17(0.1) == "0.10000000000000001" ? 0 : 2;
+}''')
+    exe = tmp_path / "io"
+    subprocess.run(["g++", "-std=c++20", "-I", os.path.join(ROOT, "include"), "-o", str(exe),
+                    str(src), "-L", os.path.join(ROOT, "paper_1502_01645_b200", "lib"), "-lalnnls",
+                    "-Wl,-rpath," + os.path.join(ROOT, "paper_1502_01645_b200", "lib")], check=True)
+    assert subprocess.run([str(exe)]).returncode == 0
