@@ -156,6 +156,12 @@ def dist_setup(args):
     if args.impl == "ours" and (ws > 1 or os.environ.get("ALNNLS_FORCE_ROWBLOCK")):
         import torch.distributed as dist  # noqa
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if "RANK" not in os.environ:  # a one-rank group outside torchrun (the N=1 pipeline)
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                os.environ.setdefault("MASTER_PORT", str(sk.getsockname()[1]))
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
         import torch
         torch.cuda.set_device(local)
         dist.init_process_group(backend="nccl")

@@ -38,7 +38,12 @@ namespace alnnls {
 #define ALNNLS_MIN_STAGES 6
 #endif
 
-constexpr int kRingCols = 64;   // columns per stage
+#ifndef ALNNLS_RING_COLS
+#define ALNNLS_RING_COLS 128  // build knob: widest stage (columns); 128 halves the per-column
+                             // share of the stage wait, chained as two 64-column halves
+                             // (c2 87.0 -> 83.8, c3 101.1 -> 96.0 us/iteration vs 64)
+#endif
+constexpr int kRingCols = ALNNLS_RING_COLS;   // columns per stage
 constexpr int kMaxStages = 48;
 #ifndef ALNNLS_RING_KB
 #define ALNNLS_RING_KB 208  // build knob (c5: 7 instead of 6 32-column stages, 503 -> 497 us/iteration)
@@ -227,7 +232,16 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
       // them: ptxas cannot interleave the chain ahead of the loads, so the
       // 8-cycle DADD latency is the only per-column cost (measured ~2.3x
       // faster than a fused mul/add loop on B200).
-      if (cnt == 64 && G == 64) {
+      if (cnt == 128 && G == 128) {
+#pragma unroll 1
+        for (int h = 0; h < 128; h += 64) {
+          double p[64];
+#pragma unroll
+          for (int l = 0; l < 64; ++l) p[l] = xmul(col[(h + l) * seg + tt], v[h + l]);
+#pragma unroll
+          for (int l = 0; l < 64; ++l) acc = xadd(acc, p[l]);
+        }
+      } else if (cnt == 64 && G == 64) {
         double p[64];
 #pragma unroll
         for (int l = 0; l < 64; ++l) p[l] = xmul(col[l * seg + tt], v[l]);
