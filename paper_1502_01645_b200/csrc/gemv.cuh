@@ -38,6 +38,10 @@ namespace alnnls {
 #define ALNNLS_MIN_STAGES 6
 #endif
 
+#ifndef ALNNLS_RPW_MIN
+#define ALNNLS_RPW_MIN 32  // build knob: fewest rows per consumer warp (8, 16 or 32);
+                          // 8 measured slower (c2 89.5 vs 83.9 us/iteration), 16 equal
+#endif
 #ifndef ALNNLS_RING_COLS
 #define ALNNLS_RING_COLS 128  // build knob: widest stage (columns); 128 halves the per-column
                              // share of the stage wait, chained as two 64-column halves
@@ -60,6 +64,7 @@ struct RowRing {
   int seg;        // doubles per column slot
   int P;          // producer warps: warps [0, P)
   int cons_warps; // consumer warps: warps [P, P + cons_warps)
+  int rpw;        // rows per consumer warp (lanes [0, rpw) own rows)
   uint32_t pos;   // stages issued so far (identical in every thread)
   uint32_t smask; // S - 1 when S is a power of two (ALNNLS_POW2_STAGES), else 0
   uint32_t sshift;
@@ -92,7 +97,17 @@ __host__ __device__ inline size_t ring_stage_bytes(int seg, int G) {
 __device__ inline void ring_setup(RowRing& r, uint8_t* smem, size_t bytes, int nrows, int seg,
                                   int max_warps) {
   r.seg = seg;
-  r.cons_warps = max(1, (nrows + 31) / 32);
+  // Rows per consumer warp: the smallest of ALNNLS_RPW_MIN, 16, 32 that fits the
+  // warps left beside the producers. Fewer rows per warp = more warps running
+  // their (latency-bound) DADD chains concurrently: while one warp waits on its
+  // chain, another forms its products (c2, 28 rows: 4 warps of 8 rows).
+  {
+    const int avail = max(1, max_warps - min(ALNNLS_PRODUCERS, 4));
+    int rpw = ALNNLS_RPW_MIN;
+    while (rpw < 32 && (nrows + rpw - 1) / rpw > avail) rpw *= 2;
+    r.rpw = rpw;
+  }
+  r.cons_warps = max(1, (nrows + r.rpw - 1) / r.rpw);
   const size_t hdr = (size_t)kMaxStages * 16;
   int G = kRingCols;
   while (G > 8 && (bytes - hdr) / ring_stage_bytes(seg, G) < ALNNLS_MIN_STAGES) G >>= 1;
@@ -196,8 +211,9 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
                  (uint32_t)(((cnt + 1) & ~1) * 8), &r.full[st]);
     }
   } else if (warp < r.P + r.cons_warps) {
-    const int t = (warp - r.P) * 32 + lane;
-    const int tt = t < nrows ? t : 0;
+    const int t = (warp - r.P) * r.rpw + lane;
+    const bool mine = lane < r.rpw && t < nrows;
+    const int tt = mine ? t : 0;
     double acc = 0.0, acc2 = 0.0;
     for (int s = 0; s < nst; ++s) {
       const uint32_t p = r.pos + s;
@@ -265,7 +281,7 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[st]);
     }
-    if (t < nrows) {
+    if (mine) {
       out[row0 + t] = acc;
       if (opos && opos[t] >= 0) out_c[opos[t]] = acc;
       if (out2) out2[row0 + t] = acc2;
