@@ -252,12 +252,15 @@ __device__ __forceinline__ void tile_coords(int mode, int t, int nti, int& ti, i
 __global__ void __launch_bounds__(TT, 1)
     syrk_tma_kernel(const __grid_constant__ TmaArgs ta, SetupArgs s, int mode) {
   extern __shared__ uint8_t dm2_raw[];
-  double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(dm2_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (the 128B swizzle atom), by offsetting the shared array itself so
+  // the compiler keeps the shared state space (LDS, not generic loads)
+  double* sm = reinterpret_cast<double*>(dm2_raw + ((1024u - (smem_u32(dm2_raw) & 1023u)) & 1023u));
   __shared__ __align__(8) uint64_t full[kStages2];
   __shared__ __align__(8) uint64_t empty[kStages2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;
   const int g = lane >> 2, t = lane & 3;
+  const int sg = (g >> 1) | ((g & 1) << 2);  // slab row of fragment row g (see the loads)
   const long long U = (long long)ta.tiles * ta.nk;
   const int G = gridDim.x, c = blockIdx.x;
   const long long u0 = U * c / G, u1 = U * (c + 1) / G;
@@ -305,22 +308,32 @@ __global__ void __launch_bounds__(TT, 1)
       mbar_wait(&full[st], (uint32_t)((q / kStages2) & 1));
       const double* as = slabA(st);
       const double* bs = slabB(st);
+      // Fragment loads, conflict-free 128-bit: the k8 step's positions (t, t + 4) take
+      // k = ks + 2t and ks + 2t + 1 (adjacent: one LDS.128 per row), and fragment row
+      // g reads slab row sg = (g >> 1) | ((g & 1) << 2) of its 8-row group, so the 8
+      // lanes of each quarter-warp land on 8 distinct 16-byte chunks of the 128B
+      // swizzle (the natural mapping put two lanes on each chunk: 2x wavefronts,
+      // 207.6 M bank conflicts per c2 Gram). The epilogue undoes the row map.
 #pragma unroll
       for (int ks = 0; ks < TK; ks += 8) {
         double af[4][4], bf[4][2];
+        const int kk = ks + 2 * t;
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
-          const int r = wm * 64 + mi * 16 + g;
-          af[mi][0] = as[swz128(r, ks + t)];
-          af[mi][1] = as[swz128(r + 8, ks + t)];
-          af[mi][2] = as[swz128(r, ks + t + 4)];
-          af[mi][3] = as[swz128(r + 8, ks + t + 4)];
+          const int r = wm * 64 + mi * 16 + sg;
+          const double2 lo = *reinterpret_cast<const double2*>(as + swz128(r, kk));
+          const double2 hi = *reinterpret_cast<const double2*>(as + swz128(r + 8, kk));
+          af[mi][0] = lo.x;
+          af[mi][2] = lo.y;
+          af[mi][1] = hi.x;
+          af[mi][3] = hi.y;
         }
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) {
-          const int r = wn * 32 + ni * 8 + g;
-          bf[ni][0] = bs[swz128(r, ks + t)];
-          bf[ni][1] = bs[swz128(r, ks + t + 4)];
+          const int r = wn * 32 + ni * 8 + sg;
+          const double2 v = *reinterpret_cast<const double2*>(bs + swz128(r, kk));
+          bf[ni][0] = v.x;
+          bf[ni][1] = v.y;
         }
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
@@ -339,8 +352,9 @@ __global__ void __launch_bounds__(TT, 1)
       for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int il = wm * 64 + mi * 16 + g + (e >> 1) * 8;
-          const int jl = wn * 32 + ni * 8 + 2 * t + (e & 1);
+          const int cn = 2 * t + (e & 1);  // fragment column -> B slab row
+          const int il = wm * 64 + mi * 16 + sg + (e >> 1) * 8;
+          const int jl = wn * 32 + ni * 8 + ((cn >> 1) | ((cn & 1) << 2));
           tile_s[jl * TB + il] = acc[mi][ni][e];
         }
     __syncthreads();
