@@ -95,14 +95,35 @@ struct Barrier {
   }
 };
 
-// 128-bit streaming load of two doubles of Q (read-only for the whole kernel;
-// no L1 allocation, Q is streamed once per pass).
-__device__ __forceinline__ double2 ldq2(const double* p) {
+// 128-bit load of two doubles of Q (read-only for the whole kernel; no L1
+// allocation) with an L2 cache policy: a fixed fraction of Q's lines is marked
+// evict_last and the rest evict_first, so that part of Q stays resident in the
+// 126 MB L2 from one iteration's pass to the next (Q at c2 is 134 MB).
+template <bool kL2>
+__device__ __forceinline__ double2 ldq2(const double* p, uint64_t pol) {
   double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-               : "=d"(v.x), "=d"(v.y)
-               : "l"(p));
+  if constexpr (kL2) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(pol));
+  } else {  // plain streaming load (the hinted form measured 15% slower when Q >> L2, c5)
+    (void)pol;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p));
+  }
   return v;
+}
+__device__ __forceinline__ uint64_t l2_policy(float frac) {
+  uint64_t pol;
+  if (frac > 0.f)
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;"
+                 : "=l"(pol) : "f"(frac));
+  else if (frac < 0.f)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 
 // Thread (rp, c) accumulates rows (2rp, 2rp+1) over columns j = c, c+C, ... of
@@ -111,9 +132,10 @@ __device__ __forceinline__ double2 ldq2(const double* p) {
 // the panel with coefficients w[j] (skipping w[j] == 0: no load). (A running-
 // pointer form of this loop measured 2.6x slower at 512 threads: the 128-register
 // budget then rematerializes the panel base per load.)
+template <bool kL2>
 __device__ __forceinline__ void panel_pass(const double* __restrict__ Qp, int R, int m,
                                            const double* __restrict__ w, int c, int C, int r2,
-                                           double& acc0, double& acc1) {
+                                           double& acc0, double& acc1, uint64_t pol) {
   constexpr int U = ALNNLS_FAST_UNROLL;
   const double* base = Qp + r2;
   int j = c;
@@ -124,7 +146,7 @@ __device__ __forceinline__ void panel_pass(const double* __restrict__ Qp, int R,
     for (int u = 0; u < U; ++u) gv[u] = w[j + u * C];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      qv[u] = gv[u] != 0.0 ? ldq2(base + (size_t)(j + u * C) * R) : make_double2(0.0, 0.0);
+      qv[u] = gv[u] != 0.0 ? ldq2<kL2>(base + (size_t)(j + u * C) * R, pol) : make_double2(0.0, 0.0);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       acc0 = fma(qv[u].x, gv[u], acc0);
@@ -134,7 +156,7 @@ __device__ __forceinline__ void panel_pass(const double* __restrict__ Qp, int R,
   for (; j < m; j += C) {
     const double gv = w[j];
     if (gv != 0.0) {
-      const double2 qv = ldq2(base + (size_t)j * R);
+      const double2 qv = ldq2<kL2>(base + (size_t)j * R, pol);
       acc0 = fma(qv.x, gv, acc0);
       acc1 = fma(qv.y, gv, acc1);
     }
@@ -142,10 +164,11 @@ __device__ __forceinline__ void panel_pass(const double* __restrict__ Qp, int R,
 }
 
 // Thread (rp, c) over a staged list of (column, coefficient) pairs, t = c, c+C, ...
+template <bool kL2>
 __device__ __forceinline__ void list_pass(const double* __restrict__ Qp, int R,
                                           const uint32_t* __restrict__ kj,
                                           const double* __restrict__ kv, int len, int c, int C,
-                                          int r2, double& acc0, double& acc1) {
+                                          int r2, double& acc0, double& acc1, uint64_t pol) {
   constexpr int U = 4;  // independent loads in flight per thread
   const double* base = Qp + r2;
   for (int t = c; t < len; t += U * C) {
@@ -155,7 +178,7 @@ __device__ __forceinline__ void list_pass(const double* __restrict__ Qp, int R,
     for (int u = 0; u < U; ++u) {
       const int tt = t + u * C;
       cv[u] = tt < len ? kv[tt] : 0.0;
-      qv[u] = tt < len ? ldq2(base + (size_t)kj[tt] * R) : make_double2(0.0, 0.0);
+      qv[u] = tt < len ? ldq2<kL2>(base + (size_t)kj[tt] * R, pol) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -368,7 +391,7 @@ __device__ void fast_record(const FastArgs& a, unsigned long long& idx, unsigned
   ++idx;
 }
 
-template <bool kCluster>
+template <bool kCluster, bool kL2>
 __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
   Barrier<kCluster> bar;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -395,6 +418,7 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
   const int i = row0 + threadIdx.x;
   const bool lead = b == 0 && threadIdx.x == 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t pol = l2_policy(a.l2_frac);
   const uint64_t t0 = globaltimer_ns();
 
   // ---- this thread's row of the current state --------------------------------------
@@ -522,7 +546,7 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
 
     // ===== u = Q gbar over own rows (one streaming pass over the passive columns) =====
     double acc0 = 0.0, acc1 = 0.0;
-    if (gthr) panel_pass(Qp, R, m, gs, grp, C, r2, acc0, acc1);
+    if (gthr) panel_pass<kL2>(Qp, R, m, gs, grp, C, r2, acc0, acc1, pol);
     const double ui = rows_from_groups(red, rsum, gthr, grp, R, r2, acc0, acc1, C, nrows);
     {
       const double dn = block_sum(own ? gs[i] * ui : 0.0, S);
@@ -599,7 +623,7 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
           }
           __syncthreads();
           if (gthr) {
-            list_pass(Qp, R, kjs, kvs, min(kKWin, ktot - w0), grp, C, r2, v0, v1);
+            list_pass<kL2>(Qp, R, kjs, kvs, min(kKWin, ktot - w0), grp, C, r2, v0, v1, pol);
           }
           __syncthreads();
         }
@@ -651,7 +675,7 @@ __global__ void __launch_bounds__(kFT, 1) fast_loop_kernel(FastArgs a) {
           }
           __syncthreads();
           if (gthr) {
-            list_pass(Qp, R, kjs, kvs, wn, grp, C, r2, v0, v1);
+            list_pass<kL2>(Qp, R, kjs, kvs, wn, grp, C, r2, v0, v1, pol);
           }
           __syncthreads();
         }
@@ -736,9 +760,9 @@ size_t fast_static_smem() {
   static size_t v = [] {
     cudaFuncAttributes fa{};
     size_t mx = sizeof(FastShared) + 256;
-    if (cudaFuncGetAttributes(&fa, fast_loop_kernel<false>) == cudaSuccess && fa.sharedSizeBytes > mx)
+    if (cudaFuncGetAttributes(&fa, fast_loop_kernel<false, false>) == cudaSuccess && fa.sharedSizeBytes > mx)
       mx = fa.sharedSizeBytes;
-    if (cudaFuncGetAttributes(&fa, fast_loop_kernel<true>) == cudaSuccess && fa.sharedSizeBytes > mx)
+    if (cudaFuncGetAttributes(&fa, fast_loop_kernel<true, false>) == cudaSuccess && fa.sharedSizeBytes > mx)
       mx = fa.sharedSizeBytes;
     (void)cudaGetLastError();
     return mx;
@@ -755,21 +779,39 @@ bool fast_loop_supported(int m, int R) {
   return fast_smem_bytes(m, false) + fast_static_smem() <= kFastSmemCap;
 }
 
+template <bool kL2>
+cudaError_t launch_fast_loop_t(const FastArgs& a0, cudaStream_t stream);
+
 cudaError_t launch_fast_loop(const FastArgs& a0, cudaStream_t stream) {
+  // L2 residency hints only when a sizable fraction of Q fits the L2 (c2 / c3: 0.7);
+  // env ALNNLS_FAST_L2_FRAC overrides (A/B)
+  const double qbytes = 8.0 * (double)a0.m * (double)a0.m;
+  double f = 94e6 / qbytes;
+  if (f > 1.0) f = 1.0;
+  if (const char* e = getenv("ALNNLS_FAST_L2_FRAC")) f = atof(e);
+  FastArgs a = a0;
+  a.l2_frac = (float)f;
+  return f >= 0.3 || f < 0.0 ? launch_fast_loop_t<true>(a, stream)
+                              : launch_fast_loop_t<false>(a, stream);
+}
+
+template <bool kL2>
+cudaError_t launch_fast_loop_t(const FastArgs& a0, cudaStream_t stream) {
   if (!fast_loop_supported(a0.m, a0.R)) return cudaErrorInvalidValue;
   FastArgs args = a0;
   // x staged beside gbar when both fit: the clamped set is then found by every CTA
   // from shared memory, without the extra barrier (m up to ~13k)
   args.local_k = fast_smem_bytes(args.m, true) + fast_static_smem() <= kFastSmemCap ? 1 : 0;
   if (getenv("ALNNLS_FAST_FORCE_A2")) args.local_k = 0;  // test hook: the large-m path
+
   const int nblk = (args.m + args.R - 1) / args.R;
   const size_t smem = fast_smem_bytes(args.m, args.local_k != 0);
   // opt in once for the largest staging any m can need (the size varies with m)
   const int smax = (int)(kFastSmemCap - fast_static_smem());
-  if (cudaError_t e = smem_optin(fast_loop_kernel<false>, smax)) return e;
-  if (cudaError_t e = smem_optin(fast_loop_kernel<true>, smax)) return e;
+  if (cudaError_t e = smem_optin(fast_loop_kernel<false, kL2>, smax)) return e;
+  if (cudaError_t e = smem_optin(fast_loop_kernel<true, kL2>, smax)) return e;
   const bool cluster_ok =
-      func_attr_once(reinterpret_cast<const void*>(fast_loop_kernel<true>),
+      func_attr_once(reinterpret_cast<const void*>(fast_loop_kernel<true, kL2>),
                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
   (void)cudaGetLastError();
   if (cluster_ok && nblk <= 16) {
@@ -786,9 +828,9 @@ cudaError_t launch_fast_loop(const FastArgs& a0, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, fast_loop_kernel<true>, &cfg);
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, fast_loop_kernel<true, kL2>, &cfg);
     if (e == cudaSuccess && nclusters > 0) {
-      e = cudaLaunchKernelEx(&cfg, fast_loop_kernel<true>, args);
+      e = cudaLaunchKernelEx(&cfg, fast_loop_kernel<true, kL2>, args);
       if (e == cudaSuccess) return e;
     }
     if (getenv("ALNNLS_DEBUG"))
@@ -797,7 +839,7 @@ cudaError_t launch_fast_loop(const FastArgs& a0, cudaStream_t stream) {
     (void)cudaGetLastError();  // no cluster of this size fits: cooperative grid instead
   }
   void* params[] = {&args};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)fast_loop_kernel<false>, dim3(nblk), dim3(kFT),
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)fast_loop_kernel<false, kL2>, dim3(nblk), dim3(kFT),
                                               params, smem, stream);
   if (e != cudaSuccess && getenv("ALNNLS_DEBUG"))
     fprintf(stderr, "fast_loop: cooperative %d x %d smem %zu: %s\n", nblk, kFT, smem,

@@ -118,6 +118,7 @@ struct FastArgs {
   double* kv;       // [nblk * R] their coefficients alpha g - x
   int* kc;          // [nblk]
   int local_k;      // set by launch_fast_loop: x staged in shared memory too
+  float l2_frac;    // set by launch_fast_loop: fraction of Q's lines loaded L2 evict_last
   double eps;
   uint64_t max_iters;
   int has_time_cap;
