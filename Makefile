@@ -36,7 +36,7 @@ $(LIB)/libalnnls_gen.so: $(PKG)/csrc/instgen.c
 	@mkdir -p $(LIB)
 	$(CC) -O2 -std=c11 -fPIC -shared -ffp-contract=off -o $@ $< -lm -pthread
 
-oracle:
+oracle: lib gen
 	$(MAKE) -C oracle
 
 facade: build/tests/facade_tests

@@ -31,365 +31,454 @@ constexpr int kBT = 512;          // threads per batched CTA (one warp per colum
 constexpr int kMaxCols = 16;      // NB upper bound (columns per CTA)
 
 enum ColPhase { kIdle = 0, kNeedP1 = 1, kNeedP2 = 2 };
+// Work a column slot still has to do in the current pass (settle rounds).
+enum ColAct {
+  kActNone = 0,
+  kActCand = 1,    // candidate step + changed set with alpha (nqp.hpp:294-303)
+  kActAccept = 2,  // x[C] = cand, grad += gd (nqp.hpp:309-313), then the next stop test
+  kActMask = 3,    // stop test on the current state (nqp.hpp:250-275)
+  kActInit = 4,    // a fresh column: x = 0, grad = q (nqp.hpp:224-225), then its stop test
+  kActFinish = 5,  // write the column's result, then take the next column
+  kActGrab = 6     // take the next column from the queue
+};
 
 struct ColState {
+#ifdef ALNNLS_BATCH_PROF
+  long long pr[8];
+#endif
   int phase[kMaxCols];
+  int act[kMaxCols];
   int col[kMaxCols];
   unsigned long long k[kMaxCols];
   int tries[kMaxCols];
   int ml[kMaxCols];
+  int cnt[kMaxCols];   // per-column counts of the elementwise phase (passive / changed)
+  int bad[kMaxCols];   // non-finite gradient entry seen
+  int term[kMaxCols];  // termination of a finishing column (-1: NumericFailure)
   double alpha[kMaxCols];
   double f[kMaxCols], gbs[kMaxCols];
   double best[kMaxCols];
+  double res[kMaxCols][3];  // chain results
+  double part[kMaxCols][4][3];  // FAST: per-warp tree partials (<= 4 warps per column)
   unsigned long long since[kMaxCols];
   unsigned long long mults[kMaxCols];
 };
 
-// Shared-memory layout of one CTA (mp = m rounded up to 8):
+// Shared-memory layout of one CTA (mp = m rounded up to 16, ps = mp + 2):
 //  - V, the GEMM input, row-major mp x ld (ld = NB + 2): the GEMM reads a row of
 //    V with 16-byte broadcasts; the padding keeps the per-column writes (lane =
 //    row) at 4-way bank sharing; rows >= m stay zero so the GEMM needs no tail.
 //  - U (GEMM output), C (candidate), X (iterate), G (gradient), q (linear term):
-//    column panels of mp doubles, so the GEMM's stores and every per-column walk
-//    are conflict-free, and a lane can load 8 consecutive entries as 4 x 16 B.
+//    column panels of stride ps. The elementwise phases walk a column with
+//    consecutive lanes (conflict-free); the chain lanes (one per column) read
+//    the same offset of NB panels, which the +2 stride spreads over the banks.
+//  - chain terms: den / df terms go to V (dead once the pass has read it; the
+//    chain lanes read one V row, NB consecutive doubles); the stop-test terms
+//    x.g and q.x go to U and C (dead after the accepted update), and g_bar^2 is
+//    formed by the chain lane from V = g_bar.
 struct BatchSmem {
   double* V;
   int ld;
-  int m, mp;
+  int m, mp, ps;
   double* U;
   double* C;
   double* X;
   double* G;
   double* q;
   __device__ double& v(int i, int b) const { return V[i * ld + b]; }
-  __device__ double* u(int b) const { return U + b * mp; }
-  __device__ double* c(int b) const { return C + b * mp; }
-  __device__ double* x(int b) const { return X + b * mp; }
-  __device__ double* g(int b) const { return G + b * mp; }
-  __device__ double* qc(int b) const { return q + b * mp; }
+  __device__ double* u(int b) const { return U + b * ps; }
+  __device__ double* c(int b) const { return C + b * ps; }
+  __device__ double* x(int b) const { return X + b * ps; }
+  __device__ double* g(int b) const { return G + b * ps; }
+  __device__ double* qc(int b) const { return q + b * ps; }
 };
 
 __host__ __device__ constexpr int batch_ld(int nb) { return nb + 2; }
 __host__ __device__ constexpr int round8(int m) { return (m + 15) & ~15; }  // (16: GEMM blocks of up to 16 rows)
+__host__ __device__ constexpr int panel_stride(int m) { return round8(m) + 2; }
 size_t batch_smem_bytes(int m, int nb) {
   const size_t mp = (size_t)round8(m);
-  return (mp * batch_ld(nb) + 5 * mp * nb) * sizeof(double);
+  return (mp * batch_ld(nb) + 5 * (size_t)panel_stride(m) * nb) * sizeof(double);
 }
 
-// 8 consecutive doubles (16-byte aligned) from shared memory.
-__device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
-  const double2* w = reinterpret_cast<const double2*>(p);
+// Reference-ordered sums, one lane per column (the chain warp, lane b = column
+// b): s = ((0 + t_0) + t_1) + ... over the m rows. A term the reference skips
+// is a -0, which leaves every sum bit-identical (s + -0 = s, and a chain that
+// starts at +0 never becomes -0), so each lane runs pure dependent DADDs, and
+// one DADD instruction advances every column's chain (the FP64 pipe is not
+// spent on one useful lane per instruction). The three stop-test sums of a
+// column run on three lanes (warp 0 lanes b and 16 + b, warp 1 lane b).
+//   lane_sum: one sum of n terms p[t * stride] (squared first when sq: the
+//   g_bar^2 terms of gbs from V = g_bar). Two register blocks of 16 alternate,
+//   so the loads of the next block are in flight during the current block's
+//   chain and the dependent DADD is the per-term cost.
+// Term of a lane's sum: the value, or its square (g_bar^2; g_bar = +0 off the mask
+// gives +0, which leaves the chain unchanged just like the reference's skipped
+// term). Branch-free (x * 1 is exact), so lanes with and without squares share
+// one instruction stream.
+__device__ __forceinline__ double lane_term(double v, bool sq) { return xmul(v, sq ? v : 1.0); }
+__device__ __forceinline__ double lane_sum(const double* __restrict__ p, int stride, bool sq,
+                                           int n) {
+  constexpr int B = 16;
+  double s = 0.0;
+  int t = 0;
+  auto load = [&](double (&r)[B], int at) {
 #pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    const double2 t = w[h];
-    v[2 * h] = t.x;
-    v[2 * h + 1] = t.y;
-  }
-}
-
-// Cross-lane ordered chains. Within a 256-index round, lane L holds the terms of
-// indices base + 8L .. base + 8L + 7 (computed in parallel); the running sums
-// are handed from lane to lane with a shuffle, so each s[k] is the single
-// ascending chain ((0 + t_0) + t_1) + ... of the reference, skipping the terms
-// whose use flag is false (exact zeros). A skipped term is added as -0, which
-// leaves every sum bit-identical (s + -0 = s, +0 included: a chain that starts
-// at +0 never becomes -0), so the chain is pure dependent DADDs with no select.
-// All lanes end with the current sums.
-template <int K>
-__device__ __forceinline__ void lane_chain(double (&s)[K], const double (&t)[K][8],
-                                           const bool (&use)[K][8], int nsteps) {
-  const int lane = threadIdx.x & 31;
-  double tt[K][8];
+    for (int e = 0; e < B; ++e) r[e] = p[(at + e) * stride];
+  };
+  auto run = [&](const double (&r)[B]) {
 #pragma unroll
-  for (int e = 0; e < 8; ++e)
-#pragma unroll
-    for (int k = 0; k < K; ++k) tt[k][e] = use[k][e] ? t[k][e] : -0.0;
-  // Branch-free hand-off: every lane adds its own 8 terms to the current sums
-  // and the sums of lane `src` (the only ones in index order) are broadcast.
-  (void)lane;
-  for (int src = 0; src < nsteps; ++src) {
-    double r[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) r[k] = s[k];
-#pragma unroll
-    for (int e = 0; e < 8; ++e)
-#pragma unroll
-      for (int k = 0; k < K; ++k) r[k] = xadd(r[k], tt[k][e]);
-#pragma unroll
-    for (int k = 0; k < K; ++k) s[k] = __shfl_sync(0xffffffffu, r[k], src);
-  }
-}
-// FAST profile: the same sums as fixed trees instead of the reference's ordered
-// chains (lane-local partials in index order, then an xor-shuffle tree; lane 0's
-// result broadcast so every lane holds identical bits). Deterministic run to run;
-// ~6x shorter than the 32-step cross-lane hand-off of lane_chain.
-template <int K>
-__device__ __forceinline__ void lane_accum(double (&acc)[K], const double (&t)[K][8],
-                                           const bool (&use)[K][8]) {
-#pragma unroll
-  for (int e = 0; e < 8; ++e)
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      if (use[k][e]) acc[k] += t[k][e];
-}
-template <int K>
-__device__ __forceinline__ void lane_finish(double (&s)[K], const double (&acc)[K]) {
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    double v = acc[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    s[k] = __shfl_sync(0xffffffffu, v, 0);
-  }
-}
-__device__ __forceinline__ int chain_steps(int m, int r0) {
-  const int left = (m - r0 + 7) >> 3;
-  return left < 32 ? left : 32;
-}
-
-__device__ void finish_col(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b, int term,
-                           int numeric) {
-  const int lane = threadIdx.x & 31;
-  const int c = S.col[b];
-  const double* xb = sm.x(b);
-  for (int i = lane; i < a.m; i += 32) a.Y[(size_t)c * a.m + i] = xb[i];
-  if (lane == 0) {
-    alnnls_column_result r;
-    r.termination = term;
-    r.numeric_failure = numeric;
-    r.iterations = S.k[b];
-    r.residual_sq = 0.0;
-    r.f_final = S.f[b];
-    r.gbs_final = S.gbs[b];
-    r.multiplies_total = S.mults[b];
-    a.res[c] = r;
-    S.phase[b] = kIdle;
-  }
-  __syncwarp();
-}
-
-// Top of an iteration for column b (nqp.hpp:250-275): g_bar into V, the gbs /
-// x.g / q.x chains, the ordered stop tests. One warp; returns true if stopped.
-__device__ bool mask_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b) {
-  const int lane = threadIdx.x & 31;
-  const double* xb = sm.x(b);
-  const double* gb = sm.g(b);
-  const double* qb = sm.qc(b);
-  for (int i = lane; i < a.m; i += 32) {
-    const double xi = xb[i], gi = gb[i];
-    sm.v(i, b) = (xi > 0.0 || gi < 0.0) ? gi : 0.0;  // g_bar
-  }
-  // the three chains in ascending index order; terms off the mask are exact
-  // zeros (g_bar = 0, x = 0) and are skipped. q.x uses x*q (same product bits).
-  int cnt = 0, bad = 0;
-  double s[3] = {0.0, 0.0, 0.0};
-  double fa[3] = {0.0, 0.0, 0.0};
-  for (int r0 = 0; r0 < a.m; r0 += 256) {
-    const int base = r0 + 8 * lane;
-    double t[3][8];
-    bool use[3][8];
-    if (base < a.m) {
-      double xv[8], gv[8], qv[8];
-      load8(xb + base, xv);
-      load8(gb + base, gv);
-      load8(qb + base, qv);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const bool p = xv[e] > 0.0 || gv[e] < 0.0;  // zero beyond m: never passive
-        cnt += p;
-        if (!isfinite(gv[e])) bad = 1;
-        const double gbar = p ? gv[e] : 0.0;
-        use[0][e] = gbar != 0.0;
-        t[0][e] = xmul(gbar, gbar);
-        use[1][e] = xv[e] != 0.0;
-        t[1][e] = xmul(xv[e], gv[e]);
-        use[2][e] = use[1][e];
-        t[2][e] = xmul(xv[e], qv[e]);
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          use[k][e] = false;
-          t[k][e] = 0.0;
-        }
+    for (int e = 0; e < B; ++e) s = xadd(s, lane_term(r[e], sq));
+  };
+  if (n >= 2 * B) {
+    double ra[B], rb[B];
+    load(ra, 0);
+    for (; t + 3 * B <= n; t += 2 * B) {
+      load(rb, t + B);
+      run(ra);
+      load(ra, t + 2 * B);
+      run(rb);
     }
-    if (a.fast) lane_accum<3>(fa, t, use);
-    else lane_chain<3>(s, t, use, chain_steps(a.m, r0));
-  }
-  if (a.fast) lane_finish<3>(s, fa);
-  for (int o = 16; o > 0; o >>= 1) {
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
-  }
-  const double gbs = s[0], xg = s[1], qx = s[2];
-  int stop = -1;
-  if (lane == 0) {
-    const double f = xmul(0.5, xadd(xg, qx));
-    const unsigned long long k = S.k[b];
-    S.f[b] = f;
-    S.gbs[b] = gbs;
-    S.ml[b] = cnt;
-    if (bad || !isfinite(f) || !isfinite(gbs)) stop = 100;
-    else if (cnt == 0) stop = ALNNLS_EMPTY_PASSIVE_SET;
-    else if (gbs < a.eps) stop = ALNNLS_GRADIENT_BELOW_EPSILON;
-    else if (k >= a.max_iters) stop = ALNNLS_MAX_ITERS;
-    else if (gbs < S.best[b]) {
-      S.best[b] = gbs;
-      S.since[b] = 0;
-    } else if (++S.since[b] >= a.stall_window) stop = ALNNLS_STALLED;
-    if (stop < 0 && !(gbs != 0.0)) stop = ALNNLS_ZERO_CURVATURE;
-    if (stop < 0) S.phase[b] = kNeedP1;
-  }
-  stop = __shfl_sync(0xffffffffu, stop, 0);
-  if (stop >= 0) finish_col(a, S, sm, b, stop == 100 ? 0 : stop, stop == 100);
-  return stop >= 0;
-}
-
-// den = g_bar . (Q g_bar) over the mask (exact_step, nqp.hpp:166-172).
-__device__ double den_chain(const BatchSmem& sm, int b, bool fast) {
-  const int lane = threadIdx.x & 31;
-  double fa[1] = {0.0};
-  const double* xb = sm.x(b);
-  const double* gb = sm.g(b);
-  const double* ub = sm.u(b);
-  double s[1] = {0.0};
-  for (int r0 = 0; r0 < sm.m; r0 += 256) {
-    const int base = r0 + 8 * lane;
-    double t[1][8];
-    bool use[1][8];
-    if (base < sm.m) {
-      double xv[8], gv[8], uv[8];
-      load8(xb + base, xv);
-      load8(gb + base, gv);
-      load8(ub + base, uv);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const double gbar = (xv[e] > 0.0 || gv[e] < 0.0) ? gv[e] : 0.0;
-        use[0][e] = gbar != 0.0;
-        t[0][e] = xmul(gbar, uv[e]);
-      }
+    if (t + 2 * B <= n) {  // ra holds [t, t + B)
+      load(rb, t + B);
+      run(ra);
+      run(rb);
+      t += 2 * B;
     } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        use[0][e] = false;
-        t[0][e] = 0.0;
-      }
+      run(ra);
+      t += B;
     }
-    if (fast) lane_accum<1>(fa, t, use);
-    else lane_chain<1>(s, t, use, chain_steps(sm.m, r0));
   }
-  if (fast) lane_finish<1>(s, fa);
-  return s[0];
+  for (; t < n; ++t) s = xadd(s, lane_term(p[t * stride], sq));
+  return s;
+}
+// FAST profile: a column's sums as fixed trees instead of the reference's
+// chains: each lane adds its rows in index order, an xor-shuffle tree combines
+// the lanes, the column's warps' partials are added in warp order by the
+// decision lane. Deterministic run to run; no chain phase.
+__device__ __forceinline__ double warp_tree(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+__device__ __forceinline__ double fast_parts(const ColState& S, int b, int k, int wpc) {
+  double s = S.part[b][0][k];
+  for (int w = 1; w < wpc; ++w) s += S.part[b][w][k];
+  return s;
 }
 
-// df = sum over the changed set of (g + 0.5 gd) * delta (nqp.hpp:307). The
-// changed set is where the candidate differs from x, and delta = cand - x is
-// recomputed with the same operation cand_phase used.
-__device__ double df_chain(const BatchSmem& sm, int b, bool fast) {
-  const int lane = threadIdx.x & 31;
-  double fa[1] = {0.0};
-  const double* xb = sm.x(b);
-  const double* gb = sm.g(b);
-  const double* cb = sm.c(b);
-  const double* ub = sm.u(b);
-  double s[1] = {0.0};
-  for (int r0 = 0; r0 < sm.m; r0 += 256) {
-    const int base = r0 + 8 * lane;
-    double t[1][8];
-    bool use[1][8];
-    if (base < sm.m) {
-      double xv[8], gv[8], cv[8], uv[8];
-      load8(xb + base, xv);
-      load8(gb + base, gv);
-      load8(cb + base, cv);
-      load8(ub + base, uv);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const double dd = cv[e] != xv[e] ? xsub(cv[e], xv[e]) : 0.0;
-        use[0][e] = dd != 0.0;
-        t[0][e] = xmul(xadd(gv[e], xmul(0.5, uv[e])), dd);
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        use[0][e] = false;
-        t[0][e] = 0.0;
-      }
-    }
-    if (fast) lane_accum<1>(fa, t, use);
-    else lane_chain<1>(s, t, use, chain_steps(sm.m, r0));
-  }
-  if (fast) lane_finish<1>(s, fa);
-  return s[0];
+// Elementwise phases: warp w works on column w / wpc (wpc = warps per column),
+// its lanes on rows sub*32 + lane, sub*32 + lane + 32*wpc, ...
+struct ColWarp {
+  int b, i0, step, sub;
+};
+__device__ __forceinline__ ColWarp col_warp(int NB) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const int wpc = nw / NB;  // NB divides the warp count (16, 8 or 4 columns, 16 warps)
+  ColWarp w;
+  w.b = warp / wpc;
+  w.sub = warp - w.b * wpc;
+  w.i0 = w.sub * 32 + lane;
+  w.step = 32 * wpc;
+  return w;
 }
 
-// Candidate step and changed set with the column's alpha (nqp.hpp:294-303):
-// C = candidate x, V = delta (0 off the changed set). Returns |changed|.
-__device__ int cand_phase(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b) {
-  const int lane = threadIdx.x & 31;
-  const double alpha = S.alpha[b];
-  const double* xb = sm.x(b);
-  const double* gb = sm.g(b);
+// Elementwise work of one settle round. Writes V = g_bar and the stop-test terms
+// (U: x g, C: x q; -0 for the terms the reference skips) for the columns about
+// to run a stop test, C = cand and V = delta for a candidate step.
+__device__ void round_elementwise(const BatchArgs& a, ColState& S, const BatchSmem& sm, int NB) {
+  const ColWarp w = col_warp(NB);
+  const int b = w.b, m = sm.m;
+  const int act = S.act[b];
+  if (act == kActNone) return;
+  double* xb = sm.x(b);
+  double* gb = sm.g(b);
   double* cb = sm.c(b);
-  int cnt = 0;
-  for (int i = lane; i < a.m; i += 32) {
-    const double xi = xb[i], gi = gb[i];
-    double d = 0.0, c = xi;
-    if (xi > 0.0 || gi < 0.0) {
-      double t = xsub(xi, xmul(alpha, gi));
-      if (t < 0.0) t = 0.0;
-      if (t != xi) {
-        c = t;
-        d = xsub(t, xi);
-        ++cnt;
+  double* ub = sm.u(b);
+  double* qb = sm.qc(b);
+  int cnt = 0, bad = 0;
+  if (act == kActCand) {
+    const double alpha = S.alpha[b];
+#pragma unroll 4
+    for (int i = w.i0; i < m; i += w.step) {
+      const double xi = xb[i], gi = gb[i];
+      double d = 0.0, c = xi;
+      if (xi > 0.0 || gi < 0.0) {
+        double t = xsub(xi, xmul(alpha, gi));  // x - (alpha g), nqp.hpp:296
+        if (t < 0.0) t = 0.0;
+        if (t != xi) {
+          c = t;
+          d = xsub(t, xi);
+          ++cnt;
+        }
+      }
+      cb[i] = c;
+      sm.v(i, b) = d;
+    }
+  } else if (act == kActAccept || act == kActMask || act == kActInit) {
+    const double* qg = a.QB + (size_t)S.col[b] * m;
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // FAST partials
+#pragma unroll 4
+    for (int i = w.i0; i < m; i += w.step) {
+      double xi, gi, qi;
+      if (act == kActAccept) {  // nqp.hpp:309-313
+        xi = cb[i];
+        gi = xadd(gb[i], ub[i]);
+        xb[i] = xi;
+        gb[i] = gi;
+        qi = qb[i];
+      } else if (act == kActInit) {  // x = 0, grad = q (nqp.hpp:224-225)
+        qi = __ldg(qg + i);
+        xi = 0.0;
+        gi = qi;
+        xb[i] = xi;
+        gb[i] = gi;
+        qb[i] = qi;
+      } else {
+        xi = xb[i];
+        gi = gb[i];
+        qi = qb[i];
+      }
+      const bool p = xi > 0.0 || gi < 0.0;
+      cnt += p;
+      if (!isfinite(gi)) bad = 1;
+      const double gbar = p ? gi : 0.0;
+      sm.v(i, b) = gbar;  // its square is formed by the chain lane
+      // x.g and q.x: the x_i = 0 terms are skipped (q.x uses x*q, same bits)
+      const double txg = xi != 0.0 ? xmul(xi, gi) : -0.0;
+      const double tqx = xi != 0.0 ? xmul(xi, qi) : -0.0;
+      if (a.fast) {
+        f0 += xmul(gbar, gbar);
+        f1 += txg;
+        f2 += tqx;
+      } else {
+        ub[i] = txg;
+        cb[i] = tqx;
       }
     }
-    cb[i] = c;
-    sm.v(i, b) = d;
+    if (a.fast) {
+      f0 = warp_tree(f0);
+      f1 = warp_tree(f1);
+      f2 = warp_tree(f2);
+      if ((threadIdx.x & 31) == 0) {
+        S.part[b][w.sub][0] = f0;
+        S.part[b][w.sub][1] = f1;
+        S.part[b][w.sub][2] = f2;
+      }
+    }
+  } else if (act == kActFinish || act == kActGrab) {
+    if (act == kActFinish)
+      for (int i = w.i0; i < m; i += w.step) a.Y[(size_t)S.col[b] * m + i] = xb[i];
+    for (int i = w.i0; i < m; i += w.step) sm.v(i, b) = 0.0;  // idle slots feed zeros
   }
-  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  __syncwarp();
-  return cnt;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (cnt) atomicAdd(S.cnt + b, cnt);
+    if (bad) S.bad[b] = 1;
+  }
 }
 
-// Loads the next RHS from the queue into slot b and runs its first stop test
-// (repeats while columns stop immediately). One warp.
-__device__ void refill(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b) {
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    int c = 0;
-    if (lane == 0) c = atomicAdd(a.next_col, 1);
-    c = __shfl_sync(0xffffffffu, c, 0);
+// One column's stop test after its stop-test chains (nqp.hpp:251-275). Lane
+// b of the chain warp. Sets act (None: continue with P1; Finish: stopped).
+__device__ void stop_test(const BatchArgs& a, ColState& S, int b) {
+  const double gbs = S.res[b][0], xg = S.res[b][1], qx = S.res[b][2];
+  const double f = xmul(0.5, xadd(xg, qx));
+  const unsigned long long k = S.k[b];
+  const int cnt = S.cnt[b];
+  S.f[b] = f;
+  S.gbs[b] = gbs;
+  S.ml[b] = cnt;
+  int stop = -2;
+  if (S.bad[b] || !isfinite(f) || !isfinite(gbs)) stop = -1;  // NumericFailure
+  else if (cnt == 0) stop = ALNNLS_EMPTY_PASSIVE_SET;
+  else if (gbs < a.eps) stop = ALNNLS_GRADIENT_BELOW_EPSILON;
+  else if (k >= a.max_iters) stop = ALNNLS_MAX_ITERS;
+  else if (gbs < S.best[b]) {
+    S.best[b] = gbs;
+    S.since[b] = 0;
+  } else if (++S.since[b] >= a.stall_window) stop = ALNNLS_STALLED;
+  if (stop == -2 && !(gbs != 0.0)) stop = ALNNLS_ZERO_CURVATURE;  // num == 0 (nqp.hpp:167)
+  if (stop == -2) {
+    S.phase[b] = kNeedP1;
+    S.act[b] = kActNone;
+  } else {
+    S.term[b] = stop;
+    S.act[b] = kActFinish;
+  }
+}
+
+// Lane b of the chain warp, after the elementwise phase of a round.
+__device__ void round_decide(const BatchArgs& a, ColState& S, int b) {
+  const int act = S.act[b];
+  if (act == kActCand) {
+    const int cl = S.cnt[b];
+    if (cl == 0) {  // nothing moved (nqp.hpp:304): next iteration on the same state
+      ++S.k[b];
+      S.act[b] = kActMask;
+    } else {
+      S.mults[b] += (unsigned long long)a.m * (unsigned long long)cl;
+      S.phase[b] = kNeedP2;
+      S.act[b] = kActNone;
+    }
+  } else if (act == kActAccept || act == kActMask || act == kActInit) {
+    stop_test(a, S, b);
+  } else if (act == kActFinish || act == kActGrab) {
+    if (act == kActFinish) {
+      alnnls_column_result r;
+      r.termination = S.term[b] < 0 ? 0 : S.term[b];
+      r.numeric_failure = S.term[b] < 0;
+      r.iterations = S.k[b];
+      r.residual_sq = 0.0;
+      r.f_final = S.f[b];
+      r.gbs_final = S.gbs[b];
+      r.multiplies_total = S.mults[b];
+      a.res[S.col[b]] = r;
+    }
+    const int c = atomicAdd(a.next_col, 1);
     if (c >= a.ncols) {
-      for (int i = lane; i < a.m; i += 32) sm.v(i, b) = 0.0;  // idle slots feed zeros
-      if (lane == 0) S.phase[b] = kIdle;
-      __syncwarp();
-      return;
-    }
-    const double* q = a.QB + (size_t)c * a.m;
-    double* xb = sm.x(b);
-    double* gb = sm.g(b);
-    double* qb = sm.qc(b);
-    for (int i = lane; i < a.m; i += 32) {
-      const double qi = __ldg(q + i);
-      xb[i] = 0.0;
-      gb[i] = qi;  // x = 0, grad = q (nqp.hpp:224-225)
-      qb[i] = qi;
-    }
-    if (lane == 0) {
+      S.phase[b] = kIdle;
+      S.act[b] = kActNone;
+    } else {
       S.col[b] = c;
       S.k[b] = 0;
       S.tries[b] = 0;
       S.best[b] = __longlong_as_double(0x7ff0000000000000LL);
       S.since[b] = 0;
       S.mults[b] = 0;
+      S.act[b] = kActInit;
     }
-    __syncwarp();
-    if (!mask_phase(a, S, sm, b)) return;
   }
 }
+
+// Settle rounds until every slot has a GEMM pass to wait for (or is idle):
+// elementwise phase, the stop-test chains of the columns that need them, the
+// per-column decisions. Whole CTA; the chain warp is warp 0 (lane b: column b).
+__device__ void settle(const BatchArgs& a, ColState& S, const BatchSmem& sm, int NB) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef ALNNLS_BATCH_PROF
+  long long t0 = clock64();
+#define BPROF(k) { const long long t1 = clock64(); if (threadIdx.x == 0) S.pr[k] += t1 - t0; t0 = t1; }
+#else
+#define BPROF(k)
+#endif
+  for (;;) {
+    __syncthreads();  // acts and counter resets are visible
+    BPROF(2)
+    int pending = 0;
+    for (int b = 0; b < NB; ++b) pending |= S.act[b] != kActNone;
+    if (!pending) return;
+    round_elementwise(a, S, sm, NB);
+    __syncthreads();
+    BPROF(3)
+#ifdef ALNNLS_BATCH_PROF
+    if (threadIdx.x == 0) S.pr[5]++;
+#endif
+    // the stop-test sums: chain k of column b on lane 32 * (k / 2) + 16 * (k % 2) + b
+    if (warp < 2) {
+      const int k = 2 * warp + (lane >> 4), b = lane & 15;
+      if (k < 3 && b < NB) {
+        const int act = S.act[b];
+        if (act == kActAccept || act == kActMask || act == kActInit) {
+          if (a.fast) {
+            S.res[b][k] = fast_parts(S, b, k, (int)(blockDim.x >> 5) / NB);
+          } else {
+            const double* p = k == 0 ? sm.V + b : (k == 1 ? sm.u(b) : sm.c(b));
+            S.res[b][k] = lane_sum(p, k == 0 ? sm.ld : 1, k == 0, sm.m);
+          }
+        }
+      }
+      asm volatile("bar.sync 1, 64;" ::: "memory");
+    }
+    if (warp == 0 && lane < NB) {
+      const int b = lane;
+      if (S.act[b] == kActAccept) ++S.k[b];
+      round_decide(a, S, b);
+      if (S.act[b] != kActNone) {
+        S.cnt[b] = 0;
+        S.bad[b] = 0;
+      }
+    }
+    BPROF(4)
+  }
+}
+
+// After a GEMM pass (U = Q V for every live column): the P1 columns' den terms
+// (exact_step, nqp.hpp:166-172) and the P2 columns' df terms (nqp.hpp:307) into
+// V, their chains, alpha / accept-or-halve (nqp.hpp:308-317), the settle rounds.
+__device__ void after_pass(const BatchArgs& a, ColState& S, const BatchSmem& sm, int NB) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = sm.m;
+#ifdef ALNNLS_BATCH_PROF
+  long long t0 = clock64();
+#endif
+  {
+    const ColWarp w = col_warp(NB);
+    const int b = w.b;
+    const int ph = S.phase[b];
+    const double* xb = sm.x(b);
+    const double* gb = sm.g(b);
+    const double* ub = sm.u(b);
+    const double* cb = sm.c(b);
+    double f = 0.0;  // FAST partial
+    if (ph == kNeedP1) {
+#pragma unroll 4
+      for (int i = w.i0; i < m; i += w.step) {
+        const double gbar = sm.v(i, b);  // the pass's input: g_bar
+        const double t = gbar != 0.0 ? xmul(gbar, ub[i]) : -0.0;
+        if (a.fast) f += t;
+        else sm.v(i, b) = t;
+      }
+    } else if (ph == kNeedP2) {
+#pragma unroll 4
+      for (int i = w.i0; i < m; i += w.step) {
+        const double dd = sm.v(i, b);  // the pass's input: delta (0 off the changed set)
+        const double t = dd != 0.0 ? xmul(xadd(gb[i], xmul(0.5, ub[i])), dd) : -0.0;
+        if (a.fast) f += t;
+        else sm.v(i, b) = t;
+      }
+    }
+    if (a.fast && ph != kIdle) {
+      f = warp_tree(f);
+      if (lane == 0) S.part[b][w.sub][0] = f;
+    }
+    (void)xb;
+    (void)cb;
+  }
+  __syncthreads();
+  BPROF(0)
+  if (warp == 0 && lane < NB) {
+    const int b = lane;
+    const int ph = S.phase[b];
+    if (ph != kIdle) {
+      const double s = a.fast ? fast_parts(S, b, 0, (int)(blockDim.x >> 5) / NB)
+                              : lane_sum(sm.V + b, sm.ld, false, m);
+      if (ph == kNeedP1) {
+        if (!(s > 0.0)) {
+          S.term[b] = ALNNLS_ZERO_CURVATURE;
+          S.act[b] = kActFinish;
+        } else {
+          S.alpha[b] = xdiv(S.gbs[b], s);
+          S.tries[b] = 0;
+          S.mults[b] += (unsigned long long)m * (unsigned long long)S.ml[b];
+          S.act[b] = kActCand;
+        }
+      } else if (s <= 0.0 || S.tries[b] >= 60) {
+        S.act[b] = kActAccept;
+      } else {
+        S.alpha[b] = xmul(S.alpha[b], 0.5);  // nqp.hpp:317
+        ++S.tries[b];
+        S.act[b] = kActCand;
+      }
+      S.cnt[b] = 0;
+      S.bad[b] = 0;
+    }
+  }
+  BPROF(1)
+  settle(a, S, sm, NB);
+}
+
 
 // One exact chain GEMM pass for a group of CG columns starting at column
 // grp * CG: U[:, col] = Q V[:, col], rows i = trow + r * ROWT (ascending j per
@@ -405,7 +494,11 @@ __device__ __forceinline__ void gemm_pass(const BatchArgs& a, const BatchSmem& s
   auto load_q = [&](int j0, double (&qv)[RPT][JB]) {
 #pragma unroll
     for (int u = 0; u < JB; ++u) {
+#ifdef ALNNLS_EXP_QL1
+      const double* qc = a.Q + (size_t)((j0 + u) & 7) * m;
+#else
       const double* qc = a.Q + (size_t)(j0 + u) * m;
+#endif
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         const int i = trow + r * ROWT;
@@ -418,12 +511,18 @@ __device__ __forceinline__ void gemm_pass(const BatchArgs& a, const BatchSmem& s
     for (int u = 0; u < JB; ++u) {
       const double* vrow = sm.V + (size_t)(j0 + u) * LD + grp * CG;
       double vb[CG];
+#ifdef ALNNLS_EXP_NOV
+#pragma unroll
+      for (int b = 0; b < CG; ++b) vb[b] = 1.0 + b + (j0 & 3);
+      (void)vrow;
+#else
 #pragma unroll
       for (int b = 0; b < CG; b += 2) {
         const double2 t = *reinterpret_cast<const double2*>(vrow + b);
         vb[b] = t.x;
         vb[b + 1] = t.y;
       }
+#endif
 #pragma unroll
       for (int r = 0; r < RPT; ++r)
 #pragma unroll
@@ -444,68 +543,9 @@ __device__ __forceinline__ void gemm_pass(const BatchArgs& a, const BatchSmem& s
     const int i = trow + r * ROWT;
     if (i < m) {
 #pragma unroll
-      for (int b = 0; b < CG; ++b) sm.U[(size_t)(grp * CG + b) * mp + i] = acc[r * CG + b];
+      for (int b = 0; b < CG; ++b) sm.U[(size_t)(grp * CG + b) * sm.ps + i] = acc[r * CG + b];
     }
   }
-}
-
-// Column b's state machine after its GEMM pass (nqp.hpp:276-318): P1 result ->
-// den, alpha, candidate step; P2 result -> df, accept (next mask / stop tests)
-// or halve and retry. One warp; V of the column is ready for its next pass.
-__device__ void column_step(const BatchArgs& a, ColState& S, const BatchSmem& sm, int b) {
-  const int lane = threadIdx.x & 31;
-  const int m = sm.m;
-  const int ph = S.phase[b];
-  if (ph == kIdle) return;
-  if (ph == kNeedP1) {
-    const double den = den_chain(sm, b, a.fast != 0);  // exact_step, nqp.hpp:166-172
-    if (!(den > 0.0)) {
-      finish_col(a, S, sm, b, ALNNLS_ZERO_CURVATURE, 0);
-      refill(a, S, sm, b);
-      return;
-    }
-    if (lane == 0) {
-      S.alpha[b] = xdiv(S.gbs[b], den);
-      S.tries[b] = 0;
-      S.mults[b] += (unsigned long long)m * (unsigned long long)S.ml[b];
-    }
-    __syncwarp();
-  } else {  // kNeedP2: gd = Q delta in U
-    const double df = df_chain(sm, b, a.fast != 0);
-    const bool accept = df <= 0.0 || S.tries[b] >= 60;
-    if (accept) {  // x[C] = cand, grad += gd (nqp.hpp:309-313)
-      double* xb = sm.x(b);
-      double* gw = sm.g(b);
-      const double* cb = sm.c(b);
-      const double* ub = sm.u(b);
-      for (int i = lane; i < m; i += 32) {
-        xb[i] = cb[i];
-        gw[i] = xadd(gw[i], ub[i]);
-      }
-      if (lane == 0) ++S.k[b];
-      __syncwarp();
-      if (mask_phase(a, S, sm, b)) refill(a, S, sm, b);
-      return;
-    }
-    if (lane == 0) {
-      S.alpha[b] = xmul(S.alpha[b], 0.5);  // nqp.hpp:317
-      ++S.tries[b];
-    }
-    __syncwarp();
-  }
-  // candidate step with the current alpha
-  const int cl = cand_phase(a, S, sm, b);
-  if (cl == 0) {  // nothing moved (nqp.hpp:304): next iteration on the same state
-    if (lane == 0) ++S.k[b];
-    __syncwarp();
-    if (mask_phase(a, S, sm, b)) refill(a, S, sm, b);
-    return;
-  }
-  if (lane == 0) {
-    S.mults[b] += (unsigned long long)m * (unsigned long long)cl;
-    S.phase[b] = kNeedP2;
-  }
-  __syncwarp();
 }
 
 // FAST profile: the pass U = Q V on the fp64 tensor cores (mma.sync m16n8k8
@@ -562,7 +602,7 @@ __device__ __forceinline__ void dmma_gemm_pass16(const BatchArgs& a, const Batch
     for (int c = 0; c < 4; ++c) {
       const int row = (c < 2 ? ra : rb);
       const int col = 8 * nt + 2 * t + (c & 1);
-      if (row < m) sm.U[(size_t)col * mp + row] = acc[nt][c];
+      if (row < m) sm.U[(size_t)col * sm.ps + row] = acc[nt][c];
     }
 }
 
@@ -572,33 +612,41 @@ __device__ __forceinline__ BatchSmem carve(double* bsm, int m, int nb) {
   sm.ld = batch_ld(nb);
   sm.m = m;
   sm.mp = mp;
+  sm.ps = panel_stride(m);
   sm.V = bsm;
   sm.U = bsm + (size_t)mp * sm.ld;
-  sm.C = sm.U + (size_t)mp * nb;
-  sm.X = sm.C + (size_t)mp * nb;
-  sm.G = sm.X + (size_t)mp * nb;
-  sm.q = sm.G + (size_t)mp * nb;
-  const int total = mp * sm.ld + 5 * mp * nb;  // zero once: pads must read as +0
+  sm.C = sm.U + (size_t)sm.ps * nb;
+  sm.X = sm.C + (size_t)sm.ps * nb;
+  sm.G = sm.X + (size_t)sm.ps * nb;
+  sm.q = sm.G + (size_t)sm.ps * nb;
+  const int total = mp * sm.ld + 5 * sm.ps * nb;  // zero once: pads must read as +0
   for (int e = threadIdx.x; e < total; e += blockDim.x) bsm[e] = 0.0;
   return sm;
 }
 
-// Every pass, all threads run the GEMM for all NB columns, then one warp per
-// column runs its state machine. (A warp-specialised variant -- 8 warps on the
-// GEMM of one half of the columns while 8 run the other half's state machines --
-// measured slower at c4: 1.71-1.86 s vs 1.65 s; with 2 warps per scheduler the
-// GEMM cannot hide the L2 latency of Q.)
+// Every pass, all threads run the GEMM for all NB columns, then the per-column
+// state machines advance in CTA-wide phases: elementwise work over (column, row)
+// by all threads, the reference-ordered sums by one lane per column (so one
+// DADD instruction advances every column's chain), the scalar decisions by the
+// same lanes. (A warp-specialised variant -- 8 warps on the GEMM of one half of
+// the columns while 8 run the other half's state machines -- measured slower in
+// round 1; with 2 warps per scheduler the GEMM cannot hide the L2 latency of Q.)
 template <int NB>
 __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
   extern __shared__ __align__(16) double bsm[];
   __shared__ ColState S;
   constexpr int LD = batch_ld(NB);
   const BatchSmem sm = carve(bsm, a.m, NB);
-  __syncthreads();
-  const int warp = threadIdx.x >> 5;
-  constexpr int nwarps = kBT / 32;
-  for (int b = warp; b < NB; b += nwarps) refill(a, S, sm, b);
-  __syncthreads();
+#ifdef ALNNLS_BATCH_PROF
+  if (threadIdx.x < 8) S.pr[threadIdx.x] = 0;
+#endif
+  if (threadIdx.x < NB) {
+    S.phase[threadIdx.x] = kIdle;
+    S.act[threadIdx.x] = kActGrab;
+    S.cnt[threadIdx.x] = 0;
+    S.bad[threadIdx.x] = 0;
+  }
+  settle(a, S, sm, NB);
 #ifndef ALNNLS_GEMM_CG
 #define ALNNLS_GEMM_CG 8
 #endif
@@ -607,20 +655,45 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
   constexpr int ROWT = kBT / GROUPS;
   constexpr int RPT = (4096 / NB + ROWT - 1) / ROWT;  // rows per thread at the largest m (4096/NB)
   const int grp = threadIdx.x / ROWT, trow = threadIdx.x % ROWT;
+#ifdef ALNNLS_BATCH_PROF
+  long long t_g = 0, t_s = 0, npass = 0, nact = 0;
+#endif
   for (;;) {
     int active = 0;
     for (int b = 0; b < NB; ++b) active |= S.phase[b] != kIdle;
     if (!active) break;
+#ifdef ALNNLS_BATCH_PROF
+    const long long c0 = clock64();
+    for (int b = 0; b < NB; ++b) nact += S.phase[b] != kIdle;
+    ++npass;
+#endif
     if (NB == 16 && a.fast) {
       dmma_gemm_pass16<LD>(a, sm);
     } else {
       gemm_pass<RPT, CG, ROWT, LD, ALNNLS_GEMM_JB>(a, sm, grp, trow);
     }
     __syncthreads();
-    for (int b = warp; b < NB; b += nwarps) column_step(a, S, sm, b);
-    __syncthreads();
+#ifdef ALNNLS_BATCH_PROF
+    const long long c1 = clock64();
+#endif
+    after_pass(a, S, sm, NB);  // ends with every thread past the last settle barrier
+#ifdef ALNNLS_BATCH_PROF
+    const long long c2 = clock64();
+    t_g += c1 - c0;
+    t_s += c2 - c1;
+#endif
   }
+#ifdef ALNNLS_BATCH_PROF
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("batched prof cta %d: passes %lld, gemm %.1f kcyc/pass, state %.1f kcyc/pass, active cols/pass %.2f\n",
+           blockIdx.x, npass, t_g / 1e3 / npass, t_s / 1e3 / npass, (double)nact / npass);
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("  cta %d per pass (kcyc): elem0 %.2f chain1 %.2f | rounds/pass %.2f: sync+check %.2f elem %.2f chain+decide %.2f\n",
+           blockIdx.x, S.pr[0] / 1e3 / npass, S.pr[1] / 1e3 / npass, (double)S.pr[5] / npass,
+           S.pr[2] / 1e3 / npass, S.pr[3] / 1e3 / npass, S.pr[4] / 1e3 / npass);
+#endif
 }
+
 
 // x[retained[a], j] = Y[a, j] / D_a; dropped columns 0 (nnls.hpp:87-96).
 __global__ void unscale_batched_kernel(const double* Y, int m, const double* scale,
