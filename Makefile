@@ -14,7 +14,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xptxas -v \
            -Xcompiler -Wall $(EXTRA)
 CU_SRCS := $(PKG)/csrc/nqp.cu $(PKG)/csrc/setup.cu $(PKG)/csrc/capi.cu $(PKG)/csrc/batched.cu \
-           $(PKG)/csrc/dmma.cu $(PKG)/csrc/fastloop.cu
+           $(PKG)/csrc/dmma.cu $(PKG)/csrc/fastloop.cu $(PKG)/csrc/small.cu
 CU_HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/alnnls.h
 CU_OBJS := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(CU_SRCS))
 

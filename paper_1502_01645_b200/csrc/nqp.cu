@@ -1196,6 +1196,9 @@ cudaError_t launch_loop(KC kcluster, KG kgrid, const LoopArgs& a, int num_ctas,
 }
 
 cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream) {
+  // small m: the cluster loop with its state in distributed shared memory (small.cu)
+  const cudaError_t e = launch_nqp_small(a, num_ctas, stream);
+  if (e != cudaErrorNotSupported) return e;
   return launch_loop(nqp_loop_kernel<true>, nqp_loop_kernel<false>, a, num_ctas, stream);
 }
 

@@ -9,7 +9,7 @@ out=build/var/$name; mkdir -p $out
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FL="$ARCH -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC $*"
 objs=""
-for f in nqp setup capi batched dmma fastloop; do
+for f in nqp setup capi batched dmma fastloop small; do
   /usr/local/cuda/bin/nvcc $FL -c -o $out/$f.o paper_1502_01645_b200/csrc/$f.cu &
   objs="$objs $out/$f.o"
 done
