@@ -58,6 +58,15 @@ struct alnnls_ctx {
   unsigned long long phase_ns[8] = {};
   uint64_t launches = 0;
   cudaEvent_t timer[2] = {};
+  // pinned host copies read after one stream sync (deferred NQP control block,
+  // the residual), so a solve needs no host round trip between the loop and its finish
+  struct Pinned {
+    LoopCtrl hc;
+    double hres;
+  };
+  Pinned* pin = nullptr;
+  uint64_t nqp_tcap = 0, nqp_mcap = 0, nqp_m = 0;
+  int nqp_record_mults = 0;
 };
 
 namespace {
@@ -157,8 +166,12 @@ int check_ctx(alnnls_ctx* ctx) {
 // ---- the device-resident NQP solve on ctx->Q / ctx->q (already uploaded) ------
 // x0: nullptr -> start at 0 (g = q); otherwise device start vector (validated).
 // solver 0: solve_nqp (nqp.hpp:215-339); 1: solve_accelerated (accelerated.hpp:21-117).
+int collect_nqp(alnnls_ctx* ctx, alnnls_summary* out);
+
+// defer: return right after the launches with the control block's copy enqueued;
+// the caller enqueues more work, synchronises once and calls collect_nqp.
 int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config* cfg,
-            const double* dstart, alnnls_summary* out, int solver = 0) {
+            const double* dstart, alnnls_summary* out, int solver = 0, bool defer = false) {
   int st__ = ALNNLS_OK;
   const double* Q = static_cast<const double*>(ctx->Q.p);
   const double* q = static_cast<const double*>(ctx->q.p);
@@ -330,22 +343,33 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
     CK(launch_nqp_loop(a, nctas, s));
   }
   CK(cudaEventRecord(ctx->ev[3], s));
-  LoopCtrl hc;
-  CK(cudaMemcpyAsync(&hc, ctrl, sizeof(LoopCtrl), cudaMemcpyDeviceToHost, s));
+  if (!ctx->pin) CK(cudaMallocHost(&ctx->pin, sizeof(alnnls_ctx::Pinned)));
+  CK(cudaMemcpyAsync(&ctx->pin->hc, ctrl, sizeof(LoopCtrl), cudaMemcpyDeviceToHost, s));
+  ctx->nqp_tcap = tcap;
+  ctx->nqp_mcap = mcap;
+  ctx->nqp_m = m;
+  ctx->nqp_record_mults = cfg->record_multiplies;
+  if (defer) return ALNNLS_OK;
   CK(cudaStreamSynchronize(s));
+  return collect_nqp(ctx, out);
+}
+
+// Fills the summary from the control block run_nqp copied (after a stream sync).
+int collect_nqp(alnnls_ctx* ctx, alnnls_summary* out) {
+  const LoopCtrl& hc = ctx->pin->hc;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
   out->t_loop_s = ms * 1e-3;
   out->termination = hc.termination;
   out->numeric_failure = hc.numeric_failure;
   out->iterations = hc.iterations;
-  out->trace_len = std::min<uint64_t>(hc.trace_len, tcap);
-  out->mult_len = cfg->record_multiplies ? std::min<uint64_t>(hc.mult_len, mcap) : 0;
+  out->trace_len = std::min<uint64_t>(hc.trace_len, ctx->nqp_tcap);
+  out->mult_len = ctx->nqp_record_mults ? std::min<uint64_t>(hc.mult_len, ctx->nqp_mcap) : 0;
   out->multiplies_total = hc.mult_total;
   out->min_iterate = hc.min_iterate;
   out->f_final = hc.f_final;
   out->gbs_final = hc.gbs_final;
-  out->m = m;
+  out->m = ctx->nqp_m;
   ctx->g_parity = hc.g_parity;
   for (int i = 0; i < 8; ++i) ctx->phase_ns[i] = hc.phase_ns[i];
   if (hc.numeric_failure)
@@ -443,14 +467,14 @@ int run_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t
     Resolved r;
     rc = resolve(ctx, cfg, m, &r);  // solve_nqp validates its config (nqp.hpp:220-221)
     if (rc) return rc;
-    rc = run_nqp(ctx, m, r, cfg, nullptr, &sum, solver | ctx->solver);
+    rc = run_nqp(ctx, m, r, cfg, nullptr, &sum, solver | ctx->solver, /*defer=*/true);
     if (rc) {
       if (out) *out = sum;
       ctx->last = sum;
       return rc;
     }
-    CK(cudaMemcpyAsync(y, ctx->g_parity ? ctx->x_alt.p : ctx->x.p, sizeof(double) * m,
-                       cudaMemcpyDeviceToDevice, s));
+    CK(launch_copy_parity(y, static_cast<double*>(ctx->x.p), static_cast<double*>(ctx->x_alt.p),
+                          static_cast<LoopCtrl*>(ctx->ctrl.p), (int)m, s));
   } else {
     // detail::empty_solve_result (nnls.hpp:107-113)
     alnnls_iter_record rec{};
@@ -471,18 +495,25 @@ int run_nnls(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t
   double* vals = ENSURE(double, vals, n + 8);
   int* len = ENSURE(int, mscalar, 4);
   CK(launch_support(xn, (int)n, list, vals, len, s));
-  int hlen = 0;
-  CK(cudaMemcpyAsync(&hlen, len, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
   double* ax = ENSURE(double, ax, d);
   double* pr = ENSURE(double, bcols, d + 8);
   double* res = ENSURE(double, resid, 2);
-  CK(launch_masked_gemv(dA, lda, (int)d, list, vals, hlen, ax, ctx->sm_count, s));
+  // the support length stays on the device: no host round trip before the residual
+  CK(launch_masked_gemv(dA, lda, (int)d, list, vals, (int)n, ax, ctx->sm_count, s, len));
   CK(launch_residual(ax, db, (int)d, pr, res, s));
   CK(cudaEventRecord(ctx->ev[4], s));
-  double hres = 0.0;
-  CK(cudaMemcpyAsync(&hres, res, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  if (!ctx->pin) CK(cudaMallocHost(&ctx->pin, sizeof(alnnls_ctx::Pinned)));
+  CK(cudaMemcpyAsync(&ctx->pin->hres, res, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));  // the one host sync after the setup's
+  const double hres = ctx->pin->hres;
+  if (m > 0) {
+    rc = collect_nqp(ctx, &sum);
+    if (rc) {
+      if (out) *out = sum;
+      ctx->last = sum;
+      return rc;
+    }
+  }
   float t01 = 0, t23 = 0, t34 = 0, t04 = 0;
   cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
   cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
@@ -707,13 +738,14 @@ int run_nnls_overlapped(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A
     if (m > 0) {
       Resolved r;
       if (int rc = resolve(ctx, cfg, m, &r)) return rc;
-      if (int rc = run_nqp(ctx, m, r, cfg, nullptr, &sum, ctx->solver)) {
+      if (int rc = run_nqp(ctx, m, r, cfg, nullptr, &sum, ctx->solver, /*defer=*/true)) {
         if (out) *out = sum;
         ctx->last = sum;
         return rc;
       }
-      CK(cudaMemcpyAsync(y, ctx->g_parity ? ctx->x_alt.p : ctx->x.p, sizeof(double) * m,
-                         cudaMemcpyDeviceToDevice, s));
+      CK(launch_copy_parity(y, static_cast<double*>(ctx->x.p),
+                            static_cast<double*>(ctx->x_alt.p),
+                            static_cast<LoopCtrl*>(ctx->ctrl.p), (int)m, s));
     } else {
       alnnls_iter_record rec{};
       alnnls_iter_record* tr = ENSURE(alnnls_iter_record, trace, 2);
@@ -729,18 +761,23 @@ int run_nnls_overlapped(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* A
     double* vals = ENSURE(double, vals, n + 8);
     int* len = ENSURE(int, mscalar, 4);
     CK(launch_support(xn, (int)n, list, vals, len, s));
-    int hlen = 0;
-    CK(cudaMemcpyAsync(&hlen, len, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
     double* ax = ENSURE(double, ax, d);
     double* pr = ENSURE(double, resid, d + 8);
     double* res = ENSURE(double, flag, 8);  // doubles in the flag buffer (ints there are done)
-    CK(launch_masked_gemv(dA, lda, (int)d, list, vals, hlen, ax, ctx->sm_count, s));
+    CK(launch_masked_gemv(dA, lda, (int)d, list, vals, (int)n, ax, ctx->sm_count, s, len));
     CK(launch_residual(ax, db, (int)d, pr, res, s));
     CK(cudaEventRecord(ctx->ev[4], s));
-    double hres = 0.0;
-    CK(cudaMemcpyAsync(&hres, res, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (!ctx->pin) CK(cudaMallocHost(&ctx->pin, sizeof(alnnls_ctx::Pinned)));
+    CK(cudaMemcpyAsync(&ctx->pin->hres, res, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const double hres = ctx->pin->hres;
+    if (m > 0) {
+      if (int rc = collect_nqp(ctx, &sum)) {
+        if (out) *out = sum;
+        ctx->last = sum;
+        return rc;
+      }
+    }
     float t01 = 0, t23 = 0, t34 = 0, t04 = 0;
     cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
     cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
@@ -824,6 +861,7 @@ void alnnls_destroy(alnnls_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->pin) cudaFreeHost(ctx->pin);
   delete ctx;
 }
 

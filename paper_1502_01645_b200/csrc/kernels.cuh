@@ -140,9 +140,14 @@ bool fast_loop_supported(int m, int R);
 cudaError_t launch_fast_loop(const FastArgs& a, cudaStream_t stream);
 
 // Exact masked GEMV over a row range: y[i] = sum_t M[i, list[t]] * vals[t].
+// dlen (optional): the length is read on the device from *dlen (no host round trip).
 cudaError_t launch_masked_gemv(const double* M, uint64_t ld, int rows, const uint32_t* list,
                                const double* vals, int len, double* y, int sm_count,
-                               cudaStream_t stream);
+                               cudaStream_t stream, const int* dlen = nullptr);
+// y = x or x_alt (m entries), whichever the finished loop's ctrl->g_parity names:
+// the iterate is taken on the device, before the host has read the control block.
+cudaError_t launch_copy_parity(double* y, const double* x, const double* x_alt,
+                               const LoopCtrl* ctrl, int m, cudaStream_t stream);
 
 // Setup (K1-K3): D_i^2 = H_ii chains, retained compaction, fused SYRK+rescale.
 struct SetupArgs {

@@ -1206,8 +1206,10 @@ cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream
 namespace {
 __global__ void __launch_bounds__(kLoopThreads, 1)
     masked_gemv_kernel(const double* M, uint64_t ld, int rows, int rows_per_cta, int blocked,
-                       const uint32_t* list, const double* vals, int len, double* y) {
+                       const uint32_t* list, const double* vals, int len, double* y,
+                       const int* dlen) {
   extern __shared__ __align__(128) uint8_t smem[];
+  if (dlen) len = *dlen;
   const int row0 = blockIdx.x * rows_per_cta;
   const int nrows = max(0, min(rows - row0, rows_per_cta));
   RowRing ring;
@@ -1224,25 +1226,42 @@ __global__ void __launch_bounds__(kLoopThreads, 1)
 
 cudaError_t gemv_launch(const double* M, uint64_t ld, int rows, int rpc, int blocked,
                         const uint32_t* list, const double* vals, int len, double* y,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const int* dlen = nullptr) {
   if (cudaError_t e = smem_optin(masked_gemv_kernel, (int)nqp_loop_smem_bytes())) return e;
   if (rows <= 0) return cudaSuccess;
   if (rpc > 352) return cudaErrorInvalidValue;  // 11 consumer warps + 1 producer
   const int grid = (rows + rpc - 1) / rpc;
   masked_gemv_kernel<<<grid, kLoopThreads, nqp_loop_smem_bytes(), stream>>>(M, ld, rows, rpc,
                                                                             blocked, list, vals,
-                                                                            len, y);
+                                                                            len, y, dlen);
   return cudaGetLastError();
 }
 }  // namespace
 
 cudaError_t launch_masked_gemv(const double* M, uint64_t ld, int rows, const uint32_t* list,
                                const double* vals, int len, double* y, int sm_count,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, const int* dlen) {
   int rpc = (rows + sm_count - 1) / sm_count;
   rpc = (rpc + 3) & ~3;
   if (rpc < 4) rpc = 4;
-  return gemv_launch(M, ld, rows, rpc, 0, list, vals, len, y, stream);
+  return gemv_launch(M, ld, rows, rpc, 0, list, vals, len, y, stream, dlen);
+}
+
+namespace {
+__global__ void copy_parity_kernel(double* y, const double* x, const double* x_alt,
+                                   const LoopCtrl* ctrl, int m) {
+  const double* src = ctrl->g_parity ? x_alt : x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    y[i] = src[i];
+}
+}  // namespace
+
+cudaError_t launch_copy_parity(double* y, const double* x, const double* x_alt,
+                               const LoopCtrl* ctrl, int m, cudaStream_t stream) {
+  if (m <= 0) return cudaSuccess;
+  copy_parity_kernel<<<(m + 255) / 256 < 148 ? (m + 255) / 256 : 148, 256, 0, stream>>>(
+      y, x, x_alt, ctrl, m);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_masked_gemv_blocked(const double* Qb, int m, int R, const uint32_t* list,
