@@ -63,6 +63,7 @@ struct alnnls_ctx {
   struct Pinned {
     LoopCtrl hc;
     double hres;
+    int hm;
   };
   Pinned* pin = nullptr;
   uint64_t nqp_tcap = 0, nqp_mcap = 0, nqp_m = 0;
@@ -217,11 +218,22 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
     mults = ENSURE(uint64_t, mults, mcap);
   }
   cudaStream_t s = ctx->stream;
-  CK(cudaMemsetAsync(gP, 0, sizeof(double) * (m + 8), s));
-  CK(cudaMemsetAsync(dC, 0, sizeof(double) * (m + 8), s));
+  // the exact loop from 0 initialises x, g and its scratch itself (launch_nqp_loop):
+  // for a small problem the cluster kernel does it in its prologue, so no extra
+  // stream operations precede the launch
+  const int R0 = (int)ctx->qR;
+  const bool fast_loop = solver == 0 && cfg->profile == ALNNLS_PROFILE_FAST &&
+                         fast_loop_supported((int)m, R0);
+  const bool zero_start = solver == 0 && !fast_loop && !dstart;
+  if (!zero_start) {
+    CK(cudaMemsetAsync(gP, 0, sizeof(double) * (m + 8), s));
+    CK(cudaMemsetAsync(dC, 0, sizeof(double) * (m + 8), s));
+  }
   if (!dstart) {
-    CK(cudaMemsetAsync(x, 0, sizeof(double) * m, s));
-    CK(cudaMemcpyAsync(g, q, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    if (!zero_start) {
+      CK(cudaMemsetAsync(x, 0, sizeof(double) * m, s));
+      CK(cudaMemcpyAsync(g, q, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    }
   } else {
     // g = matvec(Q, start) + q (nqp.hpp:231-233); skipping x_j == 0 columns is exact.
     CK(cudaMemcpyAsync(x, dstart, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
@@ -275,7 +287,8 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   a.mults_cap = mcap;
   a.ctrl = ctrl;
   a.bar = bar;
-  CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), ctx->stream));
+  if (!zero_start) CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), ctx->stream));
+  a.zero_start = zero_start ? 1 : 0;
   a.rows_per_cta = (int)ctx->qR;
   a.resident = solver == 0 && nqp_resident_fits((int)m, a.rows_per_cta) ? 1 : 0;
   if (a.rows_per_cta > 352)
@@ -423,26 +436,37 @@ int run_setup(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_
   sa.hvec_scratch = ENSURE(double, hvec, n);
   CK(launch_gram_diag(sa, s));
   CK(launch_retained(sa, s));
-  int hm = 0;
-  CK(cudaMemcpyAsync(&hm, sa.m_out, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  const uint64_t m = (uint64_t)hm;
-  const uint64_t mm = m > 0 ? m : 1;
-  ctx->qR = (uint64_t)nqp_rows_per_cta((int)mm, ctx->sm_count);
-  sa.Q = ENSURE(double, Q, blocked_size(mm, ctx->qR));
-  sa.m = (int)m;
-  sa.qR = (int)ctx->qR;
-  sa.q = ENSURE(double, q, vec_pad(m));
-  if (m > 0) {
-    if (profile == ALNNLS_PROFILE_FAST && syrk_dmma_supported(sa, 1)) {
-      if (int rc = dmma_buffers(ctx, sa)) return rc;
-      CK(launch_syrk_dmma(sa, 1, s));
-    } else {
-      if ((rc_sk = streamk_buffers(ctx, sa, 1))) return rc_sk;
-      CK(launch_syrk(sa, 1, s));
+  if (!ctx->pin) CK(cudaMallocHost(&ctx->pin, sizeof(alnnls_ctx::Pinned)));
+  CK(cudaMemcpyAsync(&ctx->pin->hm, sa.m_out, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(ctx->ev[5], s));  // the count has landed in pinned memory
+  // The retained count m is only known on the device. Speculate m = n (no zero
+  // column, the usual case) and queue the Gram + rescale right behind the count,
+  // so the host's read of m overlaps the Gram; if a column was dropped, the Gram
+  // is redone for the real m (the speculative one wrote Q in the wrong layout).
+  auto gram = [&](uint64_t m) -> int {
+    const uint64_t mm = m > 0 ? m : 1;
+    ctx->qR = (uint64_t)nqp_rows_per_cta((int)mm, ctx->sm_count);
+    sa.Q = ENSURE(double, Q, blocked_size(mm, ctx->qR));
+    sa.m = (int)m;
+    sa.qR = (int)ctx->qR;
+    sa.q = ENSURE(double, q, vec_pad(m));
+    if (m > 0) {
+      if (profile == ALNNLS_PROFILE_FAST && syrk_dmma_supported(sa, 1)) {
+        if (int rc = dmma_buffers(ctx, sa)) return rc;
+        CK(launch_syrk_dmma(sa, 1, s));
+      } else {
+        if ((rc_sk = streamk_buffers(ctx, sa, 1))) return rc_sk;
+        CK(launch_syrk(sa, 1, s));
+      }
+      CK(launch_q_from_atb(sa, 1, s));
     }
-    CK(launch_q_from_atb(sa, 1, s));
-  }
+    return ALNNLS_OK;
+  };
+  if (int rc = gram(n)) return rc;
+  CK(cudaEventSynchronize(ctx->ev[5]));  // waits for the count, not for the Gram
+  const uint64_t m = (uint64_t)ctx->pin->hm;
+  if (m != n)
+    if (int rc = gram(m)) return rc;
   *m_out = m;
   ctx->have_setup = true;
   return ALNNLS_OK;

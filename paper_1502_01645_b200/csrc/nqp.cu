@@ -1199,6 +1199,16 @@ cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream
   // small m: the cluster loop with its state in distributed shared memory (small.cu)
   const cudaError_t e = launch_nqp_small(a, num_ctas, stream);
   if (e != cudaErrorNotSupported) return e;
+  if (a.zero_start) {  // x = 0, g = q (nqp.hpp:224-225), zeroed padding and barrier words
+    const size_t m = (size_t)a.m;
+    if (cudaError_t e2 = cudaMemsetAsync(a.gP, 0, sizeof(double) * (m + 8), stream)) return e2;
+    if (cudaError_t e2 = cudaMemsetAsync(a.dC, 0, sizeof(double) * (m + 8), stream)) return e2;
+    if (cudaError_t e2 = cudaMemsetAsync(a.x, 0, sizeof(double) * m, stream)) return e2;
+    if (cudaError_t e2 = cudaMemcpyAsync(a.g, a.q, sizeof(double) * m, cudaMemcpyDeviceToDevice,
+                                         stream))
+      return e2;
+    if (cudaError_t e2 = cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned int), stream)) return e2;
+  }
   return launch_loop(nqp_loop_kernel<true>, nqp_loop_kernel<false>, a, num_ctas, stream);
 }
 

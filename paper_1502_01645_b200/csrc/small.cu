@@ -241,9 +241,10 @@ __global__ void __launch_bounds__(kST, 1) nqp_small_kernel(LoopArgs a) {
     double2* dst = reinterpret_cast<double2*>(Qs);
     for (int e = tid; e < R * m / 2; e += blockDim.x) dst[e] = __ldg(src + e);
     for (int t = tid; t < nrows; t += blockDim.x) {
-      xl[t] = a.x[row0 + t];
-      gl[t] = a.g[row0 + t];
-      ql[t] = __ldg(a.q + row0 + t);
+      const double qi = __ldg(a.q + row0 + t);
+      xl[t] = a.zero_start ? 0.0 : a.x[row0 + t];  // x = 0, grad = q (nqp.hpp:224-225)
+      gl[t] = a.zero_start ? qi : a.g[row0 + t];
+      ql[t] = qi;
     }
   } else if (tid == 0) {
     a.ctrl->numeric_failure = 0;
