@@ -172,6 +172,18 @@ int alnnls_timer_start(alnnls_ctx* ctx);
 int alnnls_timer_stop(alnnls_ctx* ctx, double* seconds);
 /* Number of this library's kernels launched on the context so far. */
 uint64_t alnnls_launch_count(const alnnls_ctx* ctx);
+/* The device loop kernel of the last solve on the context (ALNNLS_LOOP_*): the
+ * general loop as a cooperative grid or as one thread-block cluster, the small-m
+ * cluster loop with its state in distributed shared memory (the environment
+ * variable ALNNLS_SMALL=0 disables it), the FAST one-pass loop, or 0 (none). */
+enum {
+  ALNNLS_LOOP_NONE = 0,
+  ALNNLS_LOOP_GRID = 1,
+  ALNNLS_LOOP_CLUSTER = 2,
+  ALNNLS_LOOP_SMALL = 3,
+  ALNNLS_LOOP_FAST = 4
+};
+int alnnls_last_loop_kernel(const alnnls_ctx* ctx);
 /* rescale bookkeeping of the last NNLS solve/setup (nnls.hpp:32-37). */
 int alnnls_get_scale(alnnls_ctx* ctx, double* scale, uint64_t cap);
 int alnnls_get_retained(alnnls_ctx* ctx, uint64_t* idx, uint64_t cap);

@@ -20,7 +20,7 @@ EXPORTS = [
     "alnnls_get_retained", "alnnls_get_dropped", "alnnls_setup", "alnnls_get_Q", "alnnls_get_q",
     "alnnls_rescale", "alnnls_gram", "alnnls_transpose_matvec", "alnnls_matvec",
     "alnnls_masked_matvec", "alnnls_solve_nnls_batched", "alnnls_solve_nnls_batched_device",
-    "alnnls_timer_start", "alnnls_timer_stop", "alnnls_launch_count",
+    "alnnls_timer_start", "alnnls_timer_stop", "alnnls_launch_count", "alnnls_last_loop_kernel",
     "alnnls_gram_tiles", "alnnls_gram_rowblock_device", "alnnls_atb_rowblock_device",
     "alnnls_solve_nnls_gram_device", "alnnls_residual_rowblock_device",
     "alnnls_gram_partial_device",
@@ -71,6 +71,7 @@ def load():
         "alnnls_timer_start": ([vp], i32),
         "alnnls_timer_stop": ([vp, C.POINTER(C.c_double)], i32),
         "alnnls_launch_count": ([vp], u64),
+        "alnnls_last_loop_kernel": ([vp], i32),
         "alnnls_get_scale": ([vp, vp, u64], i32),
         "alnnls_get_retained": ([vp, vp, u64], i32),
         "alnnls_get_dropped": ([vp, vp, u64], i32),

@@ -197,6 +197,11 @@ class Solver:
         """Number of this library's kernels launched on the context so far."""
         return int(self.lib.alnnls_launch_count(self.ctx))
 
+    def loop_kernel(self):
+        """Loop kernel of the last solve: "grid", "cluster", "small", "fast" or "none"."""
+        k = int(self.lib.alnnls_last_loop_kernel(self.ctx))
+        return {0: "none", 1: "grid", 2: "cluster", 3: "small", 4: "fast"}.get(k, str(k))
+
     def last_summary(self):
         return self._summary
 

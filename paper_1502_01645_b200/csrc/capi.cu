@@ -57,6 +57,7 @@ struct alnnls_ctx {
   int solver = 0;  // 0: solve_nqp loop; 1: accelerated baseline (set by the *_accelerated entries)
   unsigned long long phase_ns[8] = {};
   uint64_t launches = 0;
+  int loop_kernel = 0;  // ALNNLS_LOOP_* of the last solve
   cudaEvent_t timer[2] = {};
   // pinned host copies read after one stream sync (deferred NQP control block,
   // the residual), so a solve needs no host round trip between the loop and its finish
@@ -350,10 +351,11 @@ int run_nqp(alnnls_ctx* ctx, uint64_t m, const Resolved& r, const alnnls_config*
   CK(cudaEventRecord(ctx->ev[2], s));
   if (fast) {
     CK(launch_fast_loop(fa, s));
+    ctx->loop_kernel = ALNNLS_LOOP_FAST;
   } else if (solver == 1) {
-    CK(launch_acc_loop(a, nctas, s));
+    CK(launch_acc_loop(a, nctas, s, &ctx->loop_kernel));
   } else {
-    CK(launch_nqp_loop(a, nctas, s));
+    CK(launch_nqp_loop(a, nctas, s, &ctx->loop_kernel));
   }
   CK(cudaEventRecord(ctx->ev[3], s));
   if (!ctx->pin) CK(cudaMallocHost(&ctx->pin, sizeof(alnnls_ctx::Pinned)));
@@ -1103,6 +1105,7 @@ int alnnls_timer_stop(alnnls_ctx* ctx, double* seconds) {
 }
 
 uint64_t alnnls_launch_count(const alnnls_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int alnnls_last_loop_kernel(const alnnls_ctx* ctx) { return ctx ? ctx->loop_kernel : 0; }
 
 int alnnls_get_phase_ns(alnnls_ctx* ctx, uint64_t* ns, uint64_t cap) {
   if (!ctx || !ns) return ALNNLS_EINVAL;

@@ -89,14 +89,17 @@ struct LoopArgs {
 
 // Exact device-resident solve_nqp loop (nqp.hpp:249-334). One cooperative
 // launch for the whole solve; returns the launch status.
-cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream);
+// which (optional) <- the loop kernel launched (ALNNLS_LOOP_* in alnnls.h).
+cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream,
+                            int* which = nullptr);
 // Small-m variant (small.cu): one cluster, loop state in distributed shared memory.
 // cudaErrorNotSupported when the shape does not fit it (launch_nqp_loop then takes
 // the general kernel).
 bool nqp_small_fits(int m, int R, int num_ctas);
 cudaError_t launch_nqp_small(const LoopArgs& a, int num_ctas, cudaStream_t stream);
 // Accelerated (Nesterov) baseline loop (accelerated.hpp:21-117), same CTA layout.
-cudaError_t launch_acc_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream);
+cudaError_t launch_acc_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream,
+                            int* which = nullptr);
 // frobenius_norm of the blocked m x m Q (linalg.hpp:222-226): one ascending chain
 // over the column-major entries, then sqrt, into *out (one CTA).
 cudaError_t launch_frobenius(const double* Qb, int m, int R, double* out, cudaStream_t stream);

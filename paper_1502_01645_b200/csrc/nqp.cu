@@ -24,6 +24,7 @@
 // forms the rounded products in parallel into shared memory and one thread
 // runs the dependent DADD chain, so the trajectory is bitwise the reference's.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemv.cuh"
@@ -1162,8 +1163,8 @@ int nqp_rows_per_cta(int m, int sm_count) {
 // else a cooperative grid.
 template <class KC, class KG>
 cudaError_t launch_loop(KC kcluster, KG kgrid, const LoopArgs& a, int num_ctas,
-                        cudaStream_t stream, size_t smem_bytes = nqp_loop_smem_bytes(),
-                        int threads = kLoopThreads) {
+                        cudaStream_t stream, int* which = nullptr,
+                        size_t smem_bytes = nqp_loop_smem_bytes(), int threads = kLoopThreads) {
   // attributes are per device (func_attr_once keys them by the current device)
   if (cudaError_t e = smem_optin(kgrid, (int)smem_bytes)) return e;
   if (cudaError_t e = smem_optin(kcluster, (int)smem_bytes)) return e;
@@ -1186,19 +1187,29 @@ cudaError_t launch_loop(KC kcluster, KG kgrid, const LoopArgs& a, int num_ctas,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, kcluster, &cfg) == cudaSuccess && nclusters > 0)
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kcluster, &cfg) == cudaSuccess && nclusters > 0) {
+      if (which) *which = ALNNLS_LOOP_CLUSTER;
       return cudaLaunchKernelEx(&cfg, kcluster, args);
+    }
     (void)cudaGetLastError();  // no cluster of this size fits: cooperative grid instead
   }
+  if (which) *which = ALNNLS_LOOP_GRID;
   void* params[] = {&args};
   return cudaLaunchCooperativeKernel((void*)kgrid, dim3(num_ctas), dim3(threads), params,
                                      smem_bytes, stream);
 }
 
-cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream) {
-  // small m: the cluster loop with its state in distributed shared memory (small.cu)
-  const cudaError_t e = launch_nqp_small(a, num_ctas, stream);
-  if (e != cudaErrorNotSupported) return e;
+cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream, int* which) {
+  // small m: the cluster loop with its state in distributed shared memory (small.cu);
+  // ALNNLS_SMALL=0 in the environment forces the general kernel (A/B and parity tests)
+  const char* knob = getenv("ALNNLS_SMALL");
+  if (!(knob && knob[0] == '0')) {
+    const cudaError_t e = launch_nqp_small(a, num_ctas, stream);
+    if (e != cudaErrorNotSupported) {
+      if (which) *which = ALNNLS_LOOP_SMALL;
+      return e;
+    }
+  }
   if (a.zero_start) {  // x = 0, g = q (nqp.hpp:224-225), zeroed padding and barrier words
     const size_t m = (size_t)a.m;
     if (cudaError_t e2 = cudaMemsetAsync(a.gP, 0, sizeof(double) * (m + 8), stream)) return e2;
@@ -1209,7 +1220,7 @@ cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream
       return e2;
     if (cudaError_t e2 = cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned int), stream)) return e2;
   }
-  return launch_loop(nqp_loop_kernel<true>, nqp_loop_kernel<false>, a, num_ctas, stream);
+  return launch_loop(nqp_loop_kernel<true>, nqp_loop_kernel<false>, a, num_ctas, stream, which);
 }
 
 // ---- standalone masked GEMV (masked_matvec / matvec / residual / warm start) ------------
@@ -1283,8 +1294,8 @@ cudaError_t launch_masked_gemv_blocked(const double* Qb, int m, int R, const uin
 }  // namespace alnnls
 
 namespace alnnls {
-cudaError_t launch_acc_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream) {
-  return launch_loop(acc_loop_kernel<true>, acc_loop_kernel<false>, a, num_ctas, stream);
+cudaError_t launch_acc_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream, int* which) {
+  return launch_loop(acc_loop_kernel<true>, acc_loop_kernel<false>, a, num_ctas, stream, which);
 }
 
 cudaError_t launch_frobenius(const double* Qb, int m, int R, double* out, cudaStream_t stream) {
