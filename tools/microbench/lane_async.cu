@@ -5,6 +5,7 @@
 // so there is no cross-lane synchronisation at all. Checks bitwise agreement.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 #include "gemv.cuh"
 using namespace alnnls;
@@ -120,6 +121,87 @@ __global__ void __launch_bounds__(384, 1) k_lane(const double* Qb, int m, int R,
   if (lane < nrows) y[row0 + lane] = acc;
 }
 
+
+// L1-prefetch consumer: warps 1..P prefetch (prefetch.global.L1) the CTA's column
+// segments D columns ahead of the consumer's published position; warp 0 (the
+// consumer) reads Q with plain loads (L1 hits when the prefetch landed) -- no
+// mbarrier, no wait, no branch in its loop. Correctness does not depend on the
+// prefetch. The list and values are staged in shared memory first.
+template <int D, int P, int MODE>
+__global__ void __launch_bounds__(384, 1) k_pref(const double* Qb, int m, int R, const uint32_t* list,
+                                                const double* vals, int len, double* y) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint32_t* sl = reinterpret_cast<uint32_t*>(smem);
+  double* sv = reinterpret_cast<double*>(smem + (((size_t)len * 4 + 15) & ~15));
+  __shared__ volatile int progress;
+  const int row0 = blockIdx.x * R;
+  const int nrows = max(0, min(m - row0, R));
+  for (int e = threadIdx.x; e < len; e += blockDim.x) {
+    sl[e] = list[e];
+    sv[e] = vals[e];
+  }
+  if (threadIdx.x == 0) progress = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* qb = Qb + (size_t)blockIdx.x * R * m;
+  if (warp >= 1 && warp <= P) {
+    // prefetcher: columns [pos, progress + D), round-robin over the P warps in 32-column chunks
+    int next = (warp - 1) * 32;
+    while (next < len) {
+      while (next >= progress + D) { }
+      const int c = next + lane;
+      if (c < len) {
+        const char* a = reinterpret_cast<const char*>(qb + (size_t)sl[c] * R);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a + 128));
+        if (R * 8 > 256) asm volatile("prefetch.global.L1 [%0];" ::"l"(a + 256));
+      }
+      next += P * 32;
+    }
+    return;
+  }
+  if (warp != 0) return;
+  const int tt = lane < R ? lane : R - 1;
+  const double* q = qb + tt;
+  double acc = 0.0;
+  int s = 0;
+  if (MODE == 0) {  // products of 32 columns, then their chain
+    for (; s + 32 <= len; s += 32) {
+      double p[32];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) p[l] = xmul(__ldg(q + (size_t)sl[s + l] * R), sv[s + l]);
+#pragma unroll
+      for (int l = 0; l < 32; ++l) acc = xadd(acc, p[l]);
+      if (lane == 0) progress = s + 32;
+    }
+  } else {  // pipelined: products of the next 32 while the chain of these runs
+    double pa[32], pb[32];
+    if (len >= 64) {
+#pragma unroll
+      for (int l = 0; l < 32; ++l) pa[l] = xmul(__ldg(q + (size_t)sl[l] * R), sv[l]);
+      for (; s + 96 <= len; s += 64) {
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+          pb[l] = xmul(__ldg(q + (size_t)sl[s + 32 + l] * R), sv[s + 32 + l]);
+          acc = xadd(acc, pa[l]);
+        }
+        if (lane == 0) progress = s + 32;
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+          pa[l] = xmul(__ldg(q + (size_t)sl[s + 64 + l] * R), sv[s + 64 + l]);
+          acc = xadd(acc, pb[l]);
+        }
+        if (lane == 0) progress = s + 64;
+      }
+#pragma unroll
+      for (int l = 0; l < 32; ++l) acc = xadd(acc, pa[l]);
+      s += 32;
+    }
+  }
+  for (; s < len; ++s) acc = xmac(acc, __ldg(q + (size_t)sl[s] * R), sv[s]);
+  if (lane < nrows) y[row0 + lane] = acc;
+}
+
 template <class K>
 float run(K kern, size_t smem, int nb, const double* Q, int m, int R, const uint32_t* list,
           const double* vals, int L, double* y) {
@@ -177,6 +259,20 @@ int main() {
     for (int i = 0; i < m; ++i) bad += memcmp(&a[i], &b[i], 8) != 0;
     printf("%-22s %7.2f us  %6.2f cycles/col  mismatches %d\n", name, t, t * 1965.0 / L, bad);
   };
+  auto pref = [&](auto kern, const char* name) {
+    const size_t smem = (((size_t)L * 4 + 15) & ~15) + ((L + 1) & ~1) * 8;
+    const float t = run(kern, smem, nb, Q, m, R, list, vals, L, y1);
+    CK(cudaMemcpy(b.data(), y1, m * 8, cudaMemcpyDeviceToHost));
+    int bad = 0;
+    for (int i = 0; i < m; ++i) bad += memcmp(&a[i], &b[i], 8) != 0;
+    printf("%-22s %7.2f us  %6.2f cycles/col  mismatches %d\n", name, t, t * 1965.0 / L, bad);
+  };
+  pref(k_pref<256, 4, 0>, "pref D256 P4 m0");
+  pref(k_pref<512, 4, 0>, "pref D512 P4 m0");
+  pref(k_pref<1024, 4, 0>, "pref D1024 P4 m0");
+  pref(k_pref<512, 4, 1>, "pref D512 P4 m1");
+  pref(k_pref<1024, 8, 1>, "pref D1024 P8 m1");
+  pref(k_pref<0, 0, 0>, "no prefetch m0");
   lane(k_lane<16, 8, 0>, 16, 8, "lane G16 D8 m0");
   lane(k_lane<16, 16, 0>, 16, 16, "lane G16 D16 m0");
   lane(k_lane<16, 24, 0>, 16, 24, "lane G16 D24 m0");
