@@ -111,6 +111,24 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       : "memory");
 }
 
+// The same copy with an L2 cache policy (createpolicy): e.g. a fraction of the
+// source's lines evict_last, so that part stays in L2 for the next pass.
+__device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                              uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+// Fraction `frac` of the lines evict_last (the rest evict_first).
+__device__ __forceinline__ uint64_t l2_evict_last_fraction(float frac) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;"
+               : "=l"(pol) : "f"(frac));
+  return pol;
+}
+
 // ---- block scan (exclusive) of one int per thread -----------------------------
 // Returns the exclusive prefix; *total gets the block sum. Uses `scratch`
 // (>= 33 ints of shared memory). All threads of the block must call it.

@@ -68,6 +68,7 @@ struct RowRing {
   uint32_t pos;   // stages issued so far (identical in every thread)
   uint32_t smask; // S - 1 when S is a power of two (ALNNLS_POW2_STAGES), else 0
   uint32_t sshift;
+  uint64_t l2pol; // L2 policy of the matrix copies (0: none)
 };
 
 #ifndef ALNNLS_POW2_STAGES
@@ -133,6 +134,7 @@ __device__ inline void ring_setup(RowRing& r, uint8_t* smem, size_t bytes, int n
   r.data = reinterpret_cast<double*>(smem + hdr);
   r.vals = r.data + (size_t)S * G * seg;
   r.pos = 0;
+  r.l2pol = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&r.full[s], 1);
@@ -195,8 +197,12 @@ __device__ inline void gemv_rows(RowRing& r, const double* __restrict__ base, ui
             int end = later ? __ffs(later) - 1 : 32;
             end = min(end, cnt - l0);
             const int rl = end - lane;
-            bulk_g2s(dst + (size_t)l * seg, base + (size_t)j * col_stride,
-                     (uint32_t)(rl * seg * 8), &r.full[st]);
+            if (r.l2pol)
+              bulk_g2s_hint(dst + (size_t)l * seg, base + (size_t)j * col_stride,
+                            (uint32_t)(rl * seg * 8), &r.full[st], r.l2pol);
+            else
+              bulk_g2s(dst + (size_t)l * seg, base + (size_t)j * col_stride,
+                       (uint32_t)(rl * seg * 8), &r.full[st]);
           }
         } else if (valid) {
           bulk_g2s(dst + (size_t)l * seg, base + (size_t)j * col_stride, (uint32_t)seg * 8,

@@ -75,6 +75,7 @@ struct LoopArgs {
   unsigned int* bar;  // grid barrier words {count, generation}, zeroed before launch
   int rows_per_cta;
   int resident;     // row CTAs keep their Q panel in shared memory (small m, gemv_resident)
+  float l2_frac;    // ring copies of Q: this fraction of its lines L2 evict_last (0: no hint)
   int zero_start;   // x = 0, g = q not yet written: the loop launch initialises them
                     // (the small-m kernel in its prologue; launch_nqp_loop otherwise)
   // accelerated (Nesterov) solver only (accelerated.hpp:21-117)

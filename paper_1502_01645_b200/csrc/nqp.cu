@@ -614,6 +614,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
       __syncthreads();
     } else {
       ring_setup(ring, smem, kRingSmemBytes, nrows, R, kWarps);
+      if (a.l2_frac > 0.f) ring.l2pol = l2_evict_last_fraction(a.l2_frac);
     }
   }
   double* sbuf = reinterpret_cast<double*>(smem);
@@ -1210,6 +1211,20 @@ cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream
       return e;
     }
   }
+  // L2 residency hint for the ring's copies of Q when a sizable part of Q fits the
+  // L2 (c2 / c3: P1 and P2 of an iteration read mostly the same columns); env
+  // ALNNLS_L2_FRAC overrides (A/B; 0 disables)
+  LoopArgs b = a;
+  {
+    // measured at c2 / c3 (Q = 134 MB): fraction 0 84.6 / 97.1 us per iteration,
+    // 0.3-0.5 80.8 / 92.2, 0.7 81.7 / 94.8, 1.0 84.6
+    const double qbytes = 8.0 * (double)a.m * (double)a.m;
+    double f = 50e6 / qbytes;
+    if (f > 1.0) f = 1.0;
+    if (f < 0.25) f = 0.0;
+    if (const char* e = getenv("ALNNLS_L2_FRAC")) f = atof(e);
+    b.l2_frac = (float)f;
+  }
   if (a.zero_start) {  // x = 0, g = q (nqp.hpp:224-225), zeroed padding and barrier words
     const size_t m = (size_t)a.m;
     if (cudaError_t e2 = cudaMemsetAsync(a.gP, 0, sizeof(double) * (m + 8), stream)) return e2;
@@ -1220,7 +1235,7 @@ cudaError_t launch_nqp_loop(const LoopArgs& a, int num_ctas, cudaStream_t stream
       return e2;
     if (cudaError_t e2 = cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned int), stream)) return e2;
   }
-  return launch_loop(nqp_loop_kernel<true>, nqp_loop_kernel<false>, a, num_ctas, stream, which);
+  return launch_loop(nqp_loop_kernel<true>, nqp_loop_kernel<false>, b, num_ctas, stream, which);
 }
 
 // ---- standalone masked GEMV (masked_matvec / matvec / residual / warm start) ------------
