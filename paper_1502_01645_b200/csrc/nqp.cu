@@ -406,8 +406,34 @@ __device__ void row_count(const LoopArgs& a, RowShared& S, int blk, int row0, in
 
 // Speculative update of own rows (nqp.hpp:309-313): x_next = x with x[C] = cand,
 // g_next = g + gd; then row_count on the result.
+// Own range [t_lo, t_hi) of the ascending changed list, by ONE warp (an idle
+// warp of the P2 GEMV runs it while the GEMV streams Q): a 32-ary sample, then a
+// scan of the bucket holding each bound.
+__device__ void own_changed_range(const LoopArgs& a, RowShared& S, int row0, int nrows, int cl) {
+  const int lane = threadIdx.x & 31;
+  const int step = (cl + 31) / 32;
+  const int v = lane * step < cl ? (int)__ldcg(a.chg + lane * step) : 0x7fffffff;
+  const int c_lo = __popc(__ballot_sync(0xffffffffu, v < row0));
+  const int c_hi = __popc(__ballot_sync(0xffffffffu, v < row0 + nrows));
+  const int b_lo = max(0, c_lo - 1) * step, b_hi = max(0, c_hi - 1) * step;
+  int n_lo = 0, n_hi = 0;
+  for (int j0 = 0; j0 < step; j0 += 32) {
+    const int j = j0 + lane;
+    const int w1 = j < step && b_lo + j < cl ? (int)__ldcg(a.chg + b_lo + j) : 0x7fffffff;
+    const int w2 = j < step && b_hi + j < cl ? (int)__ldcg(a.chg + b_hi + j) : 0x7fffffff;
+    n_lo += __popc(__ballot_sync(0xffffffffu, w1 < row0));
+    n_hi += __popc(__ballot_sync(0xffffffffu, w2 < row0 + nrows));
+  }
+  if (lane == 0) {
+    S.t_lo = c_lo == 0 ? 0 : b_lo + n_lo;
+    S.t_hi = c_hi == 0 ? 0 : b_hi + n_hi;
+  }
+}
+
+// have_range: own_changed_range already ran (during the P2 GEMV).
 __device__ void row_apply(const LoopArgs& a, RowShared& S, int blk, int row0, int nrows,
-                          const double* xc, const double* gc, double* xn, double* gn, int cl) {
+                          const double* xc, const double* gc, double* xn, double* gn, int cl,
+                          bool have_range = false) {
   for (int t = threadIdx.x; t < nrows; t += blockDim.x) {
     const int i = row0 + t;
     gn[i] = xadd(gc[i], a.gd[i]);
@@ -415,7 +441,7 @@ __device__ void row_apply(const LoopArgs& a, RowShared& S, int blk, int row0, in
   }
   // own range [t_lo, t_hi) of the ascending changed list: a two-round
   // blockDim-ary search (two L2 round trips instead of a 2 log2(cl)-deep chain)
-  {
+  if (!have_range) {
     const int nt = blockDim.x;
     const int step = (cl + nt - 1) / nt;  // round 1 samples chg[0], chg[step], ...
     const int i = threadIdx.x * step;
@@ -867,15 +893,23 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
 
     // ===== P2, speculative update, next passive lists ====================================
     const int cl = __ldcg(&a.ctrl->chg_len);
+    // a warp the P2 GEMV leaves idle finds this CTA's slice of the changed list
+    const int idle_w = resident ? kWarps : ring.P + ring.cons_warps;
     if (!leader) {
-      if (resident) gemv_resident(Qs, R, s_list, s_vals, row0, nrows, a.chg, a.dC, cl, a.gd);
-      else gemv_rows(ring, qblk, R, true, row0, nrows, a.chg, a.dC, cl, a.gd);
+      if (resident) {
+        gemv_resident(Qs, R, s_list, s_vals, row0, nrows, a.chg, a.dC, cl, a.gd);
+      } else {
+        if ((int)(threadIdx.x >> 5) == idle_w) own_changed_range(a, RS, row0, nrows, cl);
+        gemv_rows(ring, qblk, R, true, row0, nrows, a.chg, a.dC, cl, a.gd);
+      }
     }
     // no grid barrier after P2: row_apply reads only its own rows of gd, and the
     // leader's df chain reads gdC only after B0
     __syncthreads();
     if (leader && threadIdx.x == 0) phase_mark(L, 4);
-    if (!leader) row_apply(a, RS, blk, row0, nrows, xb[xp], gb[xp], xb[xp ^ 1], gb[xp ^ 1], cl);
+    if (!leader)
+      row_apply(a, RS, blk, row0, nrows, xb[xp], gb[xp], xb[xp ^ 1], gb[xp ^ 1], cl,
+                idle_w < kWarps);
     grid.sync();  // B_cnt
     if (leader && threadIdx.x == 0) phase_mark(L, 5);
     if (!leader)
