@@ -29,6 +29,7 @@ struct LoopCtrl {
   int state2;       // phase-B decision: P2 / no move / stop
   int g_parity;     // which gradient buffer holds the maintained gradient
   unsigned int p1_done;  // row CTAs that finished P1 (monotonic within a launch)
+  unsigned int bc_epoch; // the vector CTA's phase-B results are published (pass number)
   unsigned long long phase_ns[8];  // accumulated leader-side phase times
 };
 

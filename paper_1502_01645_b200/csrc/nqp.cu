@@ -662,6 +662,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
     a.ctrl->numeric_failure = 0;
     a.ctrl->g_parity = 0;
     a.ctrl->p1_done = 0;
+    a.ctrl->bc_epoch = 0;
     L.best_gbs = __longlong_as_double(0x7ff0000000000000LL);  // +inf
     L.since_best = 0;
     L.t_mark = t0;
@@ -878,9 +879,23 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
         __threadfence();
       }
     }
-    grid.sync();  // B_C
+    // B_C: only the vector CTA's results flow here (act, the changed set), so the
+    // grid variant signals them one way (a release store the row CTAs poll) instead
+    // of a grid barrier; the cluster variant keeps its hardware barrier
+    if constexpr (kCluster) {
+      grid.sync();
+    } else if (leader) {
+      __threadfence();  // every vector-CTA thread's writes of the changed set
+      __syncthreads();
+      if (threadIdx.x == 0) st_release_u32(&a.ctrl->bc_epoch, npass);
+    } else {
+      if (threadIdx.x == 0)
+        while (ld_acquire_u32(&a.ctrl->bc_epoch) < npass) {
+        }
+      __syncthreads();
+    }
     if (!leader) {
-      act = __ldcg(&a.ctrl->act);  // after the grid barrier: L2 read, no sys-scope volatile
+      act = __ldcg(&a.ctrl->act);  // after the barrier: L2 read, no sys-scope volatile
       if (act == kActRollback) {
         xp ^= 1;
         lp ^= 1;
