@@ -125,6 +125,10 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src_gm
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// Bulk prefetch of a global range into L2 (no destination, no completion).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
+}
 // Fraction `frac` of the lines evict_last (the rest evict_first).
 __device__ __forceinline__ uint64_t l2_evict_last_fraction(float frac) {
   uint64_t pol;

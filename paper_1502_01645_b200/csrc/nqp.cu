@@ -40,6 +40,11 @@ namespace {
 #define ALNNLS_RESIDENT_Q 1  // build knob: Q panels resident in shared memory when they fit
 #endif
 
+#ifndef ALNNLS_P1_PREFETCH
+#define ALNNLS_P1_PREFETCH 384  // build knob: columns of the next P1 prefetched into L2 after P2
+                                // (c2 79.3 -> 78.7, c3 91.0 -> 90.3 us/iteration; 1536 slower)
+#endif
+
 #ifndef ALNNLS_CHAIN_CH
 #define ALNNLS_CHAIN_CH 1024  // build knob: vector-CTA chain chunk (products per buffer)
 #endif
@@ -916,6 +921,30 @@ __global__ void __launch_bounds__(kLoopThreads, 1) nqp_loop_kernel(LoopArgs a) {
       } else {
         if ((int)(threadIdx.x >> 5) == idle_w) own_changed_range(a, RS, row0, nrows, cl);
         gemv_rows(ring, qblk, R, true, row0, nrows, a.chg, a.dC, cl, a.gd);
+#if ALNNLS_P1_PREFETCH
+        // the next P1's first stages: its passive list is not built yet, but it is
+        // mostly this iteration's; prefetch this CTA's panel runs of the first
+        // columns of the current list into L2 while the barriers and lists run
+        if ((int)(threadIdx.x >> 5) < ring.P) {
+          const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+          const int npf = min(ml_l[lp], ALNNLS_P1_PREFETCH);
+          const uint32_t* lst = ls[lp].mask;
+          for (int l0 = w * 32; l0 < npf; l0 += ring.P * 32) {
+            const int l = l0 + lane;
+            const bool valid = l < npf;
+            const uint32_t j = valid ? __ldcg(lst + l) : 0u;
+            const uint32_t jp = __shfl_up_sync(0xffffffffu, j, 1);
+            const bool start = valid && (lane == 0 || j != jp + 1u);
+            const uint32_t starts = __ballot_sync(0xffffffffu, start);
+            if (start) {
+              const uint32_t later = starts & ~((2u << lane) - 1u);
+              int end = later ? __ffs(later) - 1 : 32;
+              end = min(end, npf - l0);
+              bulk_prefetch_l2(qblk + (size_t)j * R, (uint32_t)((end - lane) * R * 8));
+            }
+          }
+        }
+#endif
       }
     }
     // no grid barrier after P2: row_apply reads only its own rows of gd, and the
