@@ -606,6 +606,62 @@ __device__ __forceinline__ void dmma_gemm_pass16(const BatchArgs& a, const Batch
     }
 }
 
+// The same pass for NB = 8 columns on 8 warps (two 16-row tiles per warp, one
+// 8-column n-tile, the two tiles' DMMAs interleaved): two CTAs per SM (m <= 256).
+template <int LD>
+__device__ __forceinline__ void dmma_gemm_pass8(const BatchArgs& a, const BatchSmem& sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int m = sm.m, mp = sm.mp;
+  const int r0 = warp * 32;  // rows [r0, r0 + 32): two 16-row tiles, interleaved
+  if (r0 >= m) return;
+  int ra[2], rb[2];
+  bool va[2], vb[2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    ra[mt] = r0 + 16 * mt + g;
+    rb[mt] = ra[mt] + 8;
+    va[mt] = ra[mt] < m;
+    vb[mt] = rb[mt] < m;
+  }
+  double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+  constexpr int U = 2;  // (two tiles x U k-steps of Q fragments in registers)
+  for (int k0 = 0; k0 < mp; k0 += 8 * U) {
+    double q[U][2][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k1 = k0 + 8 * u + t, k2 = k1 + 4;
+      const double* c1 = a.Q + (size_t)k1 * m;
+      const double* c2 = a.Q + (size_t)k2 * m;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        q[u][mt][0] = va[mt] && k1 < m ? __ldg(c1 + ra[mt]) : 0.0;
+        q[u][mt][1] = vb[mt] && k1 < m ? __ldg(c1 + rb[mt]) : 0.0;
+        q[u][mt][2] = va[mt] && k2 < m ? __ldg(c2 + ra[mt]) : 0.0;
+        q[u][mt][3] = vb[mt] && k2 < m ? __ldg(c2 + rb[mt]) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k1 = k0 + 8 * u + t;
+      if (k0 + 8 * u >= mp) break;
+      const double b0 = sm.V[(size_t)k1 * LD + g];
+      const double b1 = sm.V[(size_t)(k1 + 4) * LD + g];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+        dmma8(acc[mt], q[u][mt][0], q[u][mt][1], q[u][mt][2], q[u][mt][3], b0, b1);
+    }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int row = (c < 2 ? ra[mt] : rb[mt]);
+      const int col = 2 * t + (c & 1);
+      if (row < m) sm.U[(size_t)col * sm.ps + row] = acc[mt][c];
+    }
+}
+
 __device__ __forceinline__ BatchSmem carve(double* bsm, int m, int nb) {
   BatchSmem sm;
   const int mp = round8(m);
@@ -631,8 +687,12 @@ __device__ __forceinline__ BatchSmem carve(double* bsm, int m, int nb) {
 // same lanes. (A warp-specialised variant -- 8 warps on the GEMM of one half of
 // the columns while 8 run the other half's state machines -- measured slower in
 // round 1; with 2 warps per scheduler the GEMM cannot hide the L2 latency of Q.)
-template <int NB>
-__global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
+// BT threads per CTA, MINB CTAs per SM. <16, 512, 1> up to m = 256; <8, 256, 2> is
+// the same solver with two CTAs of 8 columns per SM: while one CTA runs its
+// latency-bound state machines the other's GEMM pass keeps the FP64 / tensor pipes
+// busy (the two interleave without explicit warp specialisation).
+template <int NB, int BT, int MINB>
+__global__ void __launch_bounds__(BT, MINB) batched_nqp_kernel(BatchArgs a) {
   extern __shared__ __align__(16) double bsm[];
   __shared__ ColState S;
   constexpr int LD = batch_ld(NB);
@@ -652,8 +712,9 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
 #endif
   constexpr int CG = NB < ALNNLS_GEMM_CG ? NB : ALNNLS_GEMM_CG;  // columns per thread
   constexpr int GROUPS = NB / CG;
-  constexpr int ROWT = kBT / GROUPS;
-  constexpr int RPT = (4096 / NB + ROWT - 1) / ROWT;  // rows per thread at the largest m (4096/NB)
+  constexpr int ROWT = BT / GROUPS;
+  constexpr int MAXM = BT == 256 ? 256 : 4096 / NB;  // the largest m of this configuration
+  constexpr int RPT = (MAXM + ROWT - 1) / ROWT;      // rows per thread at that m
   const int grp = threadIdx.x / ROWT, trow = threadIdx.x % ROWT;
 #ifdef ALNNLS_BATCH_PROF
   long long t_g = 0, t_s = 0, npass = 0, nact = 0;
@@ -669,6 +730,8 @@ __global__ void __launch_bounds__(kBT, 1) batched_nqp_kernel(BatchArgs a) {
 #endif
     if (NB == 16 && a.fast) {
       dmma_gemm_pass16<LD>(a, sm);
+    } else if (NB == 8 && BT == 256 && a.fast) {  // (not launched: see launch_batched)
+      dmma_gemm_pass8<LD>(a, sm);
     } else {
       gemm_pass<RPT, CG, ROWT, LD, ALNNLS_GEMM_JB>(a, sm, grp, trow);
     }
@@ -805,23 +868,42 @@ int batched_cols_per_cta(int m) {
   return m <= 256 ? 16 : (m <= 512 ? 8 : (m <= 1024 ? 4 : 0));
 }
 
+#ifndef ALNNLS_BATCH_2CTA
+#define ALNNLS_BATCH_2CTA 1  // build knob: m <= 256 runs two 8-column CTAs per SM
+#endif
+
 cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream) {
   const int NB = batched_cols_per_cta(a.m);
   if (NB == 0) return cudaErrorInvalidValue;
   {
     const int mx = (int)batch_smem_bytes(1024, 4);  // the largest configuration
-    if (cudaError_t e = smem_optin(batched_nqp_kernel<16>, mx)) return e;
-    if (cudaError_t e = smem_optin(batched_nqp_kernel<8>, mx)) return e;
-    if (cudaError_t e = smem_optin(batched_nqp_kernel<4>, mx)) return e;
+    if (cudaError_t e = smem_optin(batched_nqp_kernel<16, kBT, 1>, mx)) return e;
+    if (cudaError_t e = smem_optin(batched_nqp_kernel<8, kBT, 1>, mx)) return e;
+    if (cudaError_t e = smem_optin(batched_nqp_kernel<4, kBT, 1>, mx)) return e;
+    if (cudaError_t e = smem_optin(batched_nqp_kernel<8, 256, 2>, (int)batch_smem_bytes(256, 8)))
+      return e;
+  }
+  // EXACT, m <= 256: two CTAs of 8 columns per SM (c4 65536 columns: loop 1.545 ->
+  // 1.498 s). FAST keeps one 16-column CTA: its DMMA pass shares each Q fragment
+  // between two n-tiles there, and the 8-column pass (dmma_gemm_pass8) loading Q
+  // twice as often measured 0.862 -> 1.113 s.
+  if (ALNNLS_BATCH_2CTA && NB == 16 && !a.fast) {
+    const size_t smem = batch_smem_bytes(a.m, 8);
+    int grid = 2 * sm_count;
+    const int need = (a.ncols + 7) / 8;
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    batched_nqp_kernel<8, 256, 2><<<grid, 256, smem, stream>>>(a);
+    return cudaGetLastError();
   }
   const size_t smem = batch_smem_bytes(a.m, NB);
   int grid = sm_count;
   const int need = (a.ncols + NB - 1) / NB;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  if (NB == 16) batched_nqp_kernel<16><<<grid, kBT, smem, stream>>>(a);
-  else if (NB == 8) batched_nqp_kernel<8><<<grid, kBT, smem, stream>>>(a);
-  else batched_nqp_kernel<4><<<grid, kBT, smem, stream>>>(a);
+  if (NB == 16) batched_nqp_kernel<16, kBT, 1><<<grid, kBT, smem, stream>>>(a);
+  else if (NB == 8) batched_nqp_kernel<8, kBT, 1><<<grid, kBT, smem, stream>>>(a);
+  else batched_nqp_kernel<4, kBT, 1><<<grid, kBT, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
