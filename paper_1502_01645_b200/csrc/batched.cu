@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_nqp_kernel(BatchArgs a) {
   constexpr int CG = NB < ALNNLS_GEMM_CG ? NB : ALNNLS_GEMM_CG;  // columns per thread
   constexpr int GROUPS = NB / CG;
   constexpr int ROWT = BT / GROUPS;
-  constexpr int MAXM = BT == 256 ? 256 : 4096 / NB;  // the largest m of this configuration
+  constexpr int MAXM = BT < 512 ? 256 : 4096 / NB;  // the largest m of this configuration
   constexpr int RPT = (MAXM + ROWT - 1) / ROWT;      // rows per thread at that m
   const int grp = threadIdx.x / ROWT, trow = threadIdx.x % ROWT;
 #ifdef ALNNLS_BATCH_PROF
