@@ -31,9 +31,18 @@ constexpr int BK = ALNNLS_SYRK_BK;  // k slab
 #define ALNNLS_SYRK_TC 4
 #endif
 constexpr int TC = ALNNLS_SYRK_TC;       // thread tile 8 rows x TC cols
-constexpr int NT = BM * BM / (8 * TC);  // TC=4: 512 threads (4 warps per scheduler)
-constexpr int TS = BM * BM;             // doubles of one tile's chain states ([8*TC][NT])
-constexpr int LDS = BM + 2;  // padded smem row (doubles): 16B-aligned rows, <=2-way store conflicts
+#ifndef ALNNLS_SYRK_HALF
+#define ALNNLS_SYRK_HALF 0  // build knob: a CTA takes half a tile (64 of its 128 rows), two CTAs
+                            // per SM (bitwise; c2 setup 9.25 -> 9.55 ms measured, so off)
+#endif
+constexpr int BMR = ALNNLS_SYRK_HALF ? BM / 2 : BM;  // rows of one piece of a tile
+constexpr int PPT = BM / BMR;                         // pieces per tile
+constexpr int NT = BMR * BM / (8 * TC);  // TC=4: 512 threads (4 warps per scheduler), 256 for halves
+constexpr int CPS = 512 / NT;            // CTAs per SM
+constexpr int TS = BM * BM;              // doubles of one tile's chain states
+constexpr int TSP = BMR * BM;            // ... of one piece's ([8*TC][NT])
+constexpr int LDS = BM + 2;   // padded smem row (doubles): 16B-aligned rows, <=2-way store conflicts
+constexpr int LDSA = BMR + 2; // the A operand's slab rows (a piece's rows)
 // thread tile 8 rows x TC cols: rows 2tx+(r&1)+32(r>>1), cols 2ty+(c&1)+(256/TC)(c>>1)
 // (each 16B shared load of a row pair is conflict-free across the 16 tx lanes)
 
@@ -50,7 +59,7 @@ __device__ __forceinline__ void tri_tile(int t, int& ti, int& tj) {
 #define ALNNLS_SYRK_STAGES 3
 #endif
 constexpr int kStages = ALNNLS_SYRK_STAGES;  // cp.async slab ring depth
-constexpr size_t kSyrkSmem = (size_t)kStages * 2 * BK * LDS * sizeof(double);
+constexpr size_t kSyrkSmem = (size_t)kStages * BK * (LDSA + LDS) * sizeof(double);
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
@@ -80,11 +89,13 @@ __device__ __forceinline__ void tile_of(const SetupArgs& s, int mode, int t, int
 // output is ONE chain over k ascending, bit for bit the same as one CTA doing
 // all slabs.
 __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double* smem, int ti, int tj,
-                                           int kb0, int kb1, const double* pin, double* pout) {
-  auto As = reinterpret_cast<double(*)[BK][LDS]>(smem);
-  auto Bs = reinterpret_cast<double(*)[BK][LDS]>(smem + kStages * BK * LDS);
-  const int i0 = ti * BM, j0 = tj * BM;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+                                           int piece, int kb0, int kb1, const double* pin,
+                                           double* pout) {
+  auto As = reinterpret_cast<double(*)[BK][LDSA]>(smem);
+  auto Bs = reinterpret_cast<double(*)[BK][LDS]>(smem + kStages * BK * LDSA);
+  const int i0 = ti * BM + piece * BMR, j0 = tj * BM;
+  constexpr int TXN = BMR / 8;  // thread columns of the row dimension
+  const int tx = threadIdx.x % TXN, ty = threadIdx.x / TXN;
   const double* Bop = mode == 2 ? s.B : s.A;
   const uint64_t ldb = mode == 2 ? s.ldb : s.lda;
   const int nb = mode == 2 ? s.nrhs : s.n;
@@ -92,25 +103,34 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
   // loader: element e = tid + r*NT (r < LPT) of a BK x BM slab: column e/BK, row k0 + e%BK.
   // Out-of-range elements are zero-filled (src-size 0): adding +0 to a chain is exact
   // (s + (+0) == s, and s is never -0).
-  constexpr int LPT = BK * BM / NT;
-  const double* pa[LPT];
-  const double* pb[LPT];
+  constexpr int LPTA = BK * BMR / NT, LPTB = BK * BM / NT;
+  const double* pa[LPTA];
+  const double* pb[LPTB];
 #pragma unroll
-  for (int r = 0; r < LPT; ++r) {
-    const int e = threadIdx.x + r * NT;
-    const int ca = i0 + e / BK, cb = j0 + e / BK;
+  for (int r = 0; r < LPTA; ++r) {
+    const int ca = i0 + (threadIdx.x + r * NT) / BK;
     pa[r] = ca < s.n ? s.A + (size_t)ca * s.lda : nullptr;
+  }
+#pragma unroll
+  for (int r = 0; r < LPTB; ++r) {
+    const int cb = j0 + (threadIdx.x + r * NT) / BK;
     pb[r] = cb < nb ? Bop + (size_t)cb * ldb : nullptr;
   }
   auto issue = [&](int kb) {
     const int buf = (kb - kb0) % kStages;
     const int k0 = kb * BK;
 #pragma unroll
-    for (int r = 0; r < LPT; ++r) {
+    for (int r = 0; r < LPTA; ++r) {
       const int e = threadIdx.x + r * NT;
       const int kk = e % BK, k = k0 + kk;
-      const bool va = pa[r] && k < s.d, vb = pb[r] && k < s.d;
+      const bool va = pa[r] && k < s.d;
       cp_async8(&As[buf][kk][e / BK], va ? pa[r] + k : s.A, va ? 8u : 0u);
+    }
+#pragma unroll
+    for (int r = 0; r < LPTB; ++r) {
+      const int e = threadIdx.x + r * NT;
+      const int kk = e % BK, k = k0 + kk;
+      const bool vb = pb[r] && k < s.d;
       cp_async8(&Bs[buf][kk][e / BK], vb ? pb[r] + k : s.A, vb ? 8u : 0u);
     }
   };
@@ -139,7 +159,7 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
       double a[8], b[TC];
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
-        const double2 v = *reinterpret_cast<const double2*>(&As[buf][kk][2 * tx + 32 * h]);
+        const double2 v = *reinterpret_cast<const double2*>(&As[buf][kk][2 * tx + (BMR / 4) * h]);
         a[2 * h] = v.x;
         a[2 * h + 1] = v.y;
       }
@@ -172,7 +192,7 @@ __device__ __forceinline__ void syrk_piece(const SetupArgs& s, int mode, double*
   // epilogue: upper triangle only, mirrored (exact symmetry, linalg.hpp:169-170)
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const int i = i0 + 2 * tx + (r & 1) + 32 * (r >> 1);
+    const int i = i0 + 2 * tx + (r & 1) + (BMR / 4) * (r >> 1);
 #pragma unroll
     for (int c = 0; c < TC; ++c) {
       const int j = j0 + 2 * ty + (c & 1) + (256 / TC) * (c >> 1);
@@ -291,11 +311,11 @@ __global__ void __launch_bounds__(ST) syrk_small_kernel(SetupArgs s, int mode) {
 }
 
 // One CTA per output tile.
-__global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode) {
+__global__ void __launch_bounds__(NT, CPS) syrk_exact_kernel(SetupArgs s, int mode) {
   extern __shared__ __align__(16) double syrk_sm[];
   int ti, tj;
-  tile_of(s, mode, blockIdx.x, ti, tj);
-  syrk_piece(s, mode, syrk_sm, ti, tj, 0, (s.d + BK - 1) / BK, nullptr, nullptr);
+  tile_of(s, mode, blockIdx.x / PPT, ti, tj);
+  syrk_piece(s, mode, syrk_sm, ti, tj, blockIdx.x % PPT, 0, (s.d + BK - 1) / BK, nullptr, nullptr);
 }
 
 // Stream-K: one persistent CTA per SM takes an equal contiguous share of the
@@ -305,26 +325,27 @@ __global__ void __launch_bounds__(NT, 1) syrk_exact_kernel(SetupArgs s, int mode
 // takes its leading partial tile LAST (acquire), so nobody waits in practice.
 // Requires every CTA's share to span at least two tiles (checked on the host)
 // and co-residency (cooperative launch).
-__global__ void __launch_bounds__(NT, 1) syrk_streamk_kernel(SetupArgs s, int mode, int tiles) {
+__global__ void __launch_bounds__(NT, CPS) syrk_streamk_kernel(SetupArgs s, int mode, int tiles) {
   extern __shared__ __align__(16) double syrk_sm[];
   const int nk = (s.d + BK - 1) / BK;
-  const long long total = (long long)tiles * nk;
+  // units: (piece, k slab); a tile is PPT pieces of BMR rows
+  const long long total = (long long)tiles * PPT * nk;
   const long long per = (total + gridDim.x - 1) / gridDim.x;
   const long long u0 = (long long)blockIdx.x * per;
   const long long u1 = min(total, u0 + per);
   if (u0 >= u1) return;
   const int t0 = (int)(u0 / nk), k0 = (int)(u0 % nk);
   const int t1 = (int)((u1 - 1) / nk), k1 = (int)((u1 - 1) % nk) + 1;
-  double* my_part = s.sk_part + (size_t)blockIdx.x * TS;
+  double* my_part = s.sk_part + (size_t)blockIdx.x * TSP;
   int ti, tj;
-  // tile chain states carried in from earlier row blocks / out to later ones
-  // (row-block continuation, s.tpin / s.tpout, [tiles][8*TC][NT]; nullptr: none)
-  auto tin = [&](int t) { return s.tpin ? s.tpin + (size_t)t * TS : nullptr; };
-  auto tout = [&](int t) { return s.tpout ? s.tpout + (size_t)t * TS : nullptr; };
-  // 1. trailing partial tile: slabs [0, k1) of t1, handed to the next CTA
+  // piece chain states carried in from earlier row blocks / out to later ones
+  // (row-block continuation, s.tpin / s.tpout, [tiles][PPT][8*TC][NT]; nullptr: none)
+  auto tin = [&](int p) { return s.tpin ? s.tpin + (size_t)p * TSP : nullptr; };
+  auto tout = [&](int p) { return s.tpout ? s.tpout + (size_t)p * TSP : nullptr; };
+  // 1. trailing partial piece: slabs [0, k1) of t1, handed to the next CTA
   if (k1 < nk) {
-    tile_of(s, mode, t1, ti, tj);
-    syrk_piece(s, mode, syrk_sm, ti, tj, 0, k1, tin(t1), my_part);
+    tile_of(s, mode, t1 / PPT, ti, tj);
+    syrk_piece(s, mode, syrk_sm, ti, tj, t1 % PPT, 0, k1, tin(t1), my_part);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -332,14 +353,14 @@ __global__ void __launch_bounds__(NT, 1) syrk_streamk_kernel(SetupArgs s, int mo
                    : "memory");
     }
   }
-  // 2. whole tiles
+  // 2. whole pieces
   const int full_lo = k0 == 0 ? t0 : t0 + 1;
   const int full_hi = k1 == nk ? t1 : t1 - 1;
   for (int t = full_lo; t <= full_hi; ++t) {
-    tile_of(s, mode, t, ti, tj);
-    syrk_piece(s, mode, syrk_sm, ti, tj, 0, nk, tin(t), tout(t));
+    tile_of(s, mode, t / PPT, ti, tj);
+    syrk_piece(s, mode, syrk_sm, ti, tj, t % PPT, 0, nk, tin(t), tout(t));
   }
-  // 3. leading partial tile: slabs [k0, nk) of t0, continuing CTA blockIdx-1's chains
+  // 3. leading partial piece: slabs [k0, nk) of t0, continuing CTA blockIdx-1's chains
   if (k0 > 0) {
     if (threadIdx.x == 0) {
       unsigned v = 0;
@@ -349,9 +370,9 @@ __global__ void __launch_bounds__(NT, 1) syrk_streamk_kernel(SetupArgs s, int mo
       } while (v == 0);
     }
     __syncthreads();
-    tile_of(s, mode, t0, ti, tj);
-    syrk_piece(s, mode, syrk_sm, ti, tj, k0, nk, s.sk_part + (size_t)(blockIdx.x - 1) * TS,
-               tout(t0));
+    tile_of(s, mode, t0 / PPT, ti, tj);
+    syrk_piece(s, mode, syrk_sm, ti, tj, t0 % PPT, k0, nk,
+               s.sk_part + (size_t)(blockIdx.x - 1) * TSP, tout(t0));
   }
 }
 // q_b = h(j_b) / D_b with h = -(A^T b) (nnls.hpp:79, :133-134); atb = A^T b.
@@ -677,14 +698,14 @@ cudaError_t launch_retained(const SetupArgs& s, cudaStream_t stream) {
 // the chains) and ending in `pout` (nullptr: finish, write H). The states of a
 // tile are the kernel's thread layout [8*TC][NT]; feeding the row blocks in order
 // is the reference's single ascending-k chain per entry.
-__global__ void __launch_bounds__(NT, 1) syrk_rowblock_kernel(SetupArgs s, int tile_lo,
-                                                              const double* pin, double* pout) {
+__global__ void __launch_bounds__(NT, CPS) syrk_rowblock_kernel(SetupArgs s, int tile_lo,
+                                                                const double* pin, double* pout) {
   extern __shared__ __align__(16) double syrk_sm[];
   int ti, tj;
-  tile_of(s, 0, tile_lo + (int)blockIdx.x, ti, tj);
-  const size_t off = (size_t)blockIdx.x * TS;
-  syrk_piece(s, 0, syrk_sm, ti, tj, 0, (s.d + BK - 1) / BK, pin ? pin + off : nullptr,
-             pout ? pout + off : nullptr);
+  tile_of(s, 0, tile_lo + (int)blockIdx.x / PPT, ti, tj);
+  const size_t off = (size_t)blockIdx.x * TSP;  // = (tile - tile_lo) * TS + piece * TSP
+  syrk_piece(s, 0, syrk_sm, ti, tj, (int)blockIdx.x % PPT, 0, (s.d + BK - 1) / BK,
+             pin ? pin + off : nullptr, pout ? pout + off : nullptr);
 }
 
 __global__ void diag_kernel(const double* H, int n, double* diag) {
@@ -709,8 +730,9 @@ int syrk_streamk_ctas(const SetupArgs& s, int mode, int sm_count) {
   const long long nk = (s.d + BK - 1) / BK;
   // stream-K only pays when the tile grid leaves a ragged last wave, and needs
   // every share to span >= 2 tiles (one partial tile at each end at most)
-  if (tiles < 2LL * sm_count || tiles % sm_count == 0 || nk < 2) return 0;
-  return sm_count;
+  const long long ctas = (long long)sm_count * CPS, pieces = tiles * PPT;
+  if (pieces < 2LL * ctas || pieces % ctas == 0 || nk < 2) return 0;
+  return (int)ctas;
 }
 
 cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream) {
@@ -733,7 +755,7 @@ cudaError_t launch_syrk(const SetupArgs& s, int mode, cudaStream_t stream) {
     syrk_small_kernel<<<nt32 * (nt32 + 1) / 2, ST, 0, stream>>>(s, mode);
     return cudaGetLastError();
   }
-  syrk_exact_kernel<<<tiles, NT, kSyrkSmem, stream>>>(s, mode);
+  syrk_exact_kernel<<<tiles * PPT, NT, kSyrkSmem, stream>>>(s, mode);
   return cudaGetLastError();
 }
 
@@ -845,7 +867,7 @@ cudaError_t launch_syrk_rowblock(const SetupArgs& s, int tile_lo, int ntiles, co
                                  double* pout, cudaStream_t stream) {
   if (ntiles <= 0) return cudaSuccess;
   if (cudaError_t e = smem_optin(syrk_rowblock_kernel, (int)kSyrkSmem)) return e;
-  syrk_rowblock_kernel<<<ntiles, NT, kSyrkSmem, stream>>>(s, tile_lo, pin, pout);
+  syrk_rowblock_kernel<<<ntiles * PPT, NT, kSyrkSmem, stream>>>(s, tile_lo, pin, pout);
   return cudaGetLastError();
 }
 cudaError_t launch_diag(const double* H, int n, double* diag, cudaStream_t stream) {
