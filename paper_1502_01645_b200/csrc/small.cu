@@ -276,7 +276,6 @@ __global__ void __launch_bounds__(kST, 1) nqp_small_kernel(LoopArgs a) {
   unsigned long long pk = 0, pmults = 0;
   double palpha = 0.0, pgbs = 0.0;
   int ptries = 0, pml = 0;
-  int np_own = 0;
 
   for (;;) {
     // ===== publish: own passive entries of the current state, pushed to every CTA ==========
@@ -300,7 +299,6 @@ __global__ void __launch_bounds__(kST, 1) nqp_small_kernel(LoopArgs a) {
         if (f) pidx[pos] = (uint32_t)tid;
       }
       __syncthreads();
-      np_own = total;
       const int sb = (rank - 1) * R;
       for (int e = tid; e < total * C; e += blockDim.x) {  // entry j to CTA d
         const int d = e / total, j = e - d * total;
@@ -579,7 +577,6 @@ __global__ void __launch_bounds__(kST, 1) nqp_small_kernel(LoopArgs a) {
     k = kstep + 1;
     lp ^= 1;
   }
-  (void)np_own;
   // ---- epilogue: the final iterate and gradient of own rows, the leader's counters ---------
   if (rank == 1 && tid == 0) a.ctrl->phase_ns[7] = s_ph[7];
   if (leader && tid == 0) {
