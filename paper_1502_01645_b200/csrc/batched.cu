@@ -404,6 +404,77 @@ __device__ void settle(const BatchArgs& a, ColState& S, const BatchSmem& sm, int
   }
 }
 
+// FAST, one warp per column (NB = 16 on 16 warps): the whole state machine of a
+// column after its GEMM pass stays inside its warp -- the den / df tree sum, the
+// decision on lane 0, then the column's settle rounds (elementwise work + tree
+// sums + decision) -- so no CTA barrier is needed until the next pass.
+__device__ void fast_warp_pass(const BatchArgs& a, ColState& S, const BatchSmem& sm) {
+  const int b = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = sm.m;
+  const int ph = S.phase[b];
+  if (ph != kIdle) {
+    const double* gb = sm.g(b);
+    const double* ub = sm.u(b);
+    double f = 0.0;
+    if (ph == kNeedP1) {
+#pragma unroll 4
+      for (int i = lane; i < m; i += 32) {
+        const double gbar = sm.v(i, b);
+        f += gbar != 0.0 ? xmul(gbar, ub[i]) : -0.0;
+      }
+    } else {
+#pragma unroll 4
+      for (int i = lane; i < m; i += 32) {
+        const double dd = sm.v(i, b);
+        f += dd != 0.0 ? xmul(xadd(gb[i], xmul(0.5, ub[i])), dd) : -0.0;
+      }
+    }
+    f = warp_tree(f);
+    if (lane == 0) {
+      if (ph == kNeedP1) {
+        if (!(f > 0.0)) {
+          S.term[b] = ALNNLS_ZERO_CURVATURE;
+          S.act[b] = kActFinish;
+        } else {
+          S.alpha[b] = xdiv(S.gbs[b], f);
+          S.tries[b] = 0;
+          S.mults[b] += (unsigned long long)m * (unsigned long long)S.ml[b];
+          S.act[b] = kActCand;
+        }
+      } else if (f <= 0.0 || S.tries[b] >= 60) {
+        S.act[b] = kActAccept;
+      } else {
+        S.alpha[b] = xmul(S.alpha[b], 0.5);  // nqp.hpp:317
+        ++S.tries[b];
+        S.act[b] = kActCand;
+      }
+      S.cnt[b] = 0;
+      S.bad[b] = 0;
+    }
+    __syncwarp();
+  }
+  for (;;) {
+    const int act = S.act[b];
+    if (act == kActNone) break;
+    round_elementwise(a, S, sm, 16);  // this warp's column (one warp per column)
+    __syncwarp();
+    if (lane == 0) {
+      if (act == kActAccept || act == kActMask || act == kActInit) {
+        S.res[b][0] = S.part[b][0][0];
+        S.res[b][1] = S.part[b][0][1];
+        S.res[b][2] = S.part[b][0][2];
+        if (act == kActAccept) ++S.k[b];
+      }
+      round_decide(a, S, b);
+      if (S.act[b] != kActNone) {
+        S.cnt[b] = 0;
+        S.bad[b] = 0;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // After a GEMM pass (U = Q V for every live column): the P1 columns' den terms
 // (exact_step, nqp.hpp:166-172) and the P2 columns' df terms (nqp.hpp:307) into
 // V, their chains, alpha / accept-or-halve (nqp.hpp:308-317), the settle rounds.
@@ -739,7 +810,15 @@ __global__ void __launch_bounds__(BT, MINB) batched_nqp_kernel(BatchArgs a) {
 #ifdef ALNNLS_BATCH_PROF
     const long long c1 = clock64();
 #endif
-    after_pass(a, S, sm, NB);  // ends with every thread past the last settle barrier
+#ifndef ALNNLS_FAST_WARP_STATE
+#define ALNNLS_FAST_WARP_STATE 1  // build knob: FAST state machines warp-local (NB = 16)
+#endif
+    if (ALNNLS_FAST_WARP_STATE && NB == 16 && BT == 512 && a.fast) {
+      fast_warp_pass(a, S, sm);
+      __syncthreads();  // every column's V is ready for the next pass
+    } else {
+      after_pass(a, S, sm, NB);  // ends with every thread past the last settle barrier
+    }
 #ifdef ALNNLS_BATCH_PROF
     const long long c2 = clock64();
     t_g += c1 - c0;
