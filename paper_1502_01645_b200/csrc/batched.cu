@@ -643,17 +643,37 @@ __device__ __forceinline__ void dmma_gemm_pass16(const BatchArgs& a, const Batch
   const bool va = ra < m, vb = rb < m;
   double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
   constexpr int U = 4;  // k-steps whose Q fragments load together
+  // Q in fragment order (a.Qf, see qfrag_kernel): a lane's 4 values of a k8 step are
+  // 32 contiguous bytes, a warp's 1 KB -- two 16-byte loads instead of four 8-byte
+  // gathers from four columns
+  const int ks_n = mp / 8;
+  const double2* qf = a.Qf ? reinterpret_cast<const double2*>(a.Qf) +
+                                 ((size_t)warp * ks_n * 32 + lane) * 2
+                           : nullptr;
   for (int k0 = 0; k0 < mp; k0 += 8 * U) {
     double q[U][4];
+    if (qf) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k1 = k0 + 8 * u + t, k2 = k1 + 4;
-      const double* c1 = a.Q + (size_t)k1 * m;
-      const double* c2 = a.Q + (size_t)k2 * m;
-      q[u][0] = va && k1 < m ? __ldg(c1 + ra) : 0.0;
-      q[u][1] = vb && k1 < m ? __ldg(c1 + rb) : 0.0;
-      q[u][2] = va && k2 < m ? __ldg(c2 + ra) : 0.0;
-      q[u][3] = vb && k2 < m ? __ldg(c2 + rb) : 0.0;
+      for (int u = 0; u < U; ++u) {
+        const int ks = k0 / 8 + u;
+        const double2 v0 = ks < ks_n ? __ldg(qf + (size_t)ks * 64) : make_double2(0.0, 0.0);
+        const double2 v1 = ks < ks_n ? __ldg(qf + (size_t)ks * 64 + 1) : make_double2(0.0, 0.0);
+        q[u][0] = v0.x;
+        q[u][1] = v0.y;
+        q[u][2] = v1.x;
+        q[u][3] = v1.y;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k1 = k0 + 8 * u + t, k2 = k1 + 4;
+        const double* c1 = a.Q + (size_t)k1 * m;
+        const double* c2 = a.Q + (size_t)k2 * m;
+        q[u][0] = va && k1 < m ? __ldg(c1 + ra) : 0.0;
+        q[u][1] = vb && k1 < m ? __ldg(c1 + rb) : 0.0;
+        q[u][2] = va && k2 < m ? __ldg(c2 + ra) : 0.0;
+        q[u][3] = vb && k2 < m ? __ldg(c2 + rb) : 0.0;
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -947,6 +967,25 @@ int batched_cols_per_cta(int m) {
   return m <= 256 ? 16 : (m <= 512 ? 8 : (m <= 1024 ? 4 : 0));
 }
 
+// Q (m x m, column-major) into the DMMA fragment order of dmma_gemm_pass16: for warp
+// w (rows 16w..16w+15), k8 step ks and lane (g = lane / 4, t = lane % 4) the four
+// values Q(16w+g, 8ks+t), Q(16w+g+8, 8ks+t), Q(16w+g, 8ks+t+4), Q(16w+g+8, 8ks+t+4),
+// zero outside m x m. Same values, same DMMA operands: the pass's result is unchanged.
+__global__ void qfrag_kernel(const double* Q, int m, int mp, double* Qf) {
+  const int ks_n = mp / 8;
+  const int total = 16 * ks_n * 32;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int lane = e & 31, ks = (e >> 5) % ks_n, w = (e >> 5) / ks_n;
+    const int g = lane >> 2, t = lane & 3;
+    const int ra = 16 * w + g, rb = ra + 8, k1 = 8 * ks + t, k2 = k1 + 4;
+    double* o = Qf + (size_t)e * 4;
+    o[0] = ra < m && k1 < m ? Q[(size_t)k1 * m + ra] : 0.0;
+    o[1] = rb < m && k1 < m ? Q[(size_t)k1 * m + rb] : 0.0;
+    o[2] = ra < m && k2 < m ? Q[(size_t)k2 * m + ra] : 0.0;
+    o[3] = rb < m && k2 < m ? Q[(size_t)k2 * m + rb] : 0.0;
+  }
+}
+
 #ifndef ALNNLS_BATCH_2CTA
 #define ALNNLS_BATCH_2CTA 1  // build knob: m <= 256 runs two 8-column CTAs per SM
 #endif
@@ -980,9 +1019,17 @@ cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream
   const int need = (a.ncols + NB - 1) / NB;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  if (NB == 16) batched_nqp_kernel<16, kBT, 1><<<grid, kBT, smem, stream>>>(a);
-  else if (NB == 8) batched_nqp_kernel<8, kBT, 1><<<grid, kBT, smem, stream>>>(a);
-  else batched_nqp_kernel<4, kBT, 1><<<grid, kBT, smem, stream>>>(a);
+  BatchArgs b = a;
+  if (NB == 16 && a.fast && a.Qf) {
+    const int mp = round8(a.m);
+    qfrag_kernel<<<64, 256, 0, stream>>>(a.Q, a.m, mp, a.Qf);
+    if (cudaError_t e = cudaGetLastError()) return e;
+  } else {
+    b.Qf = nullptr;
+  }
+  if (NB == 16) batched_nqp_kernel<16, kBT, 1><<<grid, kBT, smem, stream>>>(b);
+  else if (NB == 8) batched_nqp_kernel<8, kBT, 1><<<grid, kBT, smem, stream>>>(b);
+  else batched_nqp_kernel<4, kBT, 1><<<grid, kBT, smem, stream>>>(b);
   return cudaGetLastError();
 }
 

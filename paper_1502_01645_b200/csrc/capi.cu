@@ -44,7 +44,7 @@ struct alnnls_ctx {
   DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
       hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb, uP, gdC, skp, skf,
       ay, axn, aw, avy, apc, tst, fgb0, fgb1, fpart, fden, fkl, fkv, fkc, dmws, dmfl, nvt,
-      nht, nwt, nv, nw, nh;
+      nht, nwt, nv, nw, nh, qfrag;
 
   // last solve
   bool last_nnls = false;
@@ -878,7 +878,7 @@ void alnnls_destroy(alnnls_ctx* ctx) {
                     &ctx->avy,    &ctx->apc,   &ctx->tst,   &ctx->fgb0,  &ctx->fgb1,
                     &ctx->fpart,  &ctx->fden,  &ctx->fkl,   &ctx->fkv,   &ctx->fkc,
                     &ctx->dmws,   &ctx->dmfl,  &ctx->nvt,   &ctx->nht,   &ctx->nwt,
-                    &ctx->nv,     &ctx->nw,    &ctx->nh};
+                    &ctx->nv,     &ctx->nw,    &ctx->nh,    &ctx->qfrag};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
@@ -1384,6 +1384,12 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
     ba.stall_window = cfg->stall_window;
     ba.next_col = counter;
     ba.fast = cfg->profile == ALNNLS_PROFILE_FAST;
+    // FAST, m <= 256: Q re-laid in DMMA fragment order for the tensor-core passes
+    ba.Qf = nullptr;
+    if (ba.fast && m <= 256) {
+      double* qf = ENSURE(double, qfrag, (size_t)((m + 15) & ~15) * 256);
+      ba.Qf = qf;
+    }
     CK(cudaEventRecord(ctx->ev[2], s));
     CK(launch_batched(ba, ctx->sm_count, s));
     CK(cudaEventRecord(ctx->ev[3], s));

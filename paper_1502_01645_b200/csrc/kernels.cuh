@@ -283,6 +283,7 @@ struct BatchArgs {
   uint64_t stall_window;
   int* next_col;       // work counter (zeroed before the launch)
   int fast;            // FAST profile: the Q V passes on the fp64 tensor cores (DMMA)
+  double* Qf;          // FAST, m <= 256: scratch of m_pad^2 doubles for Q in DMMA fragment order
 };
 cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream);
 int batched_cols_per_cta(int m);  // 0 when m is too large for the batched kernel
