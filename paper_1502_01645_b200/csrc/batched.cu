@@ -642,7 +642,10 @@ __device__ __forceinline__ void dmma_gemm_pass16(const BatchArgs& a, const Batch
   const int ra = r0 + g, rb = r0 + g + 8;
   const bool va = ra < m, vb = rb < m;
   double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-  constexpr int U = 4;  // k-steps whose Q fragments load together
+#ifndef ALNNLS_DMMA_U
+#define ALNNLS_DMMA_U 4
+#endif
+  constexpr int U = ALNNLS_DMMA_U;  // k-steps whose Q fragments load together (build knob)
   // Q in fragment order (a.Qf, see qfrag_kernel): a lane's 4 values of a k8 step are
   // 32 contiguous bytes, a warp's 1 KB -- two 16-byte loads instead of four 8-byte
   // gathers from four columns
