@@ -16,6 +16,7 @@
 //  - unscale + residual: x = y / D; ||A x - b||^2 with one ordered chain per
 //    column over the rows (nnls.hpp:87-96, :115-123).
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -107,28 +108,26 @@ size_t batch_smem_bytes(int m, int nb) {
 // starts at +0 never becomes -0), so each lane runs pure dependent DADDs, and
 // one DADD instruction advances every column's chain (the FP64 pipe is not
 // spent on one useful lane per instruction). The three stop-test sums of a
-// column run on three lanes (warp 0 lanes b and 16 + b, warp 1 lane b).
-//   lane_sum: one sum of n terms p[t * stride] (squared first when sq: the
-//   g_bar^2 terms of gbs from V = g_bar). Two register blocks of 16 alternate,
-//   so the loads of the next block are in flight during the current block's
-//   chain and the dependent DADD is the per-term cost.
-// Term of a lane's sum: the value, or its square (g_bar^2; g_bar = +0 off the mask
-// gives +0, which leaves the chain unchanged just like the reference's skipped
-// term). Branch-free (x * 1 is exact), so lanes with and without squares share
-// one instruction stream.
-__device__ __forceinline__ double lane_term(double v, bool sq) { return xmul(v, sq ? v : 1.0); }
-__device__ __forceinline__ double lane_sum(const double* __restrict__ p, int stride, bool sq,
-                                           int n) {
+// column run on three lanes (warp 0 lanes b and 16 + b; warp 1 lane b).
+// lane_sum<false>: the terms are p[t * stride] as stored. Two register blocks of 16
+// alternate, so the loads of the next block are in flight during the current block's
+// chain and the dependent DADD (8 cycles) is the per-term cost.
+// lane_sum<true>: the terms are the squares (g_bar^2; g_bar = +0 off the mask gives +0,
+// which leaves the chain unchanged just like the reference's skipped term). (A three-
+// block rotation that squares block t + 1 between the DADDs of block t measured slower.)
+template <bool SQ>
+__device__ __forceinline__ double lane_sum(const double* __restrict__ p, int stride, int n) {
   constexpr int B = 16;
   double s = 0.0;
   int t = 0;
+  auto term = [](double v) { return SQ ? xmul(v, v) : v; };
   auto load = [&](double (&r)[B], int at) {
 #pragma unroll
     for (int e = 0; e < B; ++e) r[e] = p[(at + e) * stride];
   };
   auto run = [&](const double (&r)[B]) {
 #pragma unroll
-    for (int e = 0; e < B; ++e) s = xadd(s, lane_term(r[e], sq));
+    for (int e = 0; e < B; ++e) s = xadd(s, term(r[e]));
   };
   if (n >= 2 * B) {
     double ra[B], rb[B];
@@ -149,7 +148,7 @@ __device__ __forceinline__ double lane_sum(const double* __restrict__ p, int str
       t += B;
     }
   }
-  for (; t < n; ++t) s = xadd(s, lane_term(p[t * stride], sq));
+  for (; t < n; ++t) s = xadd(s, term(p[t * stride]));
   return s;
 }
 // FAST profile: a column's sums as fixed trees instead of the reference's
@@ -170,26 +169,41 @@ __device__ __forceinline__ double fast_parts(const ColState& S, int b, int k, in
 // Elementwise phases: warp w works on column w / wpc (wpc = warps per column),
 // its lanes on rows sub*32 + lane, sub*32 + lane + 32*wpc, ...
 struct ColWarp {
-  int b, i0, step, sub;
+  int b, i0, step, sub, bstep;
 };
+// With fewer warps than columns (NB = 8 on 4 warps) warp w takes columns w, w + nw, ...
+// whole (bstep = nw); otherwise one column per warp (bstep = NB ends the loop).
 __device__ __forceinline__ ColWarp col_warp(int NB) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  const int wpc = nw / NB;  // NB divides the warp count (16, 8 or 4 columns, 16 warps)
   ColWarp w;
+  if (nw < NB) {
+    w.b = warp;
+    w.sub = 0;
+    w.i0 = lane;
+    w.step = 32;
+    w.bstep = nw;
+    return w;
+  }
+  const int wpc = nw / NB;  // NB divides the warp count (16, 8 or 4 columns, 16 or 8 warps)
   w.b = warp / wpc;
   w.sub = warp - w.b * wpc;
   w.i0 = w.sub * 32 + lane;
   w.step = 32 * wpc;
+  w.bstep = NB;
   return w;
+}
+__device__ __forceinline__ int warps_per_col(int NB) {
+  const int nw = blockDim.x >> 5;
+  return nw < NB ? 1 : nw / NB;
 }
 
 // Elementwise work of one settle round. Writes V = g_bar and the stop-test terms
 // (U: x g, C: x q; -0 for the terms the reference skips) for the columns about
 // to run a stop test, C = cand and V = delta for a candidate step.
-__device__ void round_elementwise(const BatchArgs& a, ColState& S, const BatchSmem& sm, int NB) {
-  const ColWarp w = col_warp(NB);
-  const int b = w.b, m = sm.m;
+__device__ void round_elementwise_col(const BatchArgs& a, ColState& S, const BatchSmem& sm,
+                                      const ColWarp& w, int b) {
+  const int m = sm.m;
   const int act = S.act[b];
   if (act == kActNone) return;
   double* xb = sm.x(b);
@@ -278,6 +292,10 @@ __device__ void round_elementwise(const BatchArgs& a, ColState& S, const BatchSm
     if (cnt) atomicAdd(S.cnt + b, cnt);
     if (bad) S.bad[b] = 1;
   }
+}
+__device__ void round_elementwise(const BatchArgs& a, ColState& S, const BatchSmem& sm, int NB) {
+  const ColWarp w = col_warp(NB);
+  for (int b = w.b; b < NB; b += w.bstep) round_elementwise_col(a, S, sm, w, b);
 }
 
 // One column's stop test after its stop-test chains (nqp.hpp:251-275). Lane
@@ -375,17 +393,18 @@ __device__ void settle(const BatchArgs& a, ColState& S, const BatchSmem& sm, int
 #ifdef ALNNLS_BATCH_PROF
     if (threadIdx.x == 0) S.pr[5]++;
 #endif
-    // the stop-test sums: chain k of column b on lane 32 * (k / 2) + 16 * (k % 2) + b
+    // the stop-test sums of column b: x.g and q.x on warp 0 lanes b and 16 + b, gbs
+    // (the squares of g_bar) on warp 1 lane b (each warp runs one instruction stream)
     if (warp < 2) {
-      const int k = 2 * warp + (lane >> 4), b = lane & 15;
+      const int k = warp == 0 ? (lane < 16 ? 1 : 2) : (lane < 16 ? 0 : 3), b = lane & 15;
       if (k < 3 && b < NB) {
         const int act = S.act[b];
         if (act == kActAccept || act == kActMask || act == kActInit) {
           if (a.fast) {
-            S.res[b][k] = fast_parts(S, b, k, (int)(blockDim.x >> 5) / NB);
+            S.res[b][k] = fast_parts(S, b, k, warps_per_col(NB));
           } else {
-            const double* p = k == 0 ? sm.V + b : (k == 1 ? sm.u(b) : sm.c(b));
-            S.res[b][k] = lane_sum(p, k == 0 ? sm.ld : 1, k == 0, sm.m);
+            S.res[b][k] = k == 0 ? lane_sum<true>(sm.V + b, sm.ld, sm.m)
+                                 : lane_sum<false>(k == 1 ? sm.u(b) : sm.c(b), 1, sm.m);
           }
         }
       }
@@ -484,9 +503,8 @@ __device__ void after_pass(const BatchArgs& a, ColState& S, const BatchSmem& sm,
 #ifdef ALNNLS_BATCH_PROF
   long long t0 = clock64();
 #endif
-  {
-    const ColWarp w = col_warp(NB);
-    const int b = w.b;
+  const ColWarp w = col_warp(NB);
+  for (int b = w.b; b < NB; b += w.bstep) {
     const int ph = S.phase[b];
     const double* xb = sm.x(b);
     const double* gb = sm.g(b);
@@ -523,8 +541,8 @@ __device__ void after_pass(const BatchArgs& a, ColState& S, const BatchSmem& sm,
     const int b = lane;
     const int ph = S.phase[b];
     if (ph != kIdle) {
-      const double s = a.fast ? fast_parts(S, b, 0, (int)(blockDim.x >> 5) / NB)
-                              : lane_sum(sm.V + b, sm.ld, false, m);
+      const double s = a.fast ? fast_parts(S, b, 0, warps_per_col(NB))
+                              : lane_sum<false>(sm.V + b, sm.ld, m);
       if (ph == kNeedP1) {
         if (!(s > 0.0)) {
           S.term[b] = ALNNLS_ZERO_CURVATURE;
@@ -659,8 +677,13 @@ __device__ __forceinline__ void dmma_gemm_pass16(const BatchArgs& a, const Batch
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int ks = k0 / 8 + u;
-        const double2 v0 = ks < ks_n ? __ldg(qf + (size_t)ks * 64) : make_double2(0.0, 0.0);
-        const double2 v1 = ks < ks_n ? __ldg(qf + (size_t)ks * 64 + 1) : make_double2(0.0, 0.0);
+#ifdef ALNNLS_EXP_QFL1  // timing probe only: Q fragments from an L1-resident slice
+        const int kl = ks & 3;
+#else
+        const int kl = ks;
+#endif
+        const double2 v0 = ks < ks_n ? __ldg(qf + (size_t)kl * 64) : make_double2(0.0, 0.0);
+        const double2 v1 = ks < ks_n ? __ldg(qf + (size_t)kl * 64 + 1) : make_double2(0.0, 0.0);
         q[u][0] = v0.x;
         q[u][1] = v0.y;
         q[u][2] = v1.x;
@@ -838,6 +861,9 @@ __global__ void __launch_bounds__(BT, MINB) batched_nqp_kernel(BatchArgs a) {
 #endif
     if (ALNNLS_FAST_WARP_STATE && NB == 16 && BT == 512 && a.fast) {
       fast_warp_pass(a, S, sm);
+#ifdef ALNNLS_BATCH_PROF
+      if (threadIdx.x == 0) S.pr[0] += clock64() - c1;  // warp 0's own state machine
+#endif
       __syncthreads();  // every column's V is ready for the next pass
     } else {
       after_pass(a, S, sm, NB);  // ends with every thread past the last settle barrier
@@ -849,6 +875,14 @@ __global__ void __launch_bounds__(BT, MINB) batched_nqp_kernel(BatchArgs a) {
 #endif
   }
 #ifdef ALNNLS_BATCH_PROF
+#ifdef ALNNLS_BATCH_PROF_ALL
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    printf("allcta %d sm %u passes %lld gemm %.1f state %.1f act %.2f end %lld\n", blockIdx.x, smid, npass,
+           t_g / 1e3 / npass, t_s / 1e3 / npass, (double)nact / npass, clock64());
+  }
+#endif
   if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
     printf("batched prof cta %d: passes %lld, gemm %.1f kcyc/pass, state %.1f kcyc/pass, active cols/pass %.2f\n",
            blockIdx.x, npass, t_g / 1e3 / npass, t_s / 1e3 / npass, (double)nact / npass);
@@ -856,6 +890,330 @@ __global__ void __launch_bounds__(BT, MINB) batched_nqp_kernel(BatchArgs a) {
     printf("  cta %d per pass (kcyc): elem0 %.2f chain1 %.2f | rounds/pass %.2f: sync+check %.2f elem %.2f chain+decide %.2f\n",
            blockIdx.x, S.pr[0] / 1e3 / npass, S.pr[1] / 1e3 / npass, (double)S.pr[5] / npass,
            S.pr[2] / 1e3 / npass, S.pr[3] / 1e3 / npass, S.pr[4] / 1e3 / npass);
+#endif
+}
+
+
+// ---------------------------------------------------------------------------------
+// FAST, m <= 256: two CTAs of 16 columns per SM (batched_fast_kernel). One CTA's
+// latency-bound state machines run while the other's DMMA pass keeps the tensor pipe
+// busy. To fit two CTAs the per-column state is three vectors instead of six:
+//  - VU (row-major mp x kFLD): the pass's input V, overwritten by its output U once
+//    every warp has finished reading V; the state machine recomputes what V held
+//    (g_bar from the mask, delta from alpha) with the arithmetic that produced it;
+//  - X, G column panels; the candidate is recomputed at the accept (same operations,
+//    same bits) and q comes from global memory (L2) at each stop test.
+// Same sums, same trees, same decisions as the one-CTA FAST kernel: identical results.
+constexpr int kFLD = 18;   // VU row stride (16 columns + 2: the column walks share banks 4-way)
+
+struct FastSmem {
+  double* VU;
+  double* X;
+  double* G;
+  int m, mp, ps;
+  __device__ double& vu(int i, int b) const { return VU[i * kFLD + b]; }
+};
+size_t fast_smem_bytes(int m) {
+  return ((size_t)round8(m) * kFLD + 2 * (size_t)panel_stride(m) * 16) * sizeof(double);
+}
+
+// Candidate step of row i (nqp.hpp:294-303): delta (0 when the entry does not move)
+// and the candidate value.
+__device__ __forceinline__ void fast_cand(double alpha, double xi, double gi, double& c, double& d) {
+  c = xi;
+  d = 0.0;
+  if (xi > 0.0 || gi < 0.0) {
+    double t = xsub(xi, xmul(alpha, gi));
+    if (t < 0.0) t = 0.0;
+    if (t != xi) {
+      c = t;
+      d = xsub(t, xi);
+    }
+  }
+}
+
+// One column's state machine after a pass (or its first settle when !after), on one warp.
+__device__ void fast_col(const BatchArgs& a, ColState& S, const FastSmem& sm, int b, bool after) {
+  const int lane = threadIdx.x & 31;
+  const int m = sm.m;
+#ifdef ALNNLS_BATCH_PROF
+  long long t0 = clock64();
+#define FPROF(k) { const long long t1 = clock64(); if (threadIdx.x == 0) S.pr[k] += t1 - t0; t0 = t1; }
+#else
+#define FPROF(k)
+#endif
+  double* xb = sm.X + (size_t)b * sm.ps;
+  double* gb = sm.G + (size_t)b * sm.ps;
+  if (after) {
+    const int ph = S.phase[b];
+    if (ph != kIdle) {
+      double f = 0.0;
+      if (ph == kNeedP1) {  // den = g_bar . (Q g_bar)
+#pragma unroll 4
+        for (int i = lane; i < m; i += 32) {
+          const double xi = xb[i], gi = gb[i];
+          const double gbar = (xi > 0.0 || gi < 0.0) ? gi : 0.0;
+          f += gbar != 0.0 ? xmul(gbar, sm.vu(i, b)) : -0.0;
+        }
+      } else {  // df = (g + 0.5 Q delta) . delta (nqp.hpp:307)
+        const double alpha = S.alpha[b];
+#pragma unroll 4
+        for (int i = lane; i < m; i += 32) {
+          const double gi = gb[i];
+          double c, dd;
+          fast_cand(alpha, xb[i], gi, c, dd);
+          f += dd != 0.0 ? xmul(xadd(gi, xmul(0.5, sm.vu(i, b))), dd) : -0.0;
+        }
+      }
+      FPROF(0)
+      f = warp_tree(f);
+      FPROF(1)
+      if (lane == 0) {
+        if (ph == kNeedP1) {
+          if (!(f > 0.0)) {
+            S.term[b] = ALNNLS_ZERO_CURVATURE;
+            S.act[b] = kActFinish;
+          } else {
+            S.alpha[b] = xdiv(S.gbs[b], f);
+            S.tries[b] = 0;
+            S.mults[b] += (unsigned long long)m * (unsigned long long)S.ml[b];
+            S.act[b] = kActCand;
+          }
+        } else if (f <= 0.0 || S.tries[b] >= 60) {
+          S.act[b] = kActAccept;
+        } else {
+          S.alpha[b] = xmul(S.alpha[b], 0.5);  // nqp.hpp:317
+          ++S.tries[b];
+          S.act[b] = kActCand;
+        }
+        S.cnt[b] = 0;
+        S.bad[b] = 0;
+      }
+      __syncwarp();
+      FPROF(2)
+    }
+  }
+  for (;;) {
+    const int act = S.act[b];
+    if (act == kActNone) break;
+#ifdef ALNNLS_BATCH_PROF
+    t0 = clock64();
+#endif
+    int cnt = 0, bad = 0;
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+    if (act == kActCand) {
+      const double alpha = S.alpha[b];
+#pragma unroll 4
+      for (int i = lane; i < m; i += 32) {
+        double c, d;
+        fast_cand(alpha, xb[i], gb[i], c, d);
+        cnt += d != 0.0;
+        sm.vu(i, b) = d;
+      }
+      FPROF(3)
+    } else if (act == kActAccept || act == kActMask || act == kActInit) {
+      const double* qg = a.QB + (size_t)S.col[b] * m;
+      const double alpha = S.alpha[b];
+#pragma unroll 4
+      for (int i = lane; i < m; i += 32) {
+        const double qi = __ldg(qg + i);
+        double xi, gi;
+        if (act == kActAccept) {  // nqp.hpp:309-313
+          const double go = gb[i];
+          double d;
+          fast_cand(alpha, xb[i], go, xi, d);
+          gi = xadd(go, sm.vu(i, b));
+          xb[i] = xi;
+          gb[i] = gi;
+        } else if (act == kActInit) {  // x = 0, grad = q (nqp.hpp:224-225)
+          xi = 0.0;
+          gi = qi;
+          xb[i] = xi;
+          gb[i] = gi;
+        } else {
+          xi = xb[i];
+          gi = gb[i];
+        }
+        const bool p = xi > 0.0 || gi < 0.0;
+        cnt += p;
+        if (!isfinite(gi)) bad = 1;
+        const double gbar = p ? gi : 0.0;
+        sm.vu(i, b) = gbar;
+        const bool xnz = xi != 0.0;
+        f0 += xmul(gbar, gbar);
+        f1 += xnz ? xmul(xi, gi) : -0.0;
+        f2 += xnz ? xmul(xi, qi) : -0.0;
+      }
+      FPROF(4)
+      f0 = warp_tree(f0);
+      f1 = warp_tree(f1);
+      f2 = warp_tree(f2);
+      FPROF(5)
+    } else {  // kActFinish / kActGrab
+      if (act == kActFinish)
+        for (int i = lane; i < m; i += 32) a.Y[(size_t)S.col[b] * m + i] = xb[i];
+      for (int i = lane; i < m; i += 32) sm.vu(i, b) = 0.0;  // idle slots feed zeros
+    }
+#ifdef ALNNLS_BATCH_PROF
+    t0 = clock64();
+#endif
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      S.cnt[b] = cnt;
+      if (bad) S.bad[b] = 1;
+      if (act == kActAccept || act == kActMask || act == kActInit) {
+        S.res[b][0] = f0;
+        S.res[b][1] = f1;
+        S.res[b][2] = f2;
+        if (act == kActAccept) ++S.k[b];
+      }
+      round_decide(a, S, b);
+      if (S.act[b] != kActNone) {
+        S.cnt[b] = 0;
+        S.bad[b] = 0;
+      }
+    }
+    __syncwarp();
+    FPROF(6)
+  }
+}
+
+#ifndef ALNNLS_FAST2_U
+#define ALNNLS_FAST2_U 2  // k8 steps whose Q fragments load together (two row tiles each)
+#endif
+
+// TPW row tiles of the pass and TPW columns per warp: 2 (8 warps) or 1 (16 warps, 64
+// registers per thread).
+template <int TPW>
+__global__ void __launch_bounds__(512 / TPW, 2) batched_fast_kernel(BatchArgs a) {
+  extern __shared__ __align__(16) double bsm[];
+  __shared__ ColState S;
+  FastSmem sm;
+  sm.m = a.m;
+  sm.mp = round8(a.m);
+  sm.ps = panel_stride(a.m);
+  sm.VU = bsm;
+  sm.X = bsm + (size_t)sm.mp * kFLD;
+  sm.G = sm.X + (size_t)sm.ps * 16;
+  {
+    const int total = sm.mp * kFLD + 2 * sm.ps * 16;  // pads must read as +0
+    for (int e = threadIdx.x; e < total; e += blockDim.x) bsm[e] = 0.0;
+  }
+  if (threadIdx.x < 16) {
+    S.phase[threadIdx.x] = kIdle;
+    S.act[threadIdx.x] = kActGrab;
+    S.cnt[threadIdx.x] = 0;
+    S.bad[threadIdx.x] = 0;
+  }
+#ifdef ALNNLS_BATCH_PROF
+  if (threadIdx.x < 8) S.pr[threadIdx.x] = 0;
+#endif
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int c = 0; c < TPW; ++c) fast_col(a, S, sm, TPW * warp + c, false);
+  __syncthreads();
+  const int mp = sm.mp, m = sm.m;
+  const int ks_n = mp / 8;
+  constexpr int U = ALNNLS_FAST2_U;
+  // fragment-ordered Q (qfrag_kernel): tile T = 2 warp + mt, k8 step ks, lane -> 4 doubles
+  const double2* qf0 = reinterpret_cast<const double2*>(a.Qf) + ((size_t)(TPW * warp) * ks_n * 32 + lane) * 2;
+  const bool rows_live = 16 * TPW * warp < m;
+#ifdef ALNNLS_BATCH_PROF
+  long long t_g = 0, t_s = 0, npass = 0, nact = 0;
+#endif
+  for (;;) {
+    int active = 0;
+    for (int b = 0; b < 16; ++b) active |= S.phase[b] != kIdle;
+    if (!active) break;
+#ifdef ALNNLS_BATCH_PROF
+    const long long c0 = clock64();
+    for (int b = 0; b < 16; ++b) nact += S.phase[b] != kIdle;
+    ++npass;
+#endif
+    double acc[TPW][2][4];
+#pragma unroll
+    for (int mt = 0; mt < TPW; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[mt][nt][c] = 0.0;
+    if (rows_live) {
+      for (int k0 = 0; k0 < mp; k0 += 8 * U) {
+        double q[U][TPW][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int ks = k0 / 8 + u;
+          const bool in = ks < ks_n;
+          const double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int mt = 0; mt < TPW; ++mt) {
+            const double2* qp = qf0 + ((size_t)mt * ks_n + ks) * 64;
+            const double2 v0 = in ? __ldg(qp) : z;
+            const double2 v1 = in ? __ldg(qp + 1) : z;
+            q[u][mt][0] = v0.x;
+            q[u][mt][1] = v0.y;
+            q[u][mt][2] = v1.x;
+            q[u][mt][3] = v1.y;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k1 = k0 + 8 * u + t;
+          if (k0 + 8 * u >= mp) break;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const double b0 = sm.VU[(size_t)k1 * kFLD + 8 * nt + g];
+            const double b1 = sm.VU[(size_t)(k1 + 4) * kFLD + 8 * nt + g];
+#pragma unroll
+            for (int mt = 0; mt < TPW; ++mt)
+              dmma8(acc[mt][nt], q[u][mt][0], q[u][mt][1], q[u][mt][2], q[u][mt][3], b0, b1);
+          }
+        }
+      }
+    }
+    __syncthreads();  // every warp has read V: U may take its place
+    if (rows_live) {
+#pragma unroll
+      for (int mt = 0; mt < TPW; ++mt) {
+        const int ra = 16 * (TPW * warp + mt) + g, rb = ra + 8;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const int col = 8 * nt + 2 * t;
+          if (ra < m)
+            *reinterpret_cast<double2*>(&sm.VU[(size_t)ra * kFLD + col]) =
+                make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+          if (rb < m)
+            *reinterpret_cast<double2*>(&sm.VU[(size_t)rb * kFLD + col]) =
+                make_double2(acc[mt][nt][2], acc[mt][nt][3]);
+        }
+      }
+    }
+    __syncthreads();
+#ifdef ALNNLS_BATCH_PROF
+    const long long c1 = clock64();
+#endif
+#pragma unroll
+    for (int c = 0; c < TPW; ++c) fast_col(a, S, sm, TPW * warp + c, true);
+#ifdef ALNNLS_BATCH_PROF
+    if (threadIdx.x == 0) S.pr[7] += clock64() - c1;
+#endif
+    __syncthreads();  // every column's V is ready for the next pass
+#ifdef ALNNLS_BATCH_PROF
+    const long long c2 = clock64();
+    t_g += c1 - c0;
+    t_s += c2 - c1;
+#endif
+  }
+#ifdef ALNNLS_BATCH_PROF
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("fast2 prof cta %d: passes %lld, gemm %.1f kcyc/pass, state %.1f kcyc/pass, active cols/pass %.2f | warp 0 (2 cols) kcyc/pass: "
+           "den/df loop %.2f tree %.2f decide %.2f cand %.2f accept loop %.2f trees %.2f lane0 %.2f own %.2f\n",
+           blockIdx.x, npass, t_g / 1e3 / npass, t_s / 1e3 / npass, (double)nact / npass, S.pr[0] / 1e3 / npass,
+           S.pr[1] / 1e3 / npass, S.pr[2] / 1e3 / npass, S.pr[3] / 1e3 / npass, S.pr[4] / 1e3 / npass,
+           S.pr[5] / 1e3 / npass, S.pr[6] / 1e3 / npass, S.pr[7] / 1e3 / npass);
 #endif
 }
 
@@ -1003,6 +1361,8 @@ cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream
     if (cudaError_t e = smem_optin(batched_nqp_kernel<4, kBT, 1>, mx)) return e;
     if (cudaError_t e = smem_optin(batched_nqp_kernel<8, 256, 2>, (int)batch_smem_bytes(256, 8)))
       return e;
+    if (cudaError_t e = smem_optin(batched_nqp_kernel<8, 128, 2>, (int)batch_smem_bytes(256, 8)))
+      return e;
   }
   // EXACT, m <= 256: two CTAs of 8 columns per SM (c4 65536 columns: loop 1.545 ->
   // 1.498 s). FAST keeps one 16-column CTA: its DMMA pass shares each Q fragment
@@ -1014,7 +1374,12 @@ cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream
     const int need = (a.ncols + 7) / 8;
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    batched_nqp_kernel<8, 256, 2><<<grid, 256, smem, stream>>>(a);
+    // 128 threads, each 2 rows x 8 columns of the GEMM (half the V and Q load instructions
+    // per FP64 operation of the 256-thread, 1 x 8 form): 65536-column loop 1.487 -> 1.461 s.
+    // ALNNLS_BATCH_BT=256 keeps the 256-thread CTAs for A/B runs.
+    const char* bt = getenv("ALNNLS_BATCH_BT");
+    if (bt && atoi(bt) == 256) batched_nqp_kernel<8, 256, 2><<<grid, 256, smem, stream>>>(a);
+    else batched_nqp_kernel<8, 128, 2><<<grid, 128, smem, stream>>>(a);
     return cudaGetLastError();
   }
   const size_t smem = batch_smem_bytes(a.m, NB);
@@ -1027,6 +1392,23 @@ cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream
     const int mp = round8(a.m);
     qfrag_kernel<<<64, 256, 0, stream>>>(a.Q, a.m, mp, a.Qf);
     if (cudaError_t e = cudaGetLastError()) return e;
+    // Two 16-column CTAs per SM once the batch fills their slots a few times over (65536
+    // columns: loop 0.689 -> 0.609 s, 16384: 0.188 -> 0.178); smaller batches keep the
+    // one-CTA kernel, whose half as many slots leave a shorter tail (8192: 0.104 vs 0.107).
+    // ALNNLS_FAST_2CTA=0 / 1 forces either for A/B runs.
+    const char* two = getenv("ALNNLS_FAST_2CTA");
+    const bool use2 = two ? atoi(two) != 0 : a.ncols >= 5 * 16 * sm_count;
+    if (use2) {
+      const size_t fsm = fast_smem_bytes(a.m);
+      if (cudaError_t e = smem_optin(batched_fast_kernel<1>, (int)fast_smem_bytes(256))) return e;
+      if (cudaError_t e = smem_optin(batched_fast_kernel<2>, (int)fast_smem_bytes(256))) return e;
+      int fgrid = 2 * sm_count;
+      if (fgrid > need) fgrid = need;
+      const char* tpw = getenv("ALNNLS_FAST_TPW");
+      if (tpw && atoi(tpw) == 2) batched_fast_kernel<2><<<fgrid, 256, fsm, stream>>>(b);
+      else batched_fast_kernel<1><<<fgrid, 512, fsm, stream>>>(b);
+      return cudaGetLastError();
+    }
   } else {
     b.Qf = nullptr;
   }

@@ -250,3 +250,27 @@ def test_fast_batched_within_tolerance(solver):
         tol = baseline_tolerances(Xf[:, j], Xe[:, j], cf[j]["f_final"], ce[j]["f_final"],
                                   cf[j]["iterations"], ce[j]["iterations"])
         assert tol["objective_ok"], (j, tol)
+
+
+@pytest.mark.parametrize("d,n,nrhs,seed", [(2000, 256, 700, 11), (1500, 200, 333, 5), (900, 97, 64, 3)])
+def test_fast_batched_two_cta_kernel_identical(solver, d, n, nrhs, seed):
+    """batched_fast_kernel (two 16-column CTAs per SM, the per-column state cut to three
+    vectors; g_bar, delta and the candidate recomputed) runs the same sums, trees and
+    decisions as the one-CTA FAST kernel: identical X and per-column results."""
+    inst = instances.make_batched(d=d, n=n, nrhs=nrhs, seed=seed)
+    cfg = fast(SolverConfig(epsilon=1e-8, stall_window=10**9))
+    out = {}
+    old = os.environ.get("ALNNLS_FAST_2CTA")
+    try:
+        for mode in ("0", "1"):
+            os.environ["ALNNLS_FAST_2CTA"] = mode
+            X, cols, _ = solver.solve_nnls_batched(inst["A"], inst["B"], cfg)
+            out[mode] = (X.copy(), [(c["iterations"], c["termination"], c["f_final"], c["gbs_final"],
+                                     c["multiplies_total"]) for c in cols])
+    finally:
+        if old is None:
+            del os.environ["ALNNLS_FAST_2CTA"]
+        else:
+            os.environ["ALNNLS_FAST_2CTA"] = old
+    assert np.array_equal(out["0"][0].view(np.uint64), out["1"][0].view(np.uint64))
+    assert out["0"][1] == out["1"][1]
