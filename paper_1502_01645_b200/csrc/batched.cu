@@ -933,6 +933,11 @@ __device__ __forceinline__ void fast_cand(double alpha, double xi, double gi, do
 }
 
 // One column's state machine after a pass (or its first settle when !after), on one warp.
+// Lane l owns rows l, l + 32, ... (at most 8: m <= 256), walked by fully unrolled loops
+// at fixed offsets from per-lane base pointers, one loop per action: the state machine
+// shares the SM's issue slots with the other CTA's DMMA pass, so its instruction count
+// is what it costs. Per-lane sums in ascending row order, then the xor-shuffle tree.
+#define FAST_ROWS(j) _Pragma("unroll") for (int j = 0; j < 8; ++j) if (j < nr)
 __device__ void fast_col(const BatchArgs& a, ColState& S, const FastSmem& sm, int b, bool after) {
   const int lane = threadIdx.x & 31;
   const int m = sm.m;
@@ -942,27 +947,28 @@ __device__ void fast_col(const BatchArgs& a, ColState& S, const FastSmem& sm, in
 #else
 #define FPROF(k)
 #endif
-  double* xb = sm.X + (size_t)b * sm.ps;
-  double* gb = sm.G + (size_t)b * sm.ps;
+  const int nr = (m - lane + 31) >> 5;  // this lane's rows: lane + 32 j, j < nr
+  double* xl = sm.X + (size_t)b * sm.ps + lane;
+  double* gl = sm.G + (size_t)b * sm.ps + lane;
+  double* vl = sm.VU + (size_t)lane * kFLD + b;
+  constexpr int VS = 32 * kFLD;  // VU stride between a lane's rows
   if (after) {
     const int ph = S.phase[b];
     if (ph != kIdle) {
       double f = 0.0;
       if (ph == kNeedP1) {  // den = g_bar . (Q g_bar)
-#pragma unroll 4
-        for (int i = lane; i < m; i += 32) {
-          const double xi = xb[i], gi = gb[i];
+        FAST_ROWS(j) {
+          const double xi = xl[32 * j], gi = gl[32 * j];
           const double gbar = (xi > 0.0 || gi < 0.0) ? gi : 0.0;
-          f += gbar != 0.0 ? xmul(gbar, sm.vu(i, b)) : -0.0;
+          f += gbar != 0.0 ? xmul(gbar, vl[VS * j]) : -0.0;
         }
       } else {  // df = (g + 0.5 Q delta) . delta (nqp.hpp:307)
         const double alpha = S.alpha[b];
-#pragma unroll 4
-        for (int i = lane; i < m; i += 32) {
-          const double gi = gb[i];
+        FAST_ROWS(j) {
+          const double gi = gl[32 * j];
           double c, dd;
-          fast_cand(alpha, xb[i], gi, c, dd);
-          f += dd != 0.0 ? xmul(xadd(gi, xmul(0.5, sm.vu(i, b))), dd) : -0.0;
+          fast_cand(alpha, xl[32 * j], gi, c, dd);
+          f += dd != 0.0 ? xmul(xadd(gi, xmul(0.5, vl[VS * j])), dd) : -0.0;
         }
       }
       FPROF(0)
@@ -1001,48 +1007,50 @@ __device__ void fast_col(const BatchArgs& a, ColState& S, const FastSmem& sm, in
 #endif
     int cnt = 0, bad = 0;
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+    // the stop-test terms of a row on the (new) state: mask, V = g_bar, the three sums
+    auto stop_terms = [&](int j, double xi, double gi, double qi) {
+      const bool p = xi > 0.0 || gi < 0.0;
+      cnt += p;
+      if (!isfinite(gi)) bad = 1;
+      const double gbar = p ? gi : 0.0;
+      vl[VS * j] = gbar;
+      const bool xnz = xi != 0.0;
+      f0 += xmul(gbar, gbar);
+      f1 += xnz ? xmul(xi, gi) : -0.0;
+      f2 += xnz ? xmul(xi, qi) : -0.0;
+    };
     if (act == kActCand) {
       const double alpha = S.alpha[b];
-#pragma unroll 4
-      for (int i = lane; i < m; i += 32) {
+      FAST_ROWS(j) {
         double c, d;
-        fast_cand(alpha, xb[i], gb[i], c, d);
+        fast_cand(alpha, xl[32 * j], gl[32 * j], c, d);
         cnt += d != 0.0;
-        sm.vu(i, b) = d;
+        vl[VS * j] = d;
       }
       FPROF(3)
     } else if (act == kActAccept || act == kActMask || act == kActInit) {
-      const double* qg = a.QB + (size_t)S.col[b] * m;
-      const double alpha = S.alpha[b];
-#pragma unroll 4
-      for (int i = lane; i < m; i += 32) {
-        const double qi = __ldg(qg + i);
-        double xi, gi;
-        if (act == kActAccept) {  // nqp.hpp:309-313
-          const double go = gb[i];
-          double d;
-          fast_cand(alpha, xb[i], go, xi, d);
-          gi = xadd(go, sm.vu(i, b));
-          xb[i] = xi;
-          gb[i] = gi;
-        } else if (act == kActInit) {  // x = 0, grad = q (nqp.hpp:224-225)
-          xi = 0.0;
-          gi = qi;
-          xb[i] = xi;
-          gb[i] = gi;
-        } else {
-          xi = xb[i];
-          gi = gb[i];
+      const double* ql = a.QB + (size_t)S.col[b] * m + lane;
+      if (act == kActAccept) {  // nqp.hpp:309-313
+        const double alpha = S.alpha[b];
+        FAST_ROWS(j) {
+          const double qi = __ldg(ql + 32 * j);
+          const double go = gl[32 * j];
+          double xi, d;
+          fast_cand(alpha, xl[32 * j], go, xi, d);
+          const double gi = xadd(go, vl[VS * j]);
+          xl[32 * j] = xi;
+          gl[32 * j] = gi;
+          stop_terms(j, xi, gi, qi);
         }
-        const bool p = xi > 0.0 || gi < 0.0;
-        cnt += p;
-        if (!isfinite(gi)) bad = 1;
-        const double gbar = p ? gi : 0.0;
-        sm.vu(i, b) = gbar;
-        const bool xnz = xi != 0.0;
-        f0 += xmul(gbar, gbar);
-        f1 += xnz ? xmul(xi, gi) : -0.0;
-        f2 += xnz ? xmul(xi, qi) : -0.0;
+      } else if (act == kActInit) {  // x = 0, grad = q (nqp.hpp:224-225)
+        FAST_ROWS(j) {
+          const double qi = __ldg(ql + 32 * j);
+          xl[32 * j] = 0.0;
+          gl[32 * j] = qi;
+          stop_terms(j, 0.0, qi, qi);
+        }
+      } else {
+        FAST_ROWS(j) stop_terms(j, xl[32 * j], gl[32 * j], __ldg(ql + 32 * j));
       }
       FPROF(4)
       f0 = warp_tree(f0);
@@ -1050,9 +1058,11 @@ __device__ void fast_col(const BatchArgs& a, ColState& S, const FastSmem& sm, in
       f2 = warp_tree(f2);
       FPROF(5)
     } else {  // kActFinish / kActGrab
-      if (act == kActFinish)
-        for (int i = lane; i < m; i += 32) a.Y[(size_t)S.col[b] * m + i] = xb[i];
-      for (int i = lane; i < m; i += 32) sm.vu(i, b) = 0.0;  // idle slots feed zeros
+      if (act == kActFinish) {
+        double* yl = a.Y + (size_t)S.col[b] * m + lane;
+        FAST_ROWS(j) yl[32 * j] = xl[32 * j];
+      }
+      FAST_ROWS(j) vl[VS * j] = 0.0;  // idle slots feed zeros
     }
 #ifdef ALNNLS_BATCH_PROF
     t0 = clock64();
@@ -1078,9 +1088,10 @@ __device__ void fast_col(const BatchArgs& a, ColState& S, const FastSmem& sm, in
     FPROF(6)
   }
 }
+#undef FAST_ROWS
 
 #ifndef ALNNLS_FAST2_U
-#define ALNNLS_FAST2_U 2  // k8 steps whose Q fragments load together (two row tiles each)
+#define ALNNLS_FAST2_U 1  // k8 steps whose Q fragments load together (two row tiles each); 1 measured best (0.566 s vs 0.605 U=2, 0.646 U=4 on the c4 loop)
 #endif
 
 // TPW row tiles of the pass and TPW columns per warp: 2 (8 warps) or 1 (16 warps, 64
