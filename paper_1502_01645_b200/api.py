@@ -24,6 +24,41 @@ from ._native import load
 TERMINATIONS = abi.TERMINATIONS
 
 
+class ColumnResults:
+    """Per-column results of a batched solve (alnnls_column_result records): a sequence of
+    dicts built on access, over one structured numpy copy of the records (`.array`), so a
+    65536-column batch does not pay for 65536 Python dicts inside the call."""
+    _DTYPE = np.dtype([("termination", "<i4"), ("numeric_failure", "<i4"), ("iterations", "<u8"),
+                       ("residual_sq", "<f8"), ("f_final", "<f8"), ("gbs_final", "<f8"),
+                       ("multiplies_total", "<u8")])
+
+    def __init__(self, cols):
+        assert self._DTYPE.itemsize == C.sizeof(abi.ColumnResult)
+        self.array = np.frombuffer(cols, dtype=self._DTYPE).copy() if len(cols) else \
+            np.zeros(0, dtype=self._DTYPE)
+
+    def __len__(self):
+        return len(self.array)
+
+    def _dict(self, r):
+        return {"termination": TERMINATIONS[int(r["termination"])],
+                "numeric_failure": bool(r["numeric_failure"]), "iterations": int(r["iterations"]),
+                "residual_sq": float(r["residual_sq"]), "f_final": float(r["f_final"]),
+                "gbs_final": float(r["gbs_final"]),
+                "multiplies_total": int(r["multiplies_total"])}
+
+    def __getitem__(self, j):
+        if isinstance(j, slice):
+            return [self._dict(r) for r in self.array[j]]
+        return self._dict(self.array[j])
+
+    def __iter__(self):
+        return (self._dict(r) for r in self.array)
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+
 class NumericFailure(RuntimeError):
     """antilop::NumericFailure (nqp.hpp:136-145)."""
 
@@ -358,7 +393,7 @@ class Solver:
                                                 C.byref(self._summary))
         if st != abi.OK:
             self._raise(st, trace=[])
-        return X, [self._col(c) for c in cols], self._timings()
+        return X, ColumnResults(cols), self._timings()
 
     def solve_nnls_batched_device(self, A_ptr, B_ptr, X_ptr, d, n, nrhs,
                                   config: SolverConfig = SolverConfig(), fetch_cols=True):
@@ -372,7 +407,7 @@ class Solver:
             C.byref(self._summary))
         if st != abi.OK:
             self._raise(st, trace=[])
-        return ([self._col(c) for c in cols] if cols is not None else None), self._timings()
+        return (ColumnResults(cols) if cols is not None else None), self._timings()
 
     @staticmethod
     def _col(c):
@@ -557,7 +592,7 @@ def solve_nnls_batched_multi(solvers, A, B, config: SolverConfig = SolverConfig(
                                              C.byref(summ))
     if st != abi.OK:
         solvers[0]._raise(st)
-    return X, [Solver._col(c) for c in cols], summ
+    return X, ColumnResults(cols), summ
 
 
 def default_solver(device=0):

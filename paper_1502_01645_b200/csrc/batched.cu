@@ -1362,6 +1362,11 @@ __global__ void qfrag_kernel(const double* Q, int m, int mp, double* Qf) {
 #define ALNNLS_BATCH_2CTA 1  // build knob: m <= 256 runs two 8-column CTAs per SM
 #endif
 
+cudaError_t launch_qfrag(const BatchArgs& a, cudaStream_t stream) {
+  qfrag_kernel<<<64, 256, 0, stream>>>(a.Q, a.m, round8(a.m), a.Qf);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream) {
   const int NB = batched_cols_per_cta(a.m);
   if (NB == 0) return cudaErrorInvalidValue;
@@ -1400,15 +1405,16 @@ cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream
   if (grid < 1) grid = 1;
   BatchArgs b = a;
   if (NB == 16 && a.fast && a.Qf) {
-    const int mp = round8(a.m);
-    qfrag_kernel<<<64, 256, 0, stream>>>(a.Q, a.m, mp, a.Qf);
-    if (cudaError_t e = cudaGetLastError()) return e;
-    // Two 16-column CTAs per SM once the batch fills their slots a few times over (65536
-    // columns: loop 0.689 -> 0.609 s, 16384: 0.188 -> 0.178); smaller batches keep the
-    // one-CTA kernel, whose half as many slots leave a shorter tail (8192: 0.104 vs 0.107).
+    if (!a.qf_ready)
+      if (cudaError_t e = launch_qfrag(a, stream)) return e;
+    // Two 16-column CTAs per SM whenever the batch has more than one CTA per SM to fill
+    // (loop, one-CTA vs two-CTA kernel: 4096 columns 0.0623 vs 0.0558 s, 8192 0.1045 vs
+    // 0.0983, 16384 0.189 vs 0.164, 32768 0.355 vs 0.299, 65536 0.689 vs 0.566); below
+    // that the grids are the same and the one-CTA kernel stays.
     // ALNNLS_FAST_2CTA=0 / 1 forces either for A/B runs.
     const char* two = getenv("ALNNLS_FAST_2CTA");
-    const bool use2 = two ? atoi(two) != 0 : a.ncols >= 5 * 16 * sm_count;
+    const int tot = a.total_cols > a.ncols ? a.total_cols : a.ncols;
+    const bool use2 = two ? atoi(two) != 0 : tot > 16 * sm_count;
     if (use2) {
       const size_t fsm = fast_smem_bytes(a.m);
       if (cudaError_t e = smem_optin(batched_fast_kernel<1>, (int)fast_smem_bytes(256))) return e;

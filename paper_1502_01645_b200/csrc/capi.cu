@@ -38,13 +38,15 @@ struct alnnls_ctx {
   cudaStream_t copy_stream = nullptr;  // H2D of the host-buffer entries (overlapped uploads)
   cudaEvent_t ev[6] = {};
   cudaEvent_t up[16] = {};            // row-block upload events (kMaxUpBlocks)
+  cudaStream_t bstream[2] = {};       // batched host pipeline: alternating solve streams (lazy)
+  cudaEvent_t bev[8] = {};            // its per-chunk events: [2c] q ready, [2c+1] chunk solved
   std::string err;
 
   DevBuf A, b, Q, q, x, g, y_out, u, gd, mask, gP, chg, dC, candC, gC, prod0, prod1, prod2;
   DevBuf diag, pos, scale, retained, mscalar, trace, mults, ctrl, list, vals, ax, resid, flag, H,
       hvec, start, bcols, X, x_alt, mask2, gP2, xP2, qP2, part, resb, yb, qb, uP, gdC, skp, skf,
       ay, axn, aw, avy, apc, tst, fgb0, fgb1, fpart, fden, fkl, fkv, fkc, dmws, dmfl, nvt,
-      nht, nwt, nv, nw, nh, qfrag;
+      nht, nwt, nv, nw, nh, qfrag, bcnt;
 
   // last solve
   bool last_nnls = false;
@@ -878,13 +880,17 @@ void alnnls_destroy(alnnls_ctx* ctx) {
                     &ctx->avy,    &ctx->apc,   &ctx->tst,   &ctx->fgb0,  &ctx->fgb1,
                     &ctx->fpart,  &ctx->fden,  &ctx->fkl,   &ctx->fkv,   &ctx->fkc,
                     &ctx->dmws,   &ctx->dmfl,  &ctx->nvt,   &ctx->nht,   &ctx->nwt,
-                    &ctx->nv,     &ctx->nw,    &ctx->nh,    &ctx->qfrag};
+                    &ctx->nv,     &ctx->nw,    &ctx->nh,    &ctx->qfrag, &ctx->bcnt};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->up)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->bev)
+    if (e) cudaEventDestroy(e);
+  for (auto& t : ctx->bstream)
+    if (t) cudaStreamDestroy(t);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->pin) cudaFreeHost(ctx->pin);
@@ -1322,13 +1328,57 @@ namespace {
 
 // K8 pipeline on device A (d x n, lda) and B (d x nrhs, ldb): per column bitwise
 // solve_nnls(A, B[:, j], cfg). X (n x nrhs, ld n) and per-column results.
+//
+// hB != nullptr (the host-buffer entry): dB is only allocated, and the columns of the host
+// B are uploaded in kHostChunks column chunks on the copy stream. Each chunk's finiteness
+// check and q formation wait for its own upload only, and the chunks' solves run on two
+// alternating streams, so the second chunk's upload hides under the first chunk's solve
+// and its persistent CTAs take over the SMs as the first chunk's CTAs retire (columns
+// are independent: the per-column results are those of the one-launch path). The first
+// chunk is a quarter of the columns: its upload is what stays exposed, its solve is
+// longer than the rest of the upload. *bad_b reports a non-finite B (checked after the
+// fact; the caller discards the results, as if the DenseMatrix had been validated first).
+constexpr int kHostChunks = 2;
 int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint64_t lda,
                 uint64_t nrhs, const double* dB, uint64_t ldb, const alnnls_config* cfg,
-                double* dX, alnnls_column_result* cols, alnnls_summary* out) {
+                double* dX, alnnls_column_result* cols, alnnls_summary* out,
+                const double* hB = nullptr, int* bad_b = nullptr) {
   int st__ = ALNNLS_OK;
-  cudaStream_t s = ctx->stream;
+  cudaStream_t s = ctx->stream, cs = ctx->copy_stream;
   alnnls_summary sum{};
+  // column chunks [edge[c], edge[c + 1])
+  uint64_t edge[kHostChunks + 1] = {0, nrhs, nrhs};
+  int nch = 1;
+  // ALNNLS_BATCH_OVERLAP_MIN: the smallest batch that is chunked (default 64 columns per
+  // SM: below it the upload is short and the extra launch's tail is not); 0 turns it off
+  const char* omin = getenv("ALNNLS_BATCH_OVERLAP_MIN");
+  const uint64_t min_cols = omin ? (uint64_t)atoll(omin) : (uint64_t)64 * ctx->sm_count;
+  if (hB && min_cols > 0 && nrhs >= min_cols && nrhs >= 64) {
+    nch = 2;
+    edge[1] = (nrhs / 4 + 15) / 16 * 16;
+  }
+  if (nch > 1 && !ctx->bstream[0]) {
+    for (auto& t : ctx->bstream) CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    for (auto& e : ctx->bev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   CK(cudaEventRecord(ctx->ev[0], s));
+  int* bflag = nullptr;
+  // chunk c's upload on the copy stream (a pageable B makes the call block: chunk c + 1 is
+  // therefore enqueued after chunk c's launches, which then run under it)
+  auto upload_chunk = [&](int c) -> int {
+    const uint64_t c0 = edge[c], cnt = edge[c + 1] - c0;
+    CK(cudaMemcpy2DAsync(const_cast<double*>(dB) + c0 * ldb, ldb * sizeof(double), hB + c0 * d,
+                         d * sizeof(double), d * sizeof(double), cnt, cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(ctx->up[c], cs));
+    return ALNNLS_OK;
+  };
+  if (hB) {
+    int* fl = ENSURE(int, flag, 4);
+    bflag = fl + 1;
+    CK(cudaMemsetAsync(bflag, 0, sizeof(int), s));
+    CK(cudaStreamWaitEvent(cs, ctx->ev[0], 0));
+    if (int urc = upload_chunk(0)) return urc;
+  }
   uint64_t m = 0;
   int rc = run_setup(ctx, d, n, dA, lda, nullptr, &m, cfg->profile);  // the shared Gram, once
   if (rc) return rc;
@@ -1341,71 +1391,107 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
   CK(cudaMemcpyAsync(dres, init.data(), sizeof(alnnls_column_result) * nrhs,
                      cudaMemcpyHostToDevice, s));
   double* Y = ENSURE(double, yb, (m ? m : 1) * nrhs);
+  Resolved r{};
+  double* Qc = nullptr;
+  double* QB = nullptr;
+  int* counter = nullptr;
+  BatchArgs ba{};
+  const bool dmma_q = m > 0 && cfg->profile == ALNNLS_PROFILE_FAST;
   if (m > 0) {
-    Resolved r;
     if ((rc = resolve(ctx, cfg, m, &r))) return rc;  // solve_nqp validates its config
     if (batched_cols_per_cta((int)m) == 0)
       return set_err(ctx, ALNNLS_EINVAL, "solve_nnls_batched: n > 1024 not supported");
-    double* Qc = ENSURE(double, H, m * m);
+    Qc = ENSURE(double, H, m * m);
     CK(launch_from_blocked(static_cast<double*>(ctx->Q.p), (int)m, (int)ctx->qR, Qc, m, s));
-    double* QB = ENSURE(double, qb, m * nrhs);
-    SetupArgs sa{};
-    sa.A = dA;
-    sa.lda = lda;
-    sa.d = (int)d;
-    sa.n = (int)n;
-    sa.pos = static_cast<int*>(ctx->pos.p);
-    sa.scale = static_cast<double*>(ctx->scale.p);
-    sa.m = (int)m;
-    sa.B = dB;
-    sa.ldb = ldb;
-    sa.nrhs = (int)nrhs;
-    sa.QB = QB;
-    // q_j = (-(A^T b_j))[retained] / D for every column
-    if (cfg->profile == ALNNLS_PROFILE_FAST && syrk_dmma_supported(sa, 2)) {
-      if ((rc = dmma_buffers(ctx, sa))) return rc;
-      CK(launch_syrk_dmma(sa, 2, s));
-    } else {
-      if ((rc = streamk_buffers(ctx, sa, 2))) return rc;
-      CK(launch_syrk(sa, 2, s));
-    }
-    CK(cudaEventRecord(ctx->ev[1], s));
-    int* counter = ENSURE(int, mscalar, 4);
-    CK(cudaMemsetAsync(counter, 0, sizeof(int), s));
-    BatchArgs ba{};
+    QB = ENSURE(double, qb, m * nrhs);
+    counter = ENSURE(int, bcnt, kHostChunks);
+    CK(cudaMemsetAsync(counter, 0, sizeof(int) * kHostChunks, s));
     ba.Q = Qc;
     ba.m = (int)m;
-    ba.QB = QB;
-    ba.ncols = (int)nrhs;
-    ba.Y = Y;
-    ba.res = dres;
     ba.eps = r.eps;
     ba.max_iters = r.max_iters;
     ba.stall_window = cfg->stall_window;
-    ba.next_col = counter;
     ba.fast = cfg->profile == ALNNLS_PROFILE_FAST;
+    ba.total_cols = (int)nrhs;
     // FAST, m <= 256: Q re-laid in DMMA fragment order for the tensor-core passes
     ba.Qf = nullptr;
     if (ba.fast && m <= 256) {
       double* qf = ENSURE(double, qfrag, (size_t)((m + 15) & ~15) * 256);
       ba.Qf = qf;
+      if (nch > 1) {  // once, before the chunks' launches on two streams read it
+        CK(launch_qfrag(ba, s));
+        ba.qf_ready = 1;
+      }
     }
-    CK(cudaEventRecord(ctx->ev[2], s));
-    CK(launch_batched(ba, ctx->sm_count, s));
-    CK(cudaEventRecord(ctx->ev[3], s));
-  } else {
-    CK(cudaEventRecord(ctx->ev[1], s));
-    CK(cudaEventRecord(ctx->ev[2], s));
+  }
+  for (int c = 0; c < nch; ++c) {
+    const uint64_t c0 = edge[c], cnt = edge[c + 1] - c0;
+    if (hB) {
+      CK(cudaStreamWaitEvent(s, ctx->up[c], 0));
+      CK(launch_check_finite(dB + c0 * ldb, d, cnt, ldb, bflag, s));
+    }
+    cudaStream_t ts = nch > 1 ? ctx->bstream[c & 1] : s;
+    if (m > 0) {
+      SetupArgs sa{};
+      sa.A = dA;
+      sa.lda = lda;
+      sa.d = (int)d;
+      sa.n = (int)n;
+      sa.pos = static_cast<int*>(ctx->pos.p);
+      sa.scale = static_cast<double*>(ctx->scale.p);
+      sa.m = (int)m;
+      sa.B = dB + c0 * ldb;
+      sa.ldb = ldb;
+      sa.nrhs = (int)cnt;
+      sa.QB = QB + c0 * m;
+      // q_j = (-(A^T b_j))[retained] / D for every column of the chunk
+      if (dmma_q && syrk_dmma_supported(sa, 2)) {
+        if ((rc = dmma_buffers(ctx, sa))) return rc;
+        CK(launch_syrk_dmma(sa, 2, s));
+      } else {
+        if ((rc = streamk_buffers(ctx, sa, 2))) return rc;
+        CK(launch_syrk(sa, 2, s));
+      }
+    }
+    if (c == 0) {
+      CK(cudaEventRecord(ctx->ev[1], s));
+      CK(cudaEventRecord(ctx->ev[2], s));
+    }
+    if (nch > 1) {
+      CK(cudaEventRecord(ctx->bev[2 * c], s));
+      CK(cudaStreamWaitEvent(ts, ctx->bev[2 * c], 0));
+    }
+    if (m > 0) {
+      BatchArgs bc = ba;
+      bc.QB = QB + c0 * m;
+      bc.ncols = (int)cnt;
+      bc.Y = Y + c0 * m;
+      bc.res = dres + c0;
+      bc.next_col = counter + c;
+      CK(launch_batched(bc, ctx->sm_count, ts));
+    }
+    if (nch == 1) CK(cudaEventRecord(ctx->ev[3], s));
+    CK(launch_unscale_batched(Y + c0 * m, (int)m, static_cast<double*>(ctx->scale.p),
+                              static_cast<uint32_t*>(ctx->retained.p), dX + c0 * n, (int)n,
+                              (int)cnt, ts));
+    CK(launch_residual_batched(dA, lda, (int)d, (int)n, dX + c0 * n, dB + c0 * ldb, ldb, (int)cnt,
+                               dres + c0, ts));
+    if (nch > 1) CK(cudaEventRecord(ctx->bev[2 * c + 1], ts));
+    if (hB && c + 1 < nch)
+      if (int urc = upload_chunk(c + 1)) return urc;
+  }
+  if (nch > 1) {  // join: the chunked loop time includes each chunk's unscale and residual
+    for (int c = 0; c < nch; ++c) CK(cudaStreamWaitEvent(s, ctx->bev[2 * c + 1], 0));
     CK(cudaEventRecord(ctx->ev[3], s));
   }
-  CK(launch_unscale_batched(Y, (int)m, static_cast<double*>(ctx->scale.p),
-                            static_cast<uint32_t*>(ctx->retained.p), dX, (int)n, (int)nrhs, s));
-  CK(launch_residual_batched(dA, lda, (int)d, (int)n, dX, dB, ldb, (int)nrhs, dres, s));
   CK(cudaEventRecord(ctx->ev[4], s));
   if (cols) {
     CK(cudaMemcpyAsync(cols, dres, sizeof(alnnls_column_result) * nrhs, cudaMemcpyDeviceToHost, s));
   }
+  int hbad = 0;
+  if (hB) CK(cudaMemcpyAsync(&hbad, bflag, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  if (bad_b) *bad_b = hbad;
   float t01 = 0, t23 = 0, t34 = 0, t04 = 0;
   cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
   cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
@@ -1464,15 +1550,17 @@ int alnnls_solve_nnls_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const dou
   int st__ = ALNNLS_OK;
   uint64_t lda = 0, ldb = 0;
   if ((rc = upload_matrix(ctx, ctx->A, d, n, A, &lda))) return rc;
-  if ((rc = upload_matrix(ctx, ctx->bcols, d, nrhs, B, &ldb))) return rc;
   if ((rc = device_check_finite(
-           ctx, {{static_cast<double*>(ctx->A.p), d, n, lda, "DenseMatrix: non-finite entry"},
-                 {static_cast<double*>(ctx->bcols.p), d, nrhs, ldb, "DenseMatrix: non-finite entry"}})))
+           ctx, {{static_cast<double*>(ctx->A.p), d, n, lda, "DenseMatrix: non-finite entry"}})))
     return rc;
+  ldb = round_up(d, 4);
+  double* dB = ENSURE(double, bcols, ldb * nrhs);
   double* dX = ENSURE(double, X, n * nrhs);
-  rc = run_batched(ctx, d, n, static_cast<double*>(ctx->A.p), lda, nrhs,
-                   static_cast<double*>(ctx->bcols.p), ldb, cfg, dX, cols, out);
+  int bad_b = 0;
+  rc = run_batched(ctx, d, n, static_cast<double*>(ctx->A.p), lda, nrhs, dB, ldb, cfg, dX, cols,
+                   out, B, &bad_b);  // uploads B in column chunks under the solves
   if (rc) return rc;
+  if (bad_b) return set_err(ctx, ALNNLS_EINVAL, "DenseMatrix: non-finite entry");
   return copy_out(ctx, X, dX, sizeof(double) * n * nrhs);
 }
 

@@ -284,8 +284,11 @@ struct BatchArgs {
   int* next_col;       // work counter (zeroed before the launch)
   int fast;            // FAST profile: the Q V passes on the fp64 tensor cores (DMMA)
   double* Qf;          // FAST, m <= 256: scratch of m_pad^2 doubles for Q in DMMA fragment order
+  int qf_ready;        // Qf already holds Q (launch_qfrag): launch_batched does not rewrite it
+  int total_cols;      // columns of the whole batch when this launch is one chunk of it (0: ncols)
 };
 cudaError_t launch_batched(const BatchArgs& a, int sm_count, cudaStream_t stream);
+cudaError_t launch_qfrag(const BatchArgs& a, cudaStream_t stream);  // Q -> Qf (FAST, m <= 256)
 int batched_cols_per_cta(int m);  // 0 when m is too large for the batched kernel
 cudaError_t launch_unscale_batched(const double* Y, int m, const double* scale,
                                    const uint32_t* retained, double* X, int n, int ncols,

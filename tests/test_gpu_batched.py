@@ -101,6 +101,34 @@ def test_batched_c4_full_shape_sampled_columns(solver):
     assert np.max(np.abs(X - inst["H_true"])) < 1e-3
 
 
+@pytest.mark.parametrize("profile", ["exact", "fast"])
+def test_batched_host_pipeline_chunked_upload(solver, monkeypatch, profile):
+    """The host-buffer entry uploads B in two column chunks under the solves (capi.cu
+    run_batched); forced here at a small batch: the oracle's per-column results (EXACT),
+    and exactly the one-launch path's X and column records (both profiles)."""
+    from paper_1502_01645_b200 import abi
+    inst = instances.make_batched(d=500, n=96, nrhs=203, seed=21)
+    cfg = SolverConfig(epsilon=1e-8, stall_window=10**9,
+                       profile=abi.PROFILE_FAST if profile == "fast" else abi.PROFILE_EXACT)
+    monkeypatch.setenv("ALNNLS_BATCH_OVERLAP_MIN", "0")
+    X1, c1, _ = solver.solve_nnls_batched(inst["A"], inst["B"], cfg)
+    monkeypatch.setenv("ALNNLS_BATCH_OVERLAP_MIN", "64")
+    if profile == "exact":
+        X2, c2 = check(solver, inst["A"], inst["B"], cfg)
+    else:
+        X2, c2, _ = solver.solve_nnls_batched(inst["A"], inst["B"], cfg)
+    assert same_bits(X1.reshape(-1, order="F"), X2.reshape(-1, order="F"))
+    keys = ("iterations", "termination", "residual_sq", "f_final", "gbs_final", "multiplies_total")
+    assert [[c[k] for k in keys] for c in c1] == [[c[k] for k in keys] for c in c2]
+    # a non-finite entry in the second chunk is still the reference's construction error
+    Bbad = inst["B"].copy(order="F")
+    Bbad[3, 150] = np.nan
+    with pytest.raises(Exception, match="non-finite"):
+        solver.solve_nnls_batched(inst["A"], Bbad, cfg)
+    X3, _, _ = solver.solve_nnls_batched(inst["A"], inst["B"], cfg)  # the context recovers
+    assert same_bits(X1.reshape(-1, order="F"), X3.reshape(-1, order="F"))
+
+
 # ---- NMF by alternating NNLS (SURVEY §8f row 4) over the batched entry -------------------
 def test_nmf_bitwise_vs_oracle_alternating_nnls(solver, oracle):
     """alnnls_nmf's half steps are batched solve_nnls calls (Gram shared per half
