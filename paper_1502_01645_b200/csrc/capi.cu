@@ -1474,8 +1474,14 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
     CK(launch_unscale_batched(Y + c0 * m, (int)m, static_cast<double*>(ctx->scale.p),
                               static_cast<uint32_t*>(ctx->retained.p), dX + c0 * n, (int)n,
                               (int)cnt, ts));
-    CK(launch_residual_batched(dA, lda, (int)d, (int)n, dX + c0 * n, dB + c0 * ldb, ldb, (int)cnt,
-                               dres + c0, ts));
+    if (cfg->profile == ALNNLS_PROFILE_FAST &&
+        residual_dmma_supported(dA, lda, (int)d, (int)n, (int)cnt)) {
+      CK(launch_residual_batched_dmma(dA, lda, (int)d, (int)n, dX + c0 * n, dB + c0 * ldb, ldb,
+                                      (int)cnt, dres + c0, ts));
+    } else {
+      CK(launch_residual_batched(dA, lda, (int)d, (int)n, dX + c0 * n, dB + c0 * ldb, ldb,
+                                 (int)cnt, dres + c0, ts));
+    }
     if (nch > 1) CK(cudaEventRecord(ctx->bev[2 * c + 1], ts));
     if (hB && c + 1 < nch)
       if (int urc = upload_chunk(c + 1)) return urc;

@@ -437,6 +437,149 @@ EncodeTiledFn encode_fn() {
   }();
   return fn;
 }
+// ===== FAST batched residuals: ||A x_j - b_j||^2 for every column on the fp64 tensor
+// cores (nnls.hpp:95-105 per column; the EXACT profile keeps the reference-ordered
+// residual_batched_kernel of batched.cu) ================================================
+// A CTA owns RN = 64 columns: their x (n <= 256 entries each) stay in shared memory
+// as the DMMA B operand for the CTA's whole life, and A streams through in 128-row
+// tiles, k slabs of 32 by 16-byte cp.async from L2 (A is read once per CTA: 41 MB at
+// c4, L2-resident). 8 warps as 4 (rows) x 2 (columns), warp tile 32 x 32 = 2 x 4
+// m16n8k8 accumulators. After a tile's last slab each thread subtracts its b entries,
+// squares, and adds into its own per-column sums (tiles in ascending row order); the
+// lanes of a column, then the four row warps, are summed in a fixed order at the end
+// (deterministic run to run). Strides RLDA / ldx = 4 mod 16 doubles keep both fragment
+// loads bank-conflict-free.
+constexpr int RM = 128, RN = 64, RKS = 32, RLDA = RM + 4;
+__host__ __device__ constexpr int res_ldx(int n) { return (n + RKS - 1) / RKS * RKS + 4; }
+size_t res_dmma_smem(int n) {
+  return ((size_t)RN * res_ldx(n) + 2 * (size_t)RKS * RLDA) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(TT, 1)
+residual_dmma_kernel(const double* __restrict__ A, uint64_t lda, int d, int n,
+                     const double* __restrict__ X, const double* __restrict__ B, uint64_t ldb,
+                     int ncols, alnnls_column_result* res) {
+  extern __shared__ __align__(128) double dm_sm[];
+  const int ldx = res_ldx(n);
+  double* Xs = dm_sm;                       // [RN][ldx]: x of column c at Xs[c * ldx + k]
+  double* As = dm_sm + (size_t)RN * ldx;    // [2][RKS][RLDA]: A(i0 + r, k0 + kk) at [kk][r]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 1, wc = warp & 1;
+  const int g = lane >> 2, t = lane & 3;
+  const int c0 = blockIdx.x * RN;
+  const int nks = (n + RKS - 1) / RKS;
+  const int ntile = (d + RM - 1) / RM;
+  const int nslab = ntile * nks;
+
+  // slab q = tile * nks + ks: 2048 16-byte chunks, 8 per thread
+  auto issue = [&](int q) {
+    const int i0 = (q / nks) * RM, k0 = (q % nks) * RKS;
+    double* dst = As + (size_t)(q & 1) * RKS * RLDA;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const int e = tid + p * TT, kk = e >> 6, r = (e & 63) * 2;
+      const int left = d - (i0 + r);
+      const uint32_t bytes = (k0 + kk < n && left > 0) ? (left >= 2 ? 16u : 8u) : 0u;
+      cp_async16(dst + kk * RLDA + r, bytes ? A + (size_t)(k0 + kk) * lda + i0 + r : A, bytes);
+    }
+  };
+  issue(0);
+  cp_commit();
+  for (int e = tid; e < RN * ldx; e += TT) {
+    const int c = e / ldx, k = e - c * ldx;
+    Xs[e] = (c0 + c < ncols && k < n) ? X[(size_t)(c0 + c) * n + k] : 0.0;
+  }
+
+  double acc[2][4][4];
+  double csum[4][2];
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni) csum[ni][0] = csum[ni][1] = 0.0;
+  const double* xw = Xs + (size_t)(wc * 32 + g) * ldx + t;
+  for (int q = 0; q < nslab; ++q) {
+    const int ks = q % nks;
+    if (ks == 0) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[mi][ni][c] = 0.0;
+    }
+    cp_wait<0>();
+    __syncthreads();  // slab q landed; every warp is done with slab q - 1's buffer
+    if (q + 1 < nslab) issue(q + 1);
+    cp_commit();
+    const double* as = As + (size_t)(q & 1) * RKS * RLDA + wr * 32 + g;
+    const double* xs = xw + ks * RKS;
+#pragma unroll
+    for (int k8 = 0; k8 < RKS; k8 += 8) {
+      double af[2][4], bf[4][2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        af[mi][0] = as[(k8 + t) * RLDA + mi * 16];
+        af[mi][1] = as[(k8 + t) * RLDA + mi * 16 + 8];
+        af[mi][2] = as[(k8 + t + 4) * RLDA + mi * 16];
+        af[mi][3] = as[(k8 + t + 4) * RLDA + mi * 16 + 8];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        bf[ni][0] = xs[(size_t)ni * 8 * ldx + k8];
+        bf[ni][1] = xs[(size_t)ni * 8 * ldx + k8 + 4];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
+    }
+    if (ks == nks - 1) {  // the tile is complete: (A x - b)^2 into the column sums
+      const int i0 = (q / nks) * RM + wr * 32 + g;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int col = c0 + wc * 32 + ni * 8 + 2 * t + cc;
+          if (col < ncols) {
+            const double* bp = B + (size_t)col * ldb;
+            double bv[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {  // rows i0, i0 + 8, i0 + 16, i0 + 24
+              const int i = i0 + 8 * h;
+              bv[h] = i < d ? __ldg(bp + i) : 0.0;
+            }
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const int i = i0 + 8 * h;
+              const double df = acc[h >> 1][ni][(h & 1) * 2 + cc] - bv[h];
+              if (i < d) csum[ni][cc] += df * df;
+            }
+          }
+        }
+    }
+  }
+  // lanes of a column (same t, g = 0..7), then the four row warps, in a fixed order
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      double v = csum[ni][cc];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      csum[ni][cc] = v;
+    }
+  __syncthreads();
+  double* red = As;  // [4][RN]
+  if (g == 0) {
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) red[wr * RN + wc * 32 + ni * 8 + 2 * t + cc] = csum[ni][cc];
+  }
+  __syncthreads();
+  if (tid < RN && c0 + tid < ncols)
+    res[c0 + tid].residual_sq = ((red[tid] + red[RN + tid]) + red[2 * RN + tid]) + red[3 * RN + tid];
+}
+
 // rows x cols column-major fp64 (ld doubles): box 16 rows (k) x 128 columns, 128B swizzle
 bool make_map(CUtensorMap* m, const double* p, uint64_t rows, uint64_t cols, uint64_t ld) {
   EncodeTiledFn fn = encode_fn();
@@ -493,6 +636,24 @@ cudaError_t launch_syrk_dmma(const SetupArgs& s, int mode, cudaStream_t stream, 
   if (accumulate) return cudaErrorInvalidValue;  // v1 has no accumulate epilogue
   if (cudaError_t e = smem_optin(syrk_dmma_kernel, (int)kDmmaSmem)) return e;
   syrk_dmma_kernel<<<tiles, TT, kDmmaSmem, stream>>>(s, mode);
+  return cudaGetLastError();
+}
+
+// FAST residuals on the tensor cores when the shape fits (x block resident in shared
+// memory, 16-byte cp.async sources); false: the caller uses the reference-ordered kernel.
+bool residual_dmma_supported(const double* A, uint64_t lda, int d, int n, int ncols) {
+  return n >= 1 && n <= 256 && d >= 1 && ncols >= 1 && (lda % 2) == 0 &&
+         (reinterpret_cast<uintptr_t>(A) % 16) == 0;
+}
+
+cudaError_t launch_residual_batched_dmma(const double* A, uint64_t lda, int d, int n,
+                                         const double* X, const double* B, uint64_t ldb,
+                                         int ncols, alnnls_column_result* res,
+                                         cudaStream_t stream) {
+  if (!residual_dmma_supported(A, lda, d, n, ncols)) return cudaErrorInvalidValue;
+  if (cudaError_t e = smem_optin(residual_dmma_kernel, (int)res_dmma_smem(256))) return e;
+  residual_dmma_kernel<<<(ncols + RN - 1) / RN, TT, res_dmma_smem(n), stream>>>(
+      A, lda, d, n, X, B, ldb, ncols, res);
   return cudaGetLastError();
 }
 

@@ -297,4 +297,11 @@ cudaError_t launch_residual_batched(const double* A, uint64_t lda, int d, int n,
                                     const double* B, uint64_t ldb, int ncols,
                                     alnnls_column_result* res, cudaStream_t stream);
 
+// FAST: the same residuals on the fp64 tensor cores (dmma.cu), n <= 256
+bool residual_dmma_supported(const double* A, uint64_t lda, int d, int n, int ncols);
+cudaError_t launch_residual_batched_dmma(const double* A, uint64_t lda, int d, int n,
+                                         const double* X, const double* B, uint64_t ldb,
+                                         int ncols, alnnls_column_result* res,
+                                         cudaStream_t stream);
+
 }  // namespace alnnls

@@ -274,3 +274,29 @@ def test_fast_batched_two_cta_kernel_identical(solver, d, n, nrhs, seed):
             os.environ["ALNNLS_FAST_2CTA"] = old
     assert np.array_equal(out["0"][0].view(np.uint64), out["1"][0].view(np.uint64))
     assert out["0"][1] == out["1"][1]
+
+
+@pytest.mark.parametrize("d,n,nrhs,noise", [(2000, 256, 203, 0.0), (777, 96, 130, 1e-3),
+                                            (300, 97, 64, 0.1), (129, 7, 65, 0.5)])
+def test_fast_batched_residuals_on_tensor_cores(solver, d, n, nrhs, noise):
+    """FAST batched residual_sq comes from residual_dmma_kernel (DMMA A X tiles minus B,
+    squared, fixed-order column sums; dmma.cu): it must be ||A x_j - b_j||^2 of the
+    returned x_j (nnls.hpp:95-105) up to fp64 summation-order rounding. Ragged shapes:
+    d not a multiple of 128, n not a multiple of 8 or 32, a partial column block."""
+    rng = np.random.default_rng(d + n)
+    inst = instances.make_batched(d=d, n=n, nrhs=nrhs, seed=d)
+    B = np.asfortranarray(inst["B"] + noise * rng.standard_normal(inst["B"].shape))
+    cfg = fast(SolverConfig(epsilon=1e-8, stall_window=10**9))
+    X, cols, _ = solver.solve_nnls_batched(inst["A"], B, cfg)
+    R = inst["A"] @ X - B
+    want = np.einsum("ij,ij->j", R, R)
+    got = cols.array["residual_sq"]
+    # each entry of A x - b carries ~n ulps of |A||x| + |b|; squared and summed over d rows
+    scale = (np.abs(inst["A"]) @ np.abs(X) + np.abs(B)).max(axis=0)
+    atol = d * (64 * n * np.finfo(float).eps * scale) ** 2
+    assert np.all(np.abs(got - want) <= 1e-10 * want + atol), np.max(np.abs(got - want) / (want + atol))
+    # and the EXACT profile's reference-ordered residual (of its own x, equal to FAST's within
+    # the KKT tolerance) is the same number to first order
+    Xe, ce, _ = solver.solve_nnls_batched(inst["A"], B, SolverConfig(epsilon=1e-8, stall_window=10**9))
+    if noise >= 1e-3:
+        assert np.allclose(got, ce.array["residual_sq"], rtol=1e-3)
