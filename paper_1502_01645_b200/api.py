@@ -375,16 +375,25 @@ class Solver:
             float(s_in), C.byref(out)))
         return out.value
 
-    def solve_nnls_batched(self, A, B, config: SolverConfig = SolverConfig()):
+    def solve_nnls_batched(self, A, B, config: SolverConfig = SolverConfig(), out=None):
         """solve_nnls(A, B[:, j], config) for every column j (bitwise, exact profile).
-        Returns (X (n x nrhs), [per-column dict], summary timings)."""
+        Returns (X (n x nrhs), per-column results, summary timings). `out`: an optional
+        Fortran-ordered float64 (n x nrhs) array that receives X (e.g. a pinned buffer a
+        caller reuses across NMF half steps) instead of a fresh allocation."""
         A = _fortran(A)
         B = _fortran(B)
         if A.shape[0] != B.shape[0]:
             raise ValueError("solve_nnls: A and b dimension mismatch")
         d, n = A.shape
         k = B.shape[1]
-        X = np.zeros((n, k), order="F")
+        if out is not None:
+            if (out.dtype != np.float64 or out.shape != (n, k) or not out.flags.f_contiguous
+                    or not out.flags.writeable):
+                raise ValueError("solve_nnls_batched: out must be a writable Fortran-ordered "
+                                 "float64 (n x nrhs) array")
+            X = out
+        else:
+            X = np.empty((n, k), order="F")  # the library writes every entry
         cols = (abi.ColumnResult * k)()
         self._summary = abi.Summary()
         cfg = config.to_abi(record_multiplies=False)

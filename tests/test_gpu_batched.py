@@ -125,8 +125,12 @@ def test_batched_host_pipeline_chunked_upload(solver, monkeypatch, profile):
     Bbad[3, 150] = np.nan
     with pytest.raises(Exception, match="non-finite"):
         solver.solve_nnls_batched(inst["A"], Bbad, cfg)
-    X3, _, _ = solver.solve_nnls_batched(inst["A"], inst["B"], cfg)  # the context recovers
+    buf = np.full(X1.shape, 7.0, order="F")  # the context recovers; a caller-owned result buffer
+    X3, _, _ = solver.solve_nnls_batched(inst["A"], inst["B"], cfg, out=buf)
+    assert X3 is buf
     assert same_bits(X1.reshape(-1, order="F"), X3.reshape(-1, order="F"))
+    with pytest.raises(ValueError, match="out must be"):
+        solver.solve_nnls_batched(inst["A"], inst["B"], cfg, out=np.empty(X1.shape))
 
 
 # ---- NMF by alternating NNLS over the batched entry -------------------
