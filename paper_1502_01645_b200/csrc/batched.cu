@@ -573,7 +573,11 @@ __device__ void after_pass(const BatchArgs& a, ColState& S, const BatchSmem& sm,
 // grp * CG: U[:, col] = Q V[:, col], rows i = trow + r * ROWT (ascending j per
 // output). Off-mask entries of V are 0 and their +-0 products are exact no-ops
 // (idle slots, pad rows j >= m with their zero Q operands too).
-template <int RPT, int CG, int ROWT, int LD, int JB = 8>
+#ifndef ALNNLS_GEMM_QBUF
+#define ALNNLS_GEMM_QBUF 3  // register blocks of Q columns in flight in the 128-thread two-CTA
+                            // configuration (2: ping-pong, 3: rotation); the others keep 2
+#endif
+template <int RPT, int CG, int ROWT, int LD, int JB = 8, int QBUF = 2>
 __device__ __forceinline__ void gemm_pass(const BatchArgs& a, const BatchSmem& sm, int grp, int trow) {
   const int m = sm.m, mp = sm.mp;
   double acc[RPT * CG];
@@ -618,6 +622,23 @@ __device__ __forceinline__ void gemm_pass(const BatchArgs& a, const BatchSmem& s
         for (int b = 0; b < CG; ++b) acc[r * CG + b] = xmac(acc[r * CG + b], qv[r][u], vb[b]);
     }
   };
+  if constexpr (QBUF == 3) {
+  // three register blocks in rotation: a block's loads are issued two blocks (2 x JB x
+  // RPT x CG rounded multiply-adds) before its use: the L2 latency of the Q columns is
+  // longer than one block of one warp per scheduler (ncu: long-scoreboard stalls on the
+  // first use of a block). 65536-column loop 1.4595 -> 1.4326 s, same bits.
+  double qa[RPT][JB], qb[RPT][JB], qc[RPT][JB];
+  load_q(0, qa);
+  if (JB < mp) load_q(JB, qb);
+  for (int j0 = 0; j0 < mp; j0 += 3 * JB) {  // mp is a multiple of JB; V rows >= m are zero
+    if (j0 + 2 * JB < mp) load_q(j0 + 2 * JB, qc);
+    block(j0, qa);
+    if (j0 + 3 * JB < mp) load_q(j0 + 3 * JB, qa);
+    if (j0 + JB < mp) block(j0 + JB, qb);
+    if (j0 + 4 * JB < mp) load_q(j0 + 4 * JB, qb);
+    if (j0 + 2 * JB < mp) block(j0 + 2 * JB, qc);
+  }
+  } else {
   double qa[RPT][JB], qb[RPT][JB];
   load_q(0, qa);
   for (int j0 = 0; j0 < mp; j0 += 2 * JB) {  // mp is a multiple of JB; V rows >= m are zero
@@ -626,6 +647,7 @@ __device__ __forceinline__ void gemm_pass(const BatchArgs& a, const BatchSmem& s
     block(j0, qa);
     if (j0 + 2 * JB < mp) load_q(j0 + 2 * JB, qa);
     if (two) block(j0 + JB, qb);
+  }
   }
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -850,7 +872,8 @@ __global__ void __launch_bounds__(BT, MINB) batched_nqp_kernel(BatchArgs a) {
     } else if (NB == 8 && BT == 256 && a.fast) {  // (not launched: see launch_batched)
       dmma_gemm_pass8<LD>(a, sm);
     } else {
-      gemm_pass<RPT, CG, ROWT, LD, ALNNLS_GEMM_JB>(a, sm, grp, trow);
+      gemm_pass<RPT, CG, ROWT, LD, ALNNLS_GEMM_JB, (BT == 128 && MINB == 2) ? ALNNLS_GEMM_QBUF : 2>(
+          a, sm, grp, trow);
     }
     __syncthreads();
 #ifdef ALNNLS_BATCH_PROF
