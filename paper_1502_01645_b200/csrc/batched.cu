@@ -1268,31 +1268,35 @@ __global__ void unscale_batched_kernel(const double* Y, int m, const double* sca
 // ascending i. One CTA owns kRC right-hand sides and walks all row tiles in order,
 // so each column's s is a single chain. A zero x_j adds a +-0 product, an exact
 // no-op on a chain that starts at +0 (it can never become -0), so the MACs are
-// branch-free. Each thread owns a 4 x 4 block of the tile; the next k-slab of A
-// and X is loaded into registers while the current one is multiplied.
+// branch-free. 128 threads, each an 8 x 4 block of the tile (rows 2 tx + 16 r + {0, 1},
+// columns 4 ty + c), its operands read as six 16-byte shared loads per k (four of A, two
+// of X) for 64 FP64 instructions: the 4 x 4 / 8-byte-load form needed as many LSU
+// cycles as FP64 cycles per k and ran at half the exact cap. The next k-slab of A and X
+// is loaded into registers while the current one is multiplied.
 constexpr int kRT = 64;   // rows per tile
 constexpr int kRC = 64;   // columns per CTA
 constexpr int kRK = 16;   // k slab
-__global__ void __launch_bounds__(256) residual_batched_kernel(const double* A, uint64_t lda, int d,
-                                                               int n, const double* X,
-                                                               const double* B, uint64_t ldb,
-                                                               int ncols,
-                                                               alnnls_column_result* res) {
+constexpr int kRThreads = 128;
+__global__ void __launch_bounds__(kRThreads) residual_batched_kernel(const double* A, uint64_t lda,
+                                                                     int d, int n, const double* X,
+                                                                     const double* B, uint64_t ldb,
+                                                                     int ncols,
+                                                                     alnnls_column_result* res) {
   // the slab buffers and the finished tile share one static buffer (< 48 KB)
-  __shared__ double sbuf[kRT * (kRC + 1)];
+  __shared__ __align__(16) double sbuf[kRT * (kRC + 1)];
   double(*As)[kRK][kRT] = reinterpret_cast<double(*)[kRK][kRT]>(sbuf);
   double(*Xs)[kRK][kRC] = reinterpret_cast<double(*)[kRK][kRC]>(sbuf + 2 * kRK * kRT);
   double(*Cs)[kRC + 1] = reinterpret_cast<double(*)[kRC + 1]>(sbuf);
   static_assert(2 * kRK * (kRT + kRC) <= kRT * (kRC + 1), "slab buffers fit the tile buffer");
   const int c0 = blockIdx.x * kRC;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // rows tx + 16 r, columns ty + 16 c
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
   const int nslab = (n + kRK - 1) / kRK;
   double ssum = 0.0;  // thread t < kRC: the running chain of column c0 + t
-  // slab loader: 4 A and 4 X elements per thread
-  auto fetch = [&](int i0, int k0, double (&ra)[4], double (&rx)[4]) {
+  constexpr int NF = kRT * kRK / kRThreads;  // slab loader: 8 A and 8 X elements per thread
+  auto fetch = [&](int i0, int k0, double (&ra)[NF], double (&rx)[NF]) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = threadIdx.x + 256 * u;
+    for (int u = 0; u < NF; ++u) {
+      const int e = threadIdx.x + kRThreads * u;
       const int kk = e / kRT, r = e % kRT;
       const int i = i0 + r, kcol = k0 + kk;
       ra[u] = (i < d && kcol < n) ? __ldg(A + (size_t)kcol * lda + i) : 0.0;
@@ -1301,21 +1305,21 @@ __global__ void __launch_bounds__(256) residual_batched_kernel(const double* A, 
       rx[u] = (col < ncols && kc2 < n) ? __ldg(X + (size_t)col * n + kc2) : 0.0;
     }
   };
-  auto stash = [&](int buf, const double (&ra)[4], const double (&rx)[4]) {
+  auto stash = [&](int buf, const double (&ra)[NF], const double (&rx)[NF]) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = threadIdx.x + 256 * u;
+    for (int u = 0; u < NF; ++u) {
+      const int e = threadIdx.x + kRThreads * u;
       As[buf][e / kRT][e % kRT] = ra[u];
       Xs[buf][e % kRK][e / kRK] = rx[u];
     }
   };
   for (int i0 = 0; i0 < d; i0 += kRT) {
-    double acc[4][4];
+    double acc[8][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < 8; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-    double ra[4], rx[4];
+    double ra[NF], rx[NF];
     fetch(i0, 0, ra, rx);
     stash(0, ra, rx);
     __syncthreads();
@@ -1324,13 +1328,21 @@ __global__ void __launch_bounds__(256) residual_batched_kernel(const double* A, 
       if (sl + 1 < nslab) fetch(i0, (sl + 1) * kRK, ra, rx);
 #pragma unroll
       for (int kk = 0; kk < kRK; ++kk) {
-        double av[4], xv[4];
+        double av[8], xv[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) av[r] = As[buf][kk][tx + 16 * r];
+        for (int r = 0; r < 4; ++r) {
+          const double2 t2 = *reinterpret_cast<const double2*>(&As[buf][kk][2 * tx + 16 * r]);
+          av[2 * r] = t2.x;
+          av[2 * r + 1] = t2.y;
+        }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) xv[c] = Xs[buf][kk][ty + 16 * c];
+        for (int c = 0; c < 4; c += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(&Xs[buf][kk][4 * ty + c]);
+          xv[c] = t2.x;
+          xv[c + 1] = t2.y;
+        }
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < 8; ++r)
 #pragma unroll
           for (int c = 0; c < 4; ++c) acc[r][c] = xmac(acc[r][c], av[r], xv[c]);
       }
@@ -1338,9 +1350,9 @@ __global__ void __launch_bounds__(256) residual_batched_kernel(const double* A, 
       __syncthreads();
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) Cs[tx + 16 * r][ty + 16 * c] = acc[r][c];
+      for (int c = 0; c < 4; ++c) Cs[2 * tx + 16 * (r >> 1) + (r & 1)][4 * ty + c] = acc[r][c];
     __syncthreads();
     if (threadIdx.x < kRC && c0 + (int)threadIdx.x < ncols) {
       const double* bcol = B + (size_t)(c0 + threadIdx.x) * ldb;
@@ -1471,8 +1483,8 @@ cudaError_t launch_residual_batched(const double* A, uint64_t lda, int d, int n,
                                     const double* B, uint64_t ldb, int ncols,
                                     alnnls_column_result* res, cudaStream_t stream) {
   if (ncols <= 0) return cudaSuccess;
-  residual_batched_kernel<<<(ncols + kRC - 1) / kRC, 256, 0, stream>>>(A, lda, d, n, X, B, ldb,
-                                                                         ncols, res);
+  residual_batched_kernel<<<(ncols + kRC - 1) / kRC, kRThreads, 0, stream>>>(A, lda, d, n, X, B,
+                                                                                ldb, ncols, res);
   return cudaGetLastError();
 }
 
