@@ -942,8 +942,10 @@ def run_ours_batched(args, ws, rank, local, dist):
     if args.profile == "fast":
         roof.update({"kernel": "batched_fast_kernel (warp-local per-column state machines over "
                                "DMMA m16n8k8 Q.V passes on fragment-ordered Q)",
-                     "bound": "tensor", "frac_of_exact_cap": None, "traffic": None,
-                     "traffic_note": "not captured for the FAST kernel"})
+                     "bound": "tensor", "frac_of_exact_cap": None,
+                     "traffic": (None if traffic_from_profiles("c4_nrhs8192", "batched_fast_kernel") is None
+                                 else int(traffic_from_profiles("c4_nrhs8192", "batched_fast_kernel")
+                                          * kc / 8192))})
     line = {
         "metric": C4_METRIC, "value": value, "unit": C4_UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
