@@ -1392,6 +1392,9 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
                      cudaMemcpyHostToDevice, s));
   double* Y = ENSURE(double, yb, (m ? m : 1) * nrhs);
   Resolved r{};
+  bool wide = false;
+  std::vector<alnnls_column_result> wres;
+  double wide_loop_s = 0.0;
   double* Qc = nullptr;
   double* QB = nullptr;
   int* counter = nullptr;
@@ -1399,10 +1402,16 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
   const bool dmma_q = m > 0 && cfg->profile == ALNNLS_PROFILE_FAST;
   if (m > 0) {
     if ((rc = resolve(ctx, cfg, m, &r))) return rc;  // solve_nqp validates its config
-    if (batched_cols_per_cta((int)m) == 0)
-      return set_err(ctx, ALNNLS_EINVAL, "solve_nnls_batched: n > 1024 not supported");
-    Qc = ENSURE(double, H, m * m);
-    CK(launch_from_blocked(static_cast<double*>(ctx->Q.p), (int)m, (int)ctx->qR, Qc, m, s));
+    // m > 1024 does not fit the batched kernel's shared-memory state: those columns go one
+    // at a time through the single-RHS device loop on the shared blocked Q (same per-column
+    // results as solve_nnls; any m that entry takes)
+    wide = batched_cols_per_cta((int)m) == 0;
+    if (!wide) {
+      Qc = ENSURE(double, H, m * m);
+      CK(launch_from_blocked(static_cast<double*>(ctx->Q.p), (int)m, (int)ctx->qR, Qc, m, s));
+    } else {
+      wres.resize(nrhs);
+    }
     QB = ENSURE(double, qb, m * nrhs);
     counter = ENSURE(int, bcnt, kHostChunks);
     CK(cudaMemsetAsync(counter, 0, sizeof(int) * kHostChunks, s));
@@ -1430,7 +1439,7 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
       CK(cudaStreamWaitEvent(s, ctx->up[c], 0));
       CK(launch_check_finite(dB + c0 * ldb, d, cnt, ldb, bflag, s));
     }
-    cudaStream_t ts = nch > 1 ? ctx->bstream[c & 1] : s;
+    cudaStream_t ts = nch > 1 && !wide ? ctx->bstream[c & 1] : s;
     if (m > 0) {
       SetupArgs sa{};
       sa.A = dA;
@@ -1461,7 +1470,33 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
       CK(cudaEventRecord(ctx->bev[2 * c], s));
       CK(cudaStreamWaitEvent(ts, ctx->bev[2 * c], 0));
     }
-    if (m > 0) {
+    if (m > 0 && wide) {
+      double* qv = ENSURE(double, q, vec_pad(m));
+      for (uint64_t j = c0; j < c0 + cnt; ++j) {
+        CK(cudaMemcpyAsync(qv, QB + j * m, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+        alnnls_summary cs{};
+        rc = run_nqp(ctx, m, r, cfg, nullptr, &cs, 0, /*defer=*/true);
+        if (rc) return rc;
+        CK(launch_copy_parity(Y + j * m, static_cast<double*>(ctx->x.p),
+                              static_cast<double*>(ctx->x_alt.p),
+                              static_cast<LoopCtrl*>(ctx->ctrl.p), (int)m, s));
+        CK(cudaStreamSynchronize(s));
+        rc = collect_nqp(ctx, &cs);
+        if (rc && rc != ALNNLS_ENUMERIC) return rc;  // a NumericFailure column is a result
+        wide_loop_s += cs.t_loop_s;
+        alnnls_column_result& w = wres[j];
+        w.termination = cs.numeric_failure ? 0 : cs.termination;
+        w.numeric_failure = cs.numeric_failure;
+        w.iterations = cs.iterations;
+        w.residual_sq = 0.0;
+        w.f_final = cs.f_final;
+        w.gbs_final = cs.gbs_final;
+        w.multiplies_total = cs.multiplies_total;
+      }
+      CK(cudaMemcpyAsync(dres + c0, wres.data() + c0, sizeof(alnnls_column_result) * cnt,
+                         cudaMemcpyHostToDevice, s));
+      CK(cudaEventRecord(ctx->ev[2], s));  // run_nqp re-records ev[2] / ev[3] per column
+    } else if (m > 0) {
       BatchArgs bc = ba;
       bc.QB = QB + c0 * m;
       bc.ncols = (int)cnt;
@@ -1504,7 +1539,7 @@ int run_batched(alnnls_ctx* ctx, uint64_t d, uint64_t n, const double* dA, uint6
   cudaEventElapsedTime(&t34, ctx->ev[3], ctx->ev[4]);
   cudaEventElapsedTime(&t04, ctx->ev[0], ctx->ev[4]);
   sum.t_setup_s = t01 * 1e-3;
-  sum.t_loop_s = t23 * 1e-3;
+  sum.t_loop_s = wide ? wide_loop_s : t23 * 1e-3;
   sum.t_finish_s = t34 * 1e-3;
   sum.t_total_s = t04 * 1e-3;
   sum.n = n;

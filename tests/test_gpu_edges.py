@@ -37,11 +37,24 @@ def test_batched_wide_problems_bitwise(solver, n):
         assert same_bits(X[:, j], r["x"]), j
 
 
-def test_batched_too_wide_is_rejected(solver):
-    A = np.random.default_rng(1).uniform(size=(1100, 1030))
-    B = np.asfortranarray(A[:, :2] @ np.ones((2, 3)))
-    with pytest.raises(Exception):
-        solver.solve_nnls_batched(A, B, SolverConfig(max_iters=5))
+def test_batched_wider_than_the_batched_kernel_bitwise(solver):
+    """m > 1024 does not fit the batched kernel's per-column shared-memory state: the
+    columns then run one by one through the single-RHS device loop on the shared Q
+    (capi.cu run_batched) — the reference takes any size (nnls.hpp:129-144)."""
+    rng = np.random.default_rng(1)
+    n, d = 1030, 1100
+    A = rng.uniform(size=(d, n))
+    H = np.where(rng.uniform(size=(n, 3)) < 0.5, 0.0, rng.uniform(size=(n, 3)))
+    B = np.asfortranarray(A @ H + 1e-3 * rng.standard_normal((d, 3)))
+    cfg = SolverConfig(epsilon=1e-8, max_iters=40, stall_window=10**9)
+    X, cols, _ = solver.solve_nnls_batched(A, B, cfg)
+    for j, r in enumerate(ref_columns(A, B, cfg)):
+        assert cols[j]["iterations"] == r["iterations"], j
+        assert cols[j]["termination"] == r["termination"], j
+        assert same_bits(X[:, j], r["x"]), j
+        assert same_bits([cols[j]["residual_sq"]], [r["residual_sq"]]), j
+        single = solver.solve_nnls(A, B[:, j].copy(), cfg)
+        assert same_bits(X[:, j], single.x), j
 
 
 def test_batched_with_dropped_columns(solver):
