@@ -501,7 +501,7 @@ def run_ours(args, ws, rank, local, dist):
                  "algorithmic": f"8 B x reference multiply count = {8 * mults} B per launch",
                  "traffic": traffic_from_profiles(args.workload, loop_kernel)}
     roof_setup = {"kernel": "setup: colchain + syrk_exact + rescale epilogue",
-                  "bound": "fp64", "achieved": setup_tf, "peak": FP64_PEAK_TFLOPS,
+                  "bound": "tensor", "pipe": "fp64 SIMT (exact DMUL + DADD chains; the peak is the fp64 tensor peak)", "achieved": setup_tf, "peak": FP64_PEAK_TFLOPS,
                   "unit": "TFLOP/s", "frac": setup_tf / FP64_PEAK_TFLOPS,
                   "frac_of_exact_cap": setup_tf / FP64_EXACT_CAP_TFLOPS,
                   "peak_source": "measured (tools/microbench/fp64_probe.cu, DMMA)",
@@ -510,7 +510,7 @@ def run_ours(args, ws, rank, local, dist):
     if args.profile == "fast":
         roof_loop = fast_loop_roofline(args.workload, mults, per_loop, hbm, hbm_kind)
         roof_setup.update({"kernel": "setup: syrk_dmma_kernel (fp64 tensor cores) + rescale epilogue",
-                           "frac_of_exact_cap": None,
+                           "pipe": "fp64 DMMA", "frac_of_exact_cap": None,
                            "traffic": traffic_from_profiles(args.workload, "syrk_dmma_kernel")})
     dominant = roof_loop if per_loop >= per_setup else roof_setup
     line = {
@@ -767,7 +767,7 @@ def run_ours_allreduce(args, ws, rank, local, dist):
         "roofline": {"kernel": "partial Gram per rank (" +
                      ("syrk_dmma_kernel, fp64 tensor cores" if args.profile == "fast"
                       else "exact chain SYRK") + ") + A^T b chains",
-                     "bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "bound": "tensor", "pipe": "fp64 DMMA", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": ach / FP64_PEAK_TFLOPS,
                      "peak_source": "measured (tools/microbench/fp64_probe.cu, DMMA)",
                      "algorithmic": f"rows*n*(n+1) + 2*rows*n = {flops_rank} flop per rank",
@@ -928,7 +928,7 @@ def run_ours_batched(args, ws, rank, local, dist):
     per_loop = t_loop / args.steps
     loop_tf = 2.0 * mults / per_loop / 1e12 if per_loop > 0 else 0.0
     roof = {"kernel": "batched_nqp_kernel (per-column state machines over exact chain GEMM passes)",
-            "bound": "fp64", "achieved": loop_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "bound": "tensor", "pipe": "fp64 SIMT (exact DMUL + DADD chains; the peak is the fp64 tensor peak)", "achieved": loop_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": loop_tf / FP64_PEAK_TFLOPS, "frac_of_exact_cap": loop_tf / FP64_EXACT_CAP_TFLOPS,
             "peak_source": "measured (tools/microbench/fp64_probe.cu, DMMA)",
             "algorithmic": (f"2 flop x reference multiply count (masked GEMVs) = {2 * mults} "
@@ -942,7 +942,7 @@ def run_ours_batched(args, ws, rank, local, dist):
     if args.profile == "fast":
         roof.update({"kernel": "batched_fast_kernel (warp-local per-column state machines over "
                                "DMMA m16n8k8 Q.V passes on fragment-ordered Q)",
-                     "bound": "tensor", "frac_of_exact_cap": None,
+                     "bound": "tensor", "pipe": "fp64 DMMA", "frac_of_exact_cap": None,
                      "traffic": (None if traffic_from_profiles("c4_nrhs8192", "batched_fast_kernel") is None
                                  else int(traffic_from_profiles("c4_nrhs8192", "batched_fast_kernel")
                                           * kc / 8192))})
